@@ -1,0 +1,175 @@
+/*
+ * ssg_b200.h -- C ABI of the B200-native skew-Gaussian rasterizer
+ * (libssg_b200.so, sm_100a).
+ *
+ * Plain C: device pointers, sizes, and an opaque CUDA stream (void*, a
+ * cudaStream_t).  No allocation happens inside these calls except where a
+ * function says so; the caller owns every buffer (two-phase size queries
+ * for the temporary storage).  Every call is asynchronous on `stream` and
+ * returns an ssg_status; errors are never thrown across the ABI.
+ *
+ * The entry points replace the reference's hot path
+ * (reference: pkg/src/skewsplat/...):
+ *   ssg_preprocess_forward   projection.py:151-235 project_scene (+ tiles.py:43-57
+ *                            per-primitive tile rect and count)
+ *   ssg_bin_prepare          tiles.py:58-59 counts/offsets, ordering key of tiles.py:72
+ *   ssg_bin_finish           tiles.py:59-79 duplicate + lexsort + searchsorted ranges
+ *   ssg_blend_forward        raster/_core.pyx:169-200 forward_tiles (plugin slot of
+ *                            raster/backend.py:41-43)
+ *   ssg_blend_backward       raster/_core.pyx:315-343 backward_tiles fused with the
+ *                            per-primitive slot reduction of raster/backward.py:70-73
+ *   ssg_preprocess_backward  projection.py:255-379 projection_backward
+ * The Python host layer (paper_2605_18334_b200.raster) keeps the reference's
+ * render_forward / render_backward signatures (raster/forward.py:37-38,
+ * raster/backward.py:77-79) on top of these.
+ */
+#ifndef SSG_B200_H
+#define SSG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SSG_OK = 0,
+    SSG_ERR_INVALID_ARGUMENT = 1, /* -> ValueError */
+    SSG_ERR_DIM_OVERFLOW = 2,     /* -> ValueError("image dimension overflow"), forward.py:40-41 */
+    SSG_ERR_CAPACITY = 3,         /* caller buffer too small (instances / temp storage) */
+    SSG_ERR_CUDA = 4              /* a CUDA launch or runtime error; see ssg_last_error() */
+} ssg_status;
+
+#define SSG_TILE 16               /* raster/tiles.py:16 */
+#define SSG_MAX_IMAGE_DIM 65535   /* raster/forward.py:21 */
+
+/* Scene on the device (reference Scene, scene.py:99-121).  Geometry that
+ * decides tile membership and depth order stays fp64 so the tile lists are
+ * bit-exact; appearance is fp32. */
+typedef struct ssg_scene {
+    int64_t n;
+    int32_t sh_degree;          /* 0..3 */
+    int32_t sh_coeffs;          /* K = (degree+1)^2; sh row stride is 3*K floats */
+    const double *mu;           /* (n,3) */
+    const double *log_scale;    /* (n,3) */
+    const double *rot;          /* (n,4) quaternion w,x,y,z (normalised in use) */
+    const float *sh;            /* (n,K,3) coefficient-major, then RGB */
+    const float *opacity_logits;/* (n,2) */
+    const float *beta;          /* (n,3) */
+    const float *dir;           /* (n,3) */
+} ssg_scene;
+
+/* Camera, already in OpenCV convention (camera.py:53-75, projection.py:152-167).
+ * R and t are the host's fp64 world_to_cam result; they feed the depth bits. */
+typedef struct ssg_camera {
+    double R[9];                /* R_w2c, row-major */
+    double t[3];                /* -R_w2c @ eye */
+    double campos[3];           /* c2w[:3,3] */
+    double fx, fy, cx, cy;
+    double tan_fovx, tan_fovy;
+    double near_plane;
+    double s;                   /* screen dilation */
+    int32_t width, height;
+} ssg_camera;
+
+/* Per-primitive screen record consumed by the blend kernels (64 bytes,
+ * 16-byte aligned): mean in fp64 so blend kernels can form tile-local
+ * offsets exactly; the rest fp32. */
+typedef struct ssg_splat {
+    double mean_x, mean_y;
+    float conic_a, conic_b, conic_c;
+    float skew_x, skew_y;
+    float o1, o2;
+    float r, g, b;
+    uint32_t pad0, pad1;
+} ssg_splat;
+
+/* Per-primitive buffers written by ssg_preprocess_forward. */
+typedef struct ssg_prim_buffers {
+    ssg_splat *splat;           /* (n) */
+    uint64_t *depth_key;        /* (n) order-preserving bits of the fp64 depth */
+    uint32_t *tile_count;       /* (n) tiles covered (0 if invalid) */
+    uint64_t *tile_rect;        /* (n) x0 | x1<<16 | y0<<32 | y1<<48 */
+    uint8_t *valid;             /* (n) */
+    double *depth;              /* (n) camera-space z (projection.py:161) */
+    double *radius;             /* (n) */
+    int32_t *n_skew_fallback;   /* (1) accumulated with atomics (zeroed by the call) */
+} ssg_prim_buffers;
+
+/* Binning buffers.  depth_order/rank_offset are (n); inst_* are (capacity). */
+typedef struct ssg_bin_buffers {
+    uint32_t *depth_order;      /* (n) primitive ids sorted by (depth, id) */
+    uint64_t *rank_offset;      /* (n+1) exclusive scan of counts in depth order */
+    int64_t *n_instances;       /* (1) device copy of M */
+    int64_t capacity;           /* allocated instances */
+    uint32_t *inst_prim;        /* (capacity) sorted primitive id per instance */
+    uint16_t *inst_tile;        /* (capacity) sorted tile id per instance */
+    uint32_t *inst_prim_tmp;    /* (capacity) */
+    uint16_t *inst_tile_tmp;    /* (capacity) */
+    int32_t *ranges;            /* (n_tiles, 2) half-open [start, end) */
+    void *temp;                 /* temporary storage for the sorts */
+    size_t temp_bytes;
+} ssg_bin_buffers;
+
+/* Frame outputs of the forward blend (raster/forward.py:24-34). */
+typedef struct ssg_frame_buffers {
+    float *color;               /* (H,W,3) */
+    float *final_T;             /* (H,W) */
+    int32_t *n_contrib;         /* (H,W) */
+    int32_t *last_idx;          /* (H,W) global sorted index or -1 */
+} ssg_frame_buffers;
+
+/* Gradient outputs (raster/backward.py:28-39).  d_beta == d_dir
+ * (projection.py:365-366) so one d_eta array serves both. */
+typedef struct ssg_grad_buffers {
+    float *screen;              /* (n,12) screen-space sums: d_mean2d(2) d_conic(3)
+                                   d_skew2d(2) d_opair(2) d_color(3) (raster/_cpu.py:88-93) */
+    float *d_mu;                /* (n,3) */
+    float *d_log_scale;         /* (n,3) */
+    float *d_rot;               /* (n,4) */
+    float *d_sh;                /* (n,K,3) */
+    float *d_opacity_logits;    /* (n,2) */
+    float *d_eta;               /* (n,3) */
+    float *g_uv;                /* (n) */
+    float *g_z;                 /* (n) */
+} ssg_grad_buffers;
+
+/* ---- queries ---------------------------------------------------------- */
+int ssg_abi_version(void);
+const char *ssg_last_error(void);
+void ssg_grid_dims(int32_t width, int32_t height, int32_t *tiles_x, int32_t *tiles_y);
+/* temporary storage needed by ssg_bin_prepare / ssg_bin_finish */
+int ssg_bin_temp_bytes(int64_t n, int64_t capacity, int32_t n_tiles, size_t *bytes);
+
+/* ---- forward ------------------------------------------------------------ */
+int ssg_preprocess_forward(const ssg_scene *scene, const ssg_camera *cam,
+                           const ssg_prim_buffers *out, void *stream);
+/* depth sort, counts in depth order, exclusive scan; writes bins->n_instances */
+int ssg_bin_prepare(int64_t n, const ssg_prim_buffers *prim, const ssg_bin_buffers *bins,
+                    void *stream);
+/* bin_arrays from caller screen arrays (tiles.py:43-57): fills tile_count,
+ * tile_rect and depth_key of `out` (the other fields are not touched) */
+int ssg_bin_rects(int64_t n, const double *mean2d, const double *radius, const double *depth,
+                  const uint8_t *valid, int32_t width, int32_t height,
+                  const ssg_prim_buffers *out, void *stream);
+/* duplicate, stable sort by tile, ranges; m = value of *bins->n_instances */
+int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t height,
+                   const ssg_prim_buffers *prim, const ssg_bin_buffers *bins, void *stream);
+int ssg_blend_forward(int64_t m, int32_t width, int32_t height, const float background[3],
+                      const ssg_splat *splat, const ssg_bin_buffers *bins,
+                      const ssg_frame_buffers *frame, void *stream);
+
+/* ---- backward ----------------------------------------------------------- */
+/* accumulates (n,12) screen gradients into grads->screen (zeroed by the call) */
+int ssg_blend_backward(int64_t n, int64_t m, int32_t width, int32_t height,
+                       const float background[3], const ssg_splat *splat,
+                       const ssg_bin_buffers *bins, const ssg_frame_buffers *frame,
+                       const float *dL_dpixels, const ssg_grad_buffers *grads, void *stream);
+int ssg_preprocess_backward(const ssg_scene *scene, const ssg_camera *cam,
+                            const ssg_grad_buffers *grads, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSG_B200_H */

@@ -1,0 +1,120 @@
+"""ctypes binding of libssg_b200.so (the C ABI in include/ssg_b200.h).
+
+The structures below mirror the header field for field.  Loading fails
+loudly: there is no CPU fallback anywhere in this package.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libssg_b200.so")
+
+SSG_OK = 0
+SSG_ERR_INVALID_ARGUMENT = 1
+SSG_ERR_DIM_OVERFLOW = 2
+SSG_ERR_CAPACITY = 3
+SSG_ERR_CUDA = 4
+
+EXPORTS = ("ssg_abi_version", "ssg_last_error", "ssg_grid_dims", "ssg_bin_temp_bytes",
+           "ssg_preprocess_forward", "ssg_bin_rects", "ssg_bin_prepare", "ssg_bin_finish", "ssg_blend_forward",
+           "ssg_blend_backward", "ssg_preprocess_backward")
+
+_vp = ctypes.c_void_p
+
+
+class SsgScene(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("sh_degree", ctypes.c_int32),
+                ("sh_coeffs", ctypes.c_int32), ("mu", _vp), ("log_scale", _vp), ("rot", _vp),
+                ("sh", _vp), ("opacity_logits", _vp), ("beta", _vp), ("dir", _vp)]
+
+
+class SsgCamera(ctypes.Structure):
+    _fields_ = [("R", ctypes.c_double * 9), ("t", ctypes.c_double * 3),
+                ("campos", ctypes.c_double * 3), ("fx", ctypes.c_double),
+                ("fy", ctypes.c_double), ("cx", ctypes.c_double), ("cy", ctypes.c_double),
+                ("tan_fovx", ctypes.c_double), ("tan_fovy", ctypes.c_double),
+                ("near_plane", ctypes.c_double), ("s", ctypes.c_double),
+                ("width", ctypes.c_int32), ("height", ctypes.c_int32)]
+
+
+class SsgPrimBuffers(ctypes.Structure):
+    _fields_ = [("splat", _vp), ("depth_key", _vp), ("tile_count", _vp), ("tile_rect", _vp),
+                ("valid", _vp), ("depth", _vp), ("radius", _vp), ("n_skew_fallback", _vp)]
+
+
+class SsgBinBuffers(ctypes.Structure):
+    _fields_ = [("depth_order", _vp), ("rank_offset", _vp), ("n_instances", _vp),
+                ("capacity", ctypes.c_int64), ("inst_prim", _vp), ("inst_tile", _vp),
+                ("inst_prim_tmp", _vp), ("inst_tile_tmp", _vp), ("ranges", _vp),
+                ("temp", _vp), ("temp_bytes", ctypes.c_size_t)]
+
+
+class SsgFrameBuffers(ctypes.Structure):
+    _fields_ = [("color", _vp), ("final_T", _vp), ("n_contrib", _vp), ("last_idx", _vp)]
+
+
+class SsgGradBuffers(ctypes.Structure):
+    _fields_ = [("screen", _vp), ("d_mu", _vp), ("d_log_scale", _vp), ("d_rot", _vp),
+                ("d_sh", _vp), ("d_opacity_logits", _vp), ("d_eta", _vp), ("g_uv", _vp),
+                ("g_z", _vp)]
+
+
+SPLAT_BYTES = 64
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def lib():
+    """Load libssg_b200.so; raise if it is missing (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeError(
+            f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the sm_100a extension is the only implementation)")
+    L = ctypes.CDLL(LIB_PATH)
+    L.ssg_last_error.restype = ctypes.c_char_p
+    L.ssg_abi_version.restype = ctypes.c_int
+    P = ctypes.POINTER
+    L.ssg_grid_dims.argtypes = [ctypes.c_int32, ctypes.c_int32, P(ctypes.c_int32), P(ctypes.c_int32)]
+    L.ssg_bin_temp_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                     P(ctypes.c_size_t)]
+    L.ssg_preprocess_forward.argtypes = [P(SsgScene), P(SsgCamera), P(SsgPrimBuffers), _vp]
+    L.ssg_bin_rects.argtypes = [ctypes.c_int64, _vp, _vp, _vp, _vp, ctypes.c_int32,
+                                ctypes.c_int32, P(SsgPrimBuffers), _vp]
+    L.ssg_bin_prepare.argtypes = [ctypes.c_int64, P(SsgPrimBuffers), P(SsgBinBuffers), _vp]
+    L.ssg_bin_finish.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                 P(SsgPrimBuffers), P(SsgBinBuffers), _vp]
+    L.ssg_blend_forward.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                    P(ctypes.c_float), _vp, P(SsgBinBuffers),
+                                    P(SsgFrameBuffers), _vp]
+    L.ssg_blend_backward.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                     ctypes.c_int32, P(ctypes.c_float), _vp, P(SsgBinBuffers),
+                                     P(SsgFrameBuffers), _vp, P(SsgGradBuffers), _vp]
+    L.ssg_preprocess_backward.argtypes = [P(SsgScene), P(SsgCamera), P(SsgGradBuffers), _vp]
+    if L.ssg_abi_version() != 1:
+        raise NativeError("libssg_b200.so ABI version mismatch; rebuild")
+    _lib = L
+    return L
+
+
+def check(status: int, what: str):
+    """Map an ssg_status to the reference's exception types."""
+    if status == SSG_OK:
+        return
+    msg = lib().ssg_last_error().decode(errors="replace")
+    if status == SSG_ERR_DIM_OVERFLOW:
+        raise ValueError("image dimension overflow")
+    if status == SSG_ERR_INVALID_ARGUMENT:
+        raise ValueError(f"{what}: invalid argument")
+    if status == SSG_ERR_CAPACITY:
+        raise NativeError(f"{what}: buffer capacity exceeded")
+    raise NativeError(f"{what}: CUDA error: {msg}")

@@ -1,0 +1,287 @@
+// preprocess_bwd.cu -- K8: chain screen-space gradients back to primitive
+// parameters, plus the densification statistics g_uv and g_z.
+//
+// Reference: projection.py:255-379 (projection_backward), with
+// _project_eta_vjp projection.py:126-148, _quat_backward projection.py:382-420
+// and sh_basis_grad sh.py:57-103.  Like the reference's backward, the
+// forward geometry is recomputed (not cached) from the scene; one thread per
+// primitive, fp64 registers, fp32 outputs.
+#include "ssg_common.cuh"
+
+namespace ssg {
+
+__device__ __forceinline__ void sh_basis_grad(int deg, double x, double y, double z, double (*g)[3]) {
+    // sh.py:57-103 (entries not written are zero)
+#pragma unroll
+    for (int k = 0; k < 16; k++) g[k][0] = g[k][1] = g[k][2] = 0.0;
+    if (deg < 1) return;
+    const double C1 = 0.4886025119029199;
+    g[1][1] = -C1;
+    g[2][2] = C1;
+    g[3][0] = -C1;
+    if (deg < 2) return;
+    const double C20 = 1.0925484305920792, C21 = -1.0925484305920792, C22 = 0.31539156525252005,
+                 C23 = -1.0925484305920792, C24 = 0.5462742152960396;
+    double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    g[4][0] = C20 * y; g[4][1] = C20 * x;
+    g[5][1] = C21 * z; g[5][2] = C21 * y;
+    g[6][0] = C22 * (-2.0 * x); g[6][1] = C22 * (-2.0 * y); g[6][2] = C22 * (4.0 * z);
+    g[7][0] = C23 * z; g[7][2] = C23 * x;
+    g[8][0] = C24 * (2.0 * x); g[8][1] = C24 * (-2.0 * y);
+    if (deg < 3) return;
+    const double C30 = -0.5900435899266435, C31 = 2.890611442640554, C32 = -0.4570457994644658,
+                 C33 = 0.3731763325901154, C34 = -0.4570457994644658, C35 = 1.445305721320277,
+                 C36 = -0.5900435899266435;
+    g[9][0] = C30 * 6.0 * xy; g[9][1] = C30 * (3.0 * xx - 3.0 * yy);
+    g[10][0] = C31 * yz; g[10][1] = C31 * xz; g[10][2] = C31 * xy;
+    g[11][0] = C32 * (-2.0 * xy); g[11][1] = C32 * (4.0 * zz - xx - 3.0 * yy); g[11][2] = C32 * (8.0 * yz);
+    g[12][0] = C33 * (-6.0 * xz); g[12][1] = C33 * (-6.0 * yz); g[12][2] = C33 * (6.0 * zz - 3.0 * xx - 3.0 * yy);
+    g[13][0] = C34 * (4.0 * zz - 3.0 * xx - yy); g[13][1] = C34 * (-2.0 * xy); g[13][2] = C34 * (8.0 * xz);
+    g[14][0] = C35 * (2.0 * xz); g[14][1] = C35 * (-2.0 * yz); g[14][2] = C35 * (xx - yy);
+    g[15][0] = C36 * (3.0 * xx - 3.0 * yy); g[15][1] = C36 * (-6.0 * xy);
+}
+
+template <int DEG>
+__global__ void __launch_bounds__(128)
+k_preprocess_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
+    constexpr int K = (DEG + 1) * (DEG + 1);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= sc.n) return;
+    double mu[3], ls[3], q4[4], eta[3];
+    float logit[2];
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+        mu[j] = sc.mu[3 * i + j];
+        ls[j] = sc.log_scale[3 * i + j];
+        eta[j] = (double)sc.beta[3 * i + j] + (double)sc.dir[3 * i + j];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) q4[j] = sc.rot[4 * i + j];
+    logit[0] = sc.opacity_logits[2 * i];
+    logit[1] = sc.opacity_logits[2 * i + 1];
+    Proj P;
+    project_geometry(cam, mu, ls, q4, logit, eta, P);
+
+    float *dsh = gr.d_sh + (size_t)i * 3 * K;
+    if (!P.valid) {  // zero_invalid, projection.py:368-379; g_z -> 0 (:349)
+#pragma unroll
+        for (int j = 0; j < 3; j++) gr.d_mu[3 * i + j] = gr.d_log_scale[3 * i + j] = gr.d_eta[3 * i + j] = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 4; j++) gr.d_rot[4 * i + j] = 0.0f;
+        for (int j = 0; j < 3 * K; j++) dsh[j] = 0.0f;
+        gr.d_opacity_logits[2 * i] = gr.d_opacity_logits[2 * i + 1] = 0.0f;
+        gr.g_uv[i] = 0.0f;
+        gr.g_z[i] = 0.0f;
+        return;
+    }
+    const float4 *sg4 = reinterpret_cast<const float4 *>(gr.screen + 12 * i);
+    const float4 s0 = sg4[0], s1 = sg4[1], s2 = sg4[2];
+    const double dm0 = s0.x, dm1 = s0.y;
+    const double dc0 = s0.z, dc1 = s0.w, dc2 = s1.x;
+    const double dsk0 = s1.y, dsk1 = s1.z;
+    const double dop0 = s1.w, dop1 = s2.x;
+    const double dcol[3] = {s2.y, s2.z, s2.w};
+    const double fx = cam.fx, fy = cam.fy, tz = P.tz;
+    const double *R = cam.R;
+
+    // opacity pair (projection.py:278-281)
+    gr.d_opacity_logits[2 * i] = (float)(dop0 * P.comp * P.sig[0] * (1.0 - P.sig[0]));
+    gr.d_opacity_logits[2 * i + 1] = (float)(dop1 * P.comp * P.sig[1] * (1.0 - P.sig[1]));
+    const double d_comp = dop0 * P.sig[0] + dop1 * P.sig[1];
+
+    // conic -> cov_dil: G_dil = -C Gc C (:283-289)
+    const double *C = P.inv_dil;
+    const double Gc[4] = {dc0, 0.5 * dc1, 0.5 * dc1, dc2};
+    double CG[4], Gdil[4], Graw[4];
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 2; b++) CG[2 * a + b] = C[2 * a] * Gc[b] + C[2 * a + 1] * Gc[2 + b];
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 2; b++) Gdil[2 * a + b] = -(CG[2 * a] * C[b] + CG[2 * a + 1] * C[2 + b]);
+    // comp = sqrt(det_raw / det_dil) (:291-295)
+    const double half_comp = P.det_raw > 0.0 ? 0.5 * P.comp * d_comp : 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        Graw[j] = half_comp * P.inv_raw[j];
+        Gdil[j] -= half_comp * P.inv_dil[j];
+    }
+    // skew VJP (:297-303, projection.py:126-148)
+    double g0 = P.clip0 ? 0.0 : dsk0, g1 = P.clip1 ? 0.0 : dsk1;
+    if (P.fallback) g0 = g1 = 0.0;
+    const double r3 = P.r * P.r * P.r;
+    const double s_q = -(g0 * P.v[0] + g1 * P.v[1]) / (2.0 * r3);
+    const double gv0 = g0 / P.r, gv1 = g1 / P.r;
+    double gM[4];
+    gM[0] = gv0 * P.u[0] - s_q * (P.u[0] * P.u[0]);
+    gM[1] = gv0 * P.u[1] - s_q * (P.u[0] * P.u[1]);
+    gM[2] = gv1 * P.u[0] - s_q * (P.u[1] * P.u[0]);
+    gM[3] = gv1 * P.u[1] - s_q * (P.u[1] * P.u[1]);
+    const double *Mi = P.inv_raw;
+    const double gu0 = (Mi[0] * gv0 + Mi[1] * gv1) - 2.0 * s_q * P.v[0];
+    const double gu1 = (Mi[2] * gv0 + Mi[3] * gv1) - 2.0 * s_q * P.v[1];
+    double MgM[4];
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 2; b++) MgM[2 * a + b] = Mi[2 * a] * gM[b] + Mi[2 * a + 1] * gM[2 + b];
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 2; b++) Graw[2 * a + b] += -(MgM[2 * a] * Mi[b] + MgM[2 * a + 1] * Mi[2 + b]);
+    double gw[3];
+#pragma unroll
+    for (int b = 0; b < 3; b++) gw[b] = P.T[b] * gu0 + P.T[3 + b] * gu1;
+    double geta[3];
+#pragma unroll
+    for (int b = 0; b < 3; b++)
+        geta[b] = (P.Sig[b] * gw[0] + P.Sig[3 + b] * gw[1] + P.Sig[6 + b] * gw[2]) + 2.0 * s_q * P.w[b];
+#pragma unroll
+    for (int j = 0; j < 4; j++) Graw[j] += Gdil[j];  // (:306)
+
+    // cov_raw = T Sig T^T (:308-312)
+    const double Gsym[4] = {2.0 * Graw[0], Graw[1] + Graw[2], Graw[2] + Graw[1], 2.0 * Graw[3]};
+    double TS[6], GT[6], GrT[6], GSig[9];
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++)
+            TS[3 * a + b] = P.T[3 * a] * P.Sig[b] + P.T[3 * a + 1] * P.Sig[3 + b] + P.T[3 * a + 2] * P.Sig[6 + b];
+    const double gu[2] = {gu0, gu1};
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++) GT[3 * a + b] = Gsym[2 * a] * TS[b] + Gsym[2 * a + 1] * TS[3 + b] + gu[a] * P.w[b];
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++) GrT[3 * a + b] = Graw[2 * a] * P.T[b] + Graw[2 * a + 1] * P.T[3 + b];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++)
+            GSig[3 * a + b] = P.T[a] * GrT[b] + P.T[3 + a] * GrT[3 + b] + (gw[a] * eta[b] + s_q * (eta[a] * eta[b]));
+    // T = J R_w2c -> G_J = G_T R^T (:315)
+    double GJ[6];
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int k = 0; k < 3; k++) GJ[3 * a + k] = GT[3 * a] * R[3 * k] + GT[3 * a + 1] * R[3 * k + 1] + GT[3 * a + 2] * R[3 * k + 2];
+    // Sigma = (Rq S)(Rq S)^T (:317-325)
+    double GM[9];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < 3; k++) acc += (GSig[3 * a + k] + GSig[3 * k + a]) * (P.Rq[3 * k + b] * P.scale[b]);
+            GM[3 * a + b] = acc;
+        }
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+        double gs = P.Rq[j] * GM[j] + P.Rq[3 + j] * GM[3 + j] + P.Rq[6 + j] * GM[6 + j];
+        gr.d_log_scale[3 * i + j] = (float)(gs * P.scale[j]);
+    }
+    // _quat_backward (projection.py:382-420) with G_R = G_M * scale
+    {
+        const double w = P.qn[0], x = P.qn[1], y = P.qn[2], z = P.qn[3];
+        const double dRw[9] = {0, -z, y, z, 0, -x, -y, x, 0};
+        const double dRx[9] = {0, y, z, y, -2 * x, -w, z, w, -2 * x};
+        const double dRy[9] = {-2 * y, x, w, x, 0, z, -w, z, -2 * y};
+        const double dRz[9] = {-2 * z, -w, x, w, -2 * z, y, x, y, 0};
+        double d[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int j = 0; j < 9; j++) {
+            const double GR = GM[j] * P.scale[j % 3];
+            d[0] += GR * 2.0 * dRw[j];
+            d[1] += GR * 2.0 * dRx[j];
+            d[2] += GR * 2.0 * dRy[j];
+            d[3] += GR * 2.0 * dRz[j];
+        }
+        const double inner = P.qn[0] * d[0] + P.qn[1] * d[1] + P.qn[2] * d[2] + P.qn[3] * d[3];
+#pragma unroll
+        for (int j = 0; j < 4; j++) gr.d_rot[4 * i + j] = (float)((d[j] - P.qn[j] * inner) / P.qnorm);
+    }
+    // J -> camera-space position (:327-347)
+    const double tz2 = tz * tz, tz3 = tz * tz * tz;
+    double dt0 = P.gate0 * (-fx / tz2) * GJ[2];
+    double dt1 = P.gate1 * (-fy / tz2) * GJ[5];
+    const double txc = -P.J02 * tz2 / fx, tyc = -P.J12 * tz2 / fy;
+    const double kx = P.gate0 > 0 ? 2.0 : 1.0, ky = P.gate1 > 0 ? 2.0 : 1.0;
+    double dt2 = (-fx / tz2) * GJ[0] + (-fy / tz2) * GJ[4];
+    dt2 += kx * fx * txc / tz3 * GJ[2];
+    dt2 += ky * fy * tyc / tz3 * GJ[5];
+    dt0 += dm0 * fx / tz;
+    dt1 += dm1 * fy / tz;
+    dt2 += -dm0 * fx * P.t[0] / tz2 - dm1 * fy * P.t[1] / tz2;
+    gr.g_z[i] = (float)fabs(dt2);                                           // :349
+    const double u0 = dm0 * (cam.width / 2.0), u1 = dm1 * (cam.height / 2.0);
+    gr.g_uv[i] = (float)sqrt(u0 * u0 + u1 * u1);                            // :350-351
+    double dmu[3];
+#pragma unroll
+    for (int j = 0; j < 3; j++) dmu[j] = dt0 * R[j] + dt1 * R[3 + j] + dt2 * R[6 + j];  // :353
+
+    // SH (:355-363)
+    const double dv0 = mu[0] - cam.campos[0], dv1 = mu[1] - cam.campos[1], dv2 = mu[2] - cam.campos[2];
+    const double dn = sqrt(dv0 * dv0 + dv1 * dv1 + dv2 * dv2);
+    const double dns = dn > 1e-12 ? dn : 1.0;
+    const double dx = dv0 / dns, dy = dv1 / dns, dz = dv2 / dns;
+    double basis[16];
+    sh_basis(DEG, dx, dy, dz, basis);
+    const float *shp = sc.sh + (size_t)i * 3 * K;
+    double col[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < K; k++)
+#pragma unroll
+        for (int c = 0; c < 3; c++) col[c] += basis[k] * (double)shp[3 * k + c];
+    double dcc[3];
+#pragma unroll
+    for (int c = 0; c < 3; c++) dcc[c] = (col[c] + 0.5 > 0.0) ? dcol[c] : 0.0;
+#pragma unroll
+    for (int k = 0; k < K; k++)
+#pragma unroll
+        for (int c = 0; c < 3; c++) dsh[3 * k + c] = (float)(basis[k] * dcc[c]);
+    if (DEG > 0) {
+        double bg[16][3];
+        sh_basis_grad(DEG, dx, dy, dz, bg);
+        double dd[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            const double w = (double)shp[3 * k] * dcc[0] + (double)shp[3 * k + 1] * dcc[1] +
+                             (double)shp[3 * k + 2] * dcc[2];
+#pragma unroll
+            for (int d = 0; d < 3; d++) dd[d] += w * bg[k][d];
+        }
+        const double inner = dx * dd[0] + dy * dd[1] + dz * dd[2];
+        dmu[0] += (dd[0] - dx * inner) / dns;
+        dmu[1] += (dd[1] - dy * inner) / dns;
+        dmu[2] += (dd[2] - dz * inner) / dns;
+    }
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+        gr.d_mu[3 * i + j] = (float)dmu[j];
+        gr.d_eta[3 * i + j] = (float)geta[j];                               // :365-366
+    }
+}
+
+}  // namespace ssg
+
+extern "C" int ssg_preprocess_backward(const ssg_scene *scene, const ssg_camera *cam,
+                                       const ssg_grad_buffers *grads, void *stream) {
+    using namespace ssg;
+    if (!scene || !cam || !grads) return SSG_ERR_INVALID_ARGUMENT;
+    if (scene->sh_degree < 0 || scene->sh_degree > 3) return SSG_ERR_INVALID_ARGUMENT;
+    if (scene->n == 0) return SSG_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned blocks = (unsigned)((scene->n + 127) / 128);
+    switch (scene->sh_degree) {
+        case 0: k_preprocess_backward<0><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
+        case 1: k_preprocess_backward<1><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
+        case 2: k_preprocess_backward<2><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
+        default: k_preprocess_backward<3><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
+    }
+    return check_launch("k_preprocess_backward");
+}

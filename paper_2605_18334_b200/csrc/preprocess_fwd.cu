@@ -1,0 +1,115 @@
+// preprocess_fwd.cu -- K1: per-primitive EWA projection of 3D skew Gaussians.
+//
+// Replaces project_scene (reference projection.py:151-235) together with the
+// per-primitive half of bin_arrays (raster/tiles.py:49-57: tile rectangle and
+// count).  One thread per primitive, fp64 registers, coalesced row loads of
+// the SoA scene.  Compiled with --fmad=false: the depth, mean2d and radius
+// bits decide the instance lists, which must equal the reference's exactly,
+// so no contraction may change an intermediate rounding (the reference's
+// own fused op, the BLAS dot of projection.py:160, is spelled out with
+// explicit __fma_rn in project_geometry).
+#include "ssg_common.cuh"
+
+namespace ssg {
+
+template <int DEG>
+__global__ void __launch_bounds__(256)
+k_preprocess_forward(ssg_scene sc, ssg_camera cam, ssg_prim_buffers out, int ntx, int nty) {
+    constexpr int K = (DEG + 1) * (DEG + 1);
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool fb = false;
+    if (i < sc.n) {
+        double mu[3], ls[3], q4[4], eta[3];
+        float logit[2];
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+            mu[j] = sc.mu[3 * i + j];
+            ls[j] = sc.log_scale[3 * i + j];
+            eta[j] = (double)sc.beta[3 * i + j] + (double)sc.dir[3 * i + j];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) q4[j] = sc.rot[4 * i + j];
+        logit[0] = sc.opacity_logits[2 * i];
+        logit[1] = sc.opacity_logits[2 * i + 1];
+
+        Proj P;
+        project_geometry(cam, mu, ls, q4, logit, eta, P);
+        fb = P.fallback;
+
+        // colour (projection.py:217-223): view direction, SH, +0.5, floor at 0
+        double dv0 = mu[0] - cam.campos[0], dv1 = mu[1] - cam.campos[1], dv2 = mu[2] - cam.campos[2];
+        double dn = sqrt(dv0 * dv0 + dv1 * dv1 + dv2 * dv2);
+        double dns = dn > 1e-12 ? dn : 1.0;
+        double basis[16];
+        sh_basis(DEG, dv0 / dns, dv1 / dns, dv2 / dns, basis);
+        const float *shp = sc.sh + (size_t)i * (3 * K);
+        double col[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            col[0] += basis[k] * (double)shp[3 * k];
+            col[1] += basis[k] * (double)shp[3 * k + 1];
+            col[2] += basis[k] * (double)shp[3 * k + 2];
+        }
+
+        ssg_splat s;
+        s.mean_x = P.mean2d[0];
+        s.mean_y = P.mean2d[1];
+        s.conic_a = (float)P.inv_dil[0];
+        s.conic_b = (float)P.inv_dil[1];
+        s.conic_c = (float)P.inv_dil[3];
+        s.skew_x = (float)P.skew[0];
+        s.skew_y = (float)P.skew[1];
+        s.o1 = (float)(P.sig[0] * P.comp);
+        s.o2 = (float)(P.sig[1] * P.comp);
+        double c0 = col[0] + 0.5, c1 = col[1] + 0.5, c2 = col[2] + 0.5;
+        s.r = (float)(c0 > 0.0 ? c0 : 0.0);
+        s.g = (float)(c1 > 0.0 ? c1 : 0.0);
+        s.b = (float)(c2 > 0.0 ? c2 : 0.0);
+        s.pad0 = 0;
+        s.pad1 = 0;
+        // 64-byte record as four 16-byte stores
+        const int4 *src = reinterpret_cast<const int4 *>(&s);
+        int4 *dst = reinterpret_cast<int4 *>(out.splat + i);
+#pragma unroll
+        for (int j = 0; j < 4; j++) dst[j] = src[j];
+
+        // tile rectangle and count (tiles.py:49-57)
+        uint64_t rect;
+        out.tile_count[i] = tile_rect(P.mean2d[0], P.mean2d[1], P.radius, P.valid, ntx, nty, rect);
+        out.tile_rect[i] = rect;
+        out.valid[i] = (uint8_t)P.valid;
+        out.depth[i] = P.t[2];
+        out.radius[i] = P.radius;
+        // depth > near > 0 for valid primitives: the IEEE bits are monotone
+        out.depth_key[i] = P.valid ? (uint64_t)__double_as_longlong(P.t[2]) : ~0ull;
+    }
+    // n_skew_fallback counts every primitive (projection.py:234)
+    unsigned ballot = __ballot_sync(0xffffffffu, fb);
+    if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(out.n_skew_fallback, __popc(ballot));
+}
+
+}  // namespace ssg
+
+extern "C" int ssg_preprocess_forward(const ssg_scene *scene, const ssg_camera *cam,
+                                      const ssg_prim_buffers *out, void *stream) {
+    using namespace ssg;
+    if (!scene || !cam || !out) return SSG_ERR_INVALID_ARGUMENT;
+    if (cam->width > SSG_MAX_IMAGE_DIM || cam->height > SSG_MAX_IMAGE_DIM) return SSG_ERR_DIM_OVERFLOW;
+    if (cam->width < 1 || cam->height < 1) return SSG_ERR_INVALID_ARGUMENT;
+    if (scene->sh_degree < 0 || scene->sh_degree > 3 ||
+        scene->sh_coeffs != (scene->sh_degree + 1) * (scene->sh_degree + 1))
+        return SSG_ERR_INVALID_ARGUMENT;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(out->n_skew_fallback, 0, sizeof(int32_t), st);
+    if (e != cudaSuccess) { set_error("memset fallback", e); return SSG_ERR_CUDA; }
+    if (scene->n == 0) return SSG_OK;
+    int ntx = (cam->width + SSG_TILE - 1) / SSG_TILE, nty = (cam->height + SSG_TILE - 1) / SSG_TILE;
+    unsigned blocks = (unsigned)((scene->n + 255) / 256);
+    switch (scene->sh_degree) {
+        case 0: k_preprocess_forward<0><<<blocks, 256, 0, st>>>(*scene, *cam, *out, ntx, nty); break;
+        case 1: k_preprocess_forward<1><<<blocks, 256, 0, st>>>(*scene, *cam, *out, ntx, nty); break;
+        case 2: k_preprocess_forward<2><<<blocks, 256, 0, st>>>(*scene, *cam, *out, ntx, nty); break;
+        default: k_preprocess_forward<3><<<blocks, 256, 0, st>>>(*scene, *cam, *out, ntx, nty); break;
+    }
+    return check_launch("k_preprocess_forward");
+}

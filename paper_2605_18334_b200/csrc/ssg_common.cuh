@@ -1,0 +1,267 @@
+// ssg_common.cuh -- shared device code for the sm_100a skew-splat kernels.
+//
+// Reference semantics (pkg/src/skewsplat/...):
+//   constants            kernel_math.py:17-20, raster/_core.pyx:24-29, tiles.py:16
+//   per-primitive math   projection.py:151-235 (project_scene), scene.py:66-96,
+//                        projection.py:97-123 (_project_eta), sh.py:25-109
+// All preprocess math runs in fp64 registers: the depth and the tile
+// rectangle decide the (bit-exact) instance lists.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ssg_b200.h"
+
+#define SSG_ALPHA_MAX 0.99f          // kernel_math.py:17
+#define SSG_ALPHA_SKIP (1.0f / 255.0f) // kernel_math.py:18
+#define SSG_T_STOP 1e-4f             // kernel_math.py:19
+#define SSG_BETA_CLAMP 20.0          // kernel_math.py:20
+#define SSG_SQRT1_2 0.70710678118654752f
+#define SSG_TWO_OVER_SQRT_PI 1.12837916709551257f
+#define SSG_LOG2E 1.44269504088896341f
+
+namespace ssg {
+
+void set_error(const char *what, cudaError_t e);
+int check_launch(const char *what);
+
+// ------------------------------------------------------------------ SH
+__device__ __forceinline__ void sh_basis(int deg, double x, double y, double z, double *out) {
+    // sh.py:25-54
+    out[0] = 0.28209479177387814;
+    if (deg < 1) return;
+    out[1] = -0.4886025119029199 * y;
+    out[2] = 0.4886025119029199 * z;
+    out[3] = -0.4886025119029199 * x;
+    if (deg < 2) return;
+    double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    out[4] = 1.0925484305920792 * xy;
+    out[5] = -1.0925484305920792 * yz;
+    out[6] = 0.31539156525252005 * (2.0 * zz - xx - yy);
+    out[7] = -1.0925484305920792 * xz;
+    out[8] = 0.5462742152960396 * (xx - yy);
+    if (deg < 3) return;
+    out[9] = -0.5900435899266435 * y * (3.0 * xx - yy);
+    out[10] = 2.890611442640554 * xy * z;
+    out[11] = -0.4570457994644658 * y * (4.0 * zz - xx - yy);
+    out[12] = 0.3731763325901154 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+    out[13] = -0.4570457994644658 * x * (4.0 * zz - xx - yy);
+    out[14] = 1.445305721320277 * z * (xx - yy);
+    out[15] = -0.5900435899266435 * x * (xx - 3.0 * yy);
+}
+
+// ------------------------------------------------------ projection (fp64)
+// Everything project_scene computes for one primitive that the forward and
+// backward kernels need (projection.py:41-79 minus what can be rebuilt).
+struct Proj {
+    bool valid;
+    double t[3];
+    double tz;
+    double mean2d[2];
+    double J00, J02, J11, J12;
+    double gate0, gate1;
+    double T[6];       // Tmat = J R_w2c (2x3)
+    double Sig[9];     // sigma_world
+    double Rq[9];
+    double qn[4], qnorm;
+    double scale[3];
+    double cov[4];     // cov_raw
+    double inv_raw[4];
+    double inv_dil[4];
+    double det_raw, dd;
+    double comp, radius;
+    double sig[2];
+    double eta[3], w[3], u[2], v[2], r;
+    bool fallback, clip0, clip1;
+    double skew[2];
+};
+
+// projection.py:151-210 and _project_eta projection.py:97-123.
+// `mu`, `ls`, `q` fp64; `eta` = beta + dir (evaluated in fp64 from the fp32
+// inputs), logits fp32.
+__device__ __forceinline__ void project_geometry(const ssg_camera &cam, const double mu[3],
+                                                 const double ls[3], const double q4[4],
+                                                 const float logit[2], const double eta[3],
+                                                 Proj &P) {
+    const double *R = cam.R;
+    // projection.py:160 -- numpy/BLAS bits: fma(m2,R2,fma(m1,R1,m0*R0)) + t
+#pragma unroll
+    for (int c = 0; c < 3; c++)
+        P.t[c] = __dadd_rn(__fma_rn(mu[2], R[3 * c + 2], __fma_rn(mu[1], R[3 * c + 1], __dmul_rn(mu[0], R[3 * c]))),
+                           cam.t[c]);
+    double depth = P.t[2];
+    P.valid = depth > cam.near_plane;
+    double tz = P.valid ? depth : 1.0;
+    P.tz = tz;
+    double limx = __dmul_rn(1.3, cam.tan_fovx), limy = __dmul_rn(1.3, cam.tan_fovy);
+    double txz = __ddiv_rn(P.t[0], tz), tyz = __ddiv_rn(P.t[1], tz);
+    P.gate0 = fabs(txz) <= limx ? 1.0 : 0.0;
+    P.gate1 = fabs(tyz) <= limy ? 1.0 : 0.0;
+    double txc = __dmul_rn(fmin(fmax(txz, -limx), limx), tz);
+    double tyc = __dmul_rn(fmin(fmax(tyz, -limy), limy), tz);
+    double tz2 = __dmul_rn(tz, tz);
+    P.J00 = __ddiv_rn(cam.fx, tz);
+    P.J02 = __ddiv_rn(__dmul_rn(-cam.fx, txc), tz2);
+    P.J11 = __ddiv_rn(cam.fy, tz);
+    P.J12 = __ddiv_rn(__dmul_rn(-cam.fy, tyc), tz2);
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+        P.T[c] = __dadd_rn(__dmul_rn(P.J00, R[c]), __dmul_rn(P.J02, R[6 + c]));
+        P.T[3 + c] = __dadd_rn(__dmul_rn(P.J11, R[3 + c]), __dmul_rn(P.J12, R[6 + c]));
+    }
+    // scene.py:66-96
+    double nrm = sqrt(q4[0] * q4[0] + q4[1] * q4[1] + q4[2] * q4[2] + q4[3] * q4[3]);
+    double w = q4[0] / nrm, x = q4[1] / nrm, y = q4[2] / nrm, z = q4[3] / nrm;
+    P.qn[0] = w; P.qn[1] = x; P.qn[2] = y; P.qn[3] = z; P.qnorm = nrm;
+    P.Rq[0] = 1 - 2 * (y * y + z * z);
+    P.Rq[1] = 2 * (x * y - w * z);
+    P.Rq[2] = 2 * (x * z + w * y);
+    P.Rq[3] = 2 * (x * y + w * z);
+    P.Rq[4] = 1 - 2 * (x * x + z * z);
+    P.Rq[5] = 2 * (y * z - w * x);
+    P.Rq[6] = 2 * (x * z - w * y);
+    P.Rq[7] = 2 * (y * z + w * x);
+    P.Rq[8] = 1 - 2 * (x * x + y * y);
+#pragma unroll
+    for (int j = 0; j < 3; j++) P.scale[j] = exp(ls[j]);
+    double M[9];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++) M[3 * a + b] = P.Rq[3 * a + b] * P.scale[b];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++)
+            P.Sig[3 * a + b] = M[3 * a] * M[3 * b] + M[3 * a + 1] * M[3 * b + 1] + M[3 * a + 2] * M[3 * b + 2];
+    double TS[6];
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++)
+            TS[3 * a + b] = P.T[3 * a] * P.Sig[b] + P.T[3 * a + 1] * P.Sig[3 + b] + P.T[3 * a + 2] * P.Sig[6 + b];
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 2; b++)
+            P.cov[2 * a + b] = TS[3 * a] * P.T[3 * b] + TS[3 * a + 1] * P.T[3 * b + 1] + TS[3 * a + 2] * P.T[3 * b + 2];
+    double cd0 = P.cov[0] + cam.s, cd1 = P.cov[1], cd2 = P.cov[2], cd3 = P.cov[3] + cam.s;
+    P.det_raw = P.cov[0] * P.cov[3] - P.cov[1] * P.cov[2];
+    double det_dil = cd0 * cd3 - cd1 * cd2;
+    bool dok = det_dil > 1e-300;
+    P.valid = P.valid && dok;
+    P.dd = dok ? det_dil : 1.0;
+    P.inv_dil[0] = cd3 / P.dd;
+    P.inv_dil[3] = cd0 / P.dd;
+    P.inv_dil[1] = -cd1 / P.dd;
+    P.inv_dil[2] = -cd2 / P.dd;
+    P.comp = sqrt((P.det_raw > 0.0 ? P.det_raw : 0.0) / P.dd);
+    double mid = 0.5 * (cd0 + cd3);
+    double disc = mid * mid - det_dil;
+    double lam = mid + sqrt(disc > 0.0 ? disc : 0.0);
+    P.radius = 3.0 * sqrt(lam > 0.0 ? lam : 0.0);
+    // projection.py:207 -- unclamped ratio, no contraction
+    P.mean2d[0] = __dadd_rn(__dmul_rn(cam.fx, txz), cam.cx);
+    P.mean2d[1] = __dadd_rn(__dmul_rn(cam.fy, tyz), cam.cy);
+    // kernel_math.py:158-165
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+        double l = (double)logit[j];
+        double sgm;
+        if (l >= 0) sgm = 1.0 / (1.0 + exp(-l));
+        else { double ex = exp(l); sgm = ex / (1.0 + ex); }
+        P.sig[j] = sgm;
+    }
+    // _project_eta (projection.py:97-123)
+#pragma unroll
+    for (int j = 0; j < 3; j++) P.eta[j] = eta[j];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+        P.w[a] = P.Sig[3 * a] * eta[0] + P.Sig[3 * a + 1] * eta[1] + P.Sig[3 * a + 2] * eta[2];
+#pragma unroll
+    for (int a = 0; a < 2; a++) P.u[a] = P.T[3 * a] * P.w[0] + P.T[3 * a + 1] * P.w[1] + P.T[3 * a + 2] * P.w[2];
+    double p = eta[0] * P.w[0] + eta[1] * P.w[1] + eta[2] * P.w[2];
+    bool ok = P.det_raw > 1e-300;
+    double d = ok ? P.det_raw : 1.0;
+    if (ok) {
+        P.inv_raw[0] = P.cov[3] / d;
+        P.inv_raw[3] = P.cov[0] / d;
+        P.inv_raw[1] = -P.cov[1] / d;
+        P.inv_raw[2] = -P.cov[2] / d;
+    } else {
+        P.inv_raw[0] = P.inv_raw[1] = P.inv_raw[2] = P.inv_raw[3] = 0.0;
+    }
+    P.v[0] = P.inv_raw[0] * P.u[0] + P.inv_raw[1] * P.u[1];
+    P.v[1] = P.inv_raw[2] * P.u[0] + P.inv_raw[3] * P.u[1];
+    double qq = p - (P.u[0] * P.v[0] + P.u[1] * P.v[1]);
+    double radicand = 1.0 + qq;
+    P.fallback = (!ok) || (radicand <= 0.0);
+    P.r = sqrt(P.fallback ? 1.0 : radicand);
+    double s0 = P.fallback ? 0.0 : P.v[0] / P.r;
+    double s1 = P.fallback ? 0.0 : P.v[1] / P.r;
+    P.clip0 = fabs(s0) > SSG_BETA_CLAMP;
+    P.clip1 = fabs(s1) > SSG_BETA_CLAMP;
+    P.skew[0] = fmin(fmax(s0, -SSG_BETA_CLAMP), SSG_BETA_CLAMP);
+    P.skew[1] = fmin(fmax(s1, -SSG_BETA_CLAMP), SSG_BETA_CLAMP);
+}
+
+// ------------------------------------------------------------- tile rect
+// raster/tiles.py:49-57: r = ceil(radius); [floor((m-r)/16), floor((m+r)/16)+1)
+// clipped to the grid, evaluated in fp64 exactly as numpy does (no products,
+// so no contraction can change it).  Returns the packed rect and the count.
+__device__ __forceinline__ uint32_t tile_rect(double mx, double my, double radius, bool valid,
+                                              int ntx, int nty, uint64_t &packed) {
+    double r = ceil(radius);
+    double fx0 = floor((mx - r) / 16.0), fx1 = floor((mx + r) / 16.0) + 1.0;
+    double fy0 = floor((my - r) / 16.0), fy1 = floor((my + r) / 16.0) + 1.0;
+    int x0 = (int)fmin(fmax(fx0, 0.0), (double)ntx);
+    int x1 = (int)fmin(fmax(fx1, 0.0), (double)ntx);
+    int y0 = (int)fmin(fmax(fy0, 0.0), (double)nty);
+    int y1 = (int)fmin(fmax(fy1, 0.0), (double)nty);
+    int nx = valid ? max(x1 - x0, 0) : 0;
+    int ny = valid ? max(y1 - y0, 0) : 0;
+    packed = (uint64_t)x0 | ((uint64_t)x1 << 16) | ((uint64_t)y0 << 32) | ((uint64_t)y1 << 48);
+    return (uint32_t)(nx * ny);
+}
+
+// --------------------------------------------------------- blend math
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float fast_rcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// erfc(x) for x >= 0 with ~1e-7 relative error everywhere (Chebyshev-fitted
+// exp form, one rcp + one ex2).  The reference erf (raster/_core.pyx:57-74)
+// is near-exact fp64; this keeps the *relative* error of E = 1 + erf(z) =
+// erfc(-z) small even deep in the lower tail, which the alpha-skip test
+// depends on.
+__device__ __forceinline__ float erfc_pos(float x) {
+    float t = fast_rcp(fmaf(0.5f, x, 1.0f));
+    float p = fmaf(t, 0.17087277f, -0.82215223f);
+    p = fmaf(t, p, 1.48851587f);
+    p = fmaf(t, p, -1.13520398f);
+    p = fmaf(t, p, 0.27886807f);
+    p = fmaf(t, p, -0.18628806f);
+    p = fmaf(t, p, 0.09678418f);
+    p = fmaf(t, p, 0.37409196f);
+    p = fmaf(t, p, 1.00002368f);
+    p = fmaf(t, p, -1.26551223f);
+    return t * fast_exp2((p - x * x) * SSG_LOG2E);
+}
+
+// E = 1 + erf(z) (raster/_core.pyx:137); exactly 1 at z == 0 like the
+// reference (erf(0) == 0 exactly, kernel_math.py:79-80).
+__device__ __forceinline__ float skew_E(float z) {
+    float y = erfc_pos(fabsf(z));
+    float E = z > 0.0f ? 2.0f - y : y;
+    return z == 0.0f ? 1.0f : E;
+}
+
+}  // namespace ssg

@@ -1,0 +1,336 @@
+"""Device-resident rasterizer engine (host side of the C ABI).
+
+PyTorch provides device memory and the stream; every computation is a call
+into libssg_b200.so.  Buffers are owned here and grown on demand; results
+returned by Engine methods are views of engine buffers that stay valid
+until the next call with the same engine.
+
+Stage map (reference pkg/src/skewsplat/...):
+  Engine.project_and_bin   projection.py:151-235 + raster/tiles.py:43-79
+  Engine.forward           raster/forward.py:37-54 (device part)
+  Engine.backward          raster/backward.py:77-99 (device part)
+"""
+
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import math
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .camera import CameraView, intrinsics, to_opencv, world_to_cam
+
+TILE = 16
+
+
+def grid_dims(width: int, height: int) -> tuple[int, int]:
+    """raster/tiles.py:29-30."""
+    return -(-width // TILE), -(-height // TILE)
+
+
+def camera_struct(view: CameraView, s: float) -> N.SsgCamera:
+    """Host-side camera constants, evaluated with numpy exactly as the
+    reference does (camera.py:60-75, projection.py:152-167)."""
+    view = to_opencv(view)
+    r_w2c, t_vec = world_to_cam(view)
+    K = intrinsics(view)
+    cam = N.SsgCamera()
+    cam.R[:] = [float(x) for x in np.ascontiguousarray(r_w2c).ravel()]
+    cam.t[:] = [float(x) for x in t_vec]
+    cam.campos[:] = [float(x) for x in view.c2w[:3, 3]]
+    cam.fx, cam.fy = float(K[0, 0]), float(K[1, 1])
+    cam.cx, cam.cy = float(K[0, 2]), float(K[1, 2])
+    cam.tan_fovx = math.tan(view.fov_x / 2.0)
+    cam.tan_fovy = math.tan(view.fov_y / 2.0)
+    cam.near_plane = float(view.near)
+    cam.s = float(s)
+    cam.width, cam.height = int(view.width), int(view.height)
+    return cam
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+class DeviceScene:
+    """Scene resident in HBM: fp64 geometry (mu, log_scale, rot) that decides
+    depth order and tile membership, fp32 appearance (sh, logits, beta, dir)."""
+
+    def __init__(self, mu, log_scale, rot, sh, opacity_logits, beta, dir, background, sh_degree):
+        self.mu, self.log_scale, self.rot = mu, log_scale, rot
+        self.sh, self.opacity_logits, self.beta, self.dir = sh, opacity_logits, beta, dir
+        self.background = np.asarray(background, dtype=np.float64).reshape(3)
+        self.sh_degree = int(sh_degree)
+        self.n = int(mu.shape[0])
+        self.K = (self.sh_degree + 1) ** 2
+
+    @classmethod
+    def from_host(cls, scene, device=None) -> "DeviceScene":
+        """Upload a reference-layout fp64 Scene (any object with the reference
+        attributes).  fp64 -> fp32 conversion of the appearance fields runs on
+        the device after the copy."""
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        deg = int(scene.sh_degree)
+        K = (deg + 1) ** 2
+        n = int(np.asarray(scene.mu).shape[0])
+
+        def up(a, shape, f32):
+            a = np.ascontiguousarray(a, dtype=np.float64).reshape(shape)
+            t = torch.from_numpy(a).to(dev, non_blocking=True)
+            return t.float() if f32 else t
+
+        sh = np.asarray(scene.sh)
+        if sh.ndim != 3:
+            sh = sh.reshape(n, -1, 3)
+        return cls(up(scene.mu, (n, 3), False), up(scene.log_scale, (n, 3), False),
+                   up(scene.rot, (n, 4), False), up(sh[:, :K, :], (n, K, 3), True),
+                   up(scene.opacity_logits, (n, 2), True), up(scene.beta, (n, 3), True),
+                   up(scene.dir, (n, 3), True), scene.background, deg)
+
+    def struct(self) -> N.SsgScene:
+        s = N.SsgScene()
+        s.n, s.sh_degree, s.sh_coeffs = self.n, self.sh_degree, self.K
+        s.mu, s.log_scale, s.rot = _ptr(self.mu), _ptr(self.log_scale), _ptr(self.rot)
+        s.sh, s.opacity_logits = _ptr(self.sh), _ptr(self.opacity_logits)
+        s.beta, s.dir = _ptr(self.beta), _ptr(self.dir)
+        return s
+
+
+@dataclasses.dataclass
+class DeviceFrame:
+    color: torch.Tensor       # (H,W,3) f32
+    final_T: torch.Tensor     # (H,W) f32
+    n_contrib: torch.Tensor   # (H,W) i32
+    last_idx: torch.Tensor    # (H,W) i32
+    width: int
+    height: int
+    n_primitives: int
+    n_instances: int
+    s: float
+
+
+@dataclasses.dataclass
+class DeviceGrads:
+    screen: torch.Tensor      # (N,12)
+    d_mu: torch.Tensor
+    d_log_scale: torch.Tensor
+    d_rot: torch.Tensor
+    d_sh: torch.Tensor
+    d_opacity_logits: torch.Tensor
+    d_eta: torch.Tensor       # d_beta == d_dir (projection.py:365-366)
+    g_uv: torch.Tensor
+    g_z: torch.Tensor
+
+
+class Engine:
+    def __init__(self, device=None):
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.lib = N.lib()
+        self._prim_n = -1
+        self._bins_key = None
+        self._frame_key = None
+        self._grad_key = None
+        self.capacity = 0
+        self.last_m = 0
+
+    # ------------------------------------------------------------ buffers
+    def _empty(self, shape, dtype):
+        return torch.empty(shape, dtype=dtype, device=self.device)
+
+    def _ensure_prim(self, n: int):
+        if n <= self._prim_n and self._prim_n >= 0:
+            return
+        nn = max(n, 1)
+        self.splat = self._empty((nn, N.SPLAT_BYTES // 8), torch.float64)
+        self.depth_key = self._empty((nn,), torch.int64)
+        self.tile_count = self._empty((nn,), torch.int32)
+        self.tile_rect = self._empty((nn,), torch.int64)
+        self.valid = self._empty((nn,), torch.uint8)
+        self.depth = self._empty((nn,), torch.float64)
+        self.radius = self._empty((nn,), torch.float64)
+        self.n_fallback = self._empty((1,), torch.int32)
+        self.depth_order = self._empty((nn,), torch.int32)
+        self.rank_offset = self._empty((nn + 1,), torch.int64)
+        self.n_inst_dev = self._empty((1,), torch.int64)
+        self._prim_n = nn
+        self._bins_key = None
+
+    def _prim_struct(self) -> N.SsgPrimBuffers:
+        p = N.SsgPrimBuffers()
+        p.splat, p.depth_key, p.tile_count = _ptr(self.splat), _ptr(self.depth_key), _ptr(self.tile_count)
+        p.tile_rect, p.valid, p.depth = _ptr(self.tile_rect), _ptr(self.valid), _ptr(self.depth)
+        p.radius, p.n_skew_fallback = _ptr(self.radius), _ptr(self.n_fallback)
+        return p
+
+    def _ensure_bins(self, n: int, m: int, n_tiles: int):
+        cap = self.capacity
+        if m > cap:
+            cap = max(int(m * 1.25) + 1024, 1024)
+        key = (self._prim_n, cap, n_tiles)
+        if key == self._bins_key:
+            return
+        if cap != self.capacity:
+            self.inst_prim = self._empty((cap,), torch.int32)
+            self.inst_tile = self._empty((cap,), torch.int16)
+            self.inst_prim_tmp = self._empty((cap,), torch.int32)
+            self.inst_tile_tmp = self._empty((cap,), torch.int16)
+            self.capacity = cap
+        self.ranges = self._empty((n_tiles, 2), torch.int32)
+        nbytes = ctypes.c_size_t(0)
+        N.check(self.lib.ssg_bin_temp_bytes(self._prim_n, cap, max(n_tiles, 1), ctypes.byref(nbytes)),
+                "ssg_bin_temp_bytes")
+        self.temp = self._empty((max(int(nbytes.value), 1),), torch.uint8)
+        self._bins_key = key
+
+    def _bins_struct(self) -> N.SsgBinBuffers:
+        b = N.SsgBinBuffers()
+        b.depth_order, b.rank_offset, b.n_instances = _ptr(self.depth_order), _ptr(self.rank_offset), _ptr(self.n_inst_dev)
+        b.capacity = self.capacity
+        if self.capacity > 0:
+            b.inst_prim, b.inst_tile = _ptr(self.inst_prim), _ptr(self.inst_tile)
+            b.inst_prim_tmp, b.inst_tile_tmp = _ptr(self.inst_prim_tmp), _ptr(self.inst_tile_tmp)
+        if self._bins_key is not None:
+            b.ranges, b.temp, b.temp_bytes = _ptr(self.ranges), _ptr(self.temp), self.temp.numel()
+        return b
+
+    def _ensure_frame(self, W: int, H: int):
+        if self._frame_key == (W, H):
+            return
+        self.color = self._empty((H, W, 3), torch.float32)
+        self.final_T = self._empty((H, W), torch.float32)
+        self.n_contrib = self._empty((H, W), torch.int32)
+        self.last_idx = self._empty((H, W), torch.int32)
+        self._frame_key = (W, H)
+
+    def _frame_struct(self, final_T=None, last_idx=None) -> N.SsgFrameBuffers:
+        f = N.SsgFrameBuffers()
+        f.color, f.n_contrib = _ptr(self.color), _ptr(self.n_contrib)
+        f.final_T = _ptr(self.final_T if final_T is None else final_T)
+        f.last_idx = _ptr(self.last_idx if last_idx is None else last_idx)
+        return f
+
+    def _ensure_grads(self, n: int, K: int):
+        if self._grad_key == (n, K):
+            return
+        nn = max(n, 1)
+        self.g_screen = self._empty((nn, 12), torch.float32)
+        self.g_mu = self._empty((nn, 3), torch.float32)
+        self.g_log_scale = self._empty((nn, 3), torch.float32)
+        self.g_rot = self._empty((nn, 4), torch.float32)
+        self.g_sh = self._empty((nn, K, 3), torch.float32)
+        self.g_logits = self._empty((nn, 2), torch.float32)
+        self.g_eta = self._empty((nn, 3), torch.float32)
+        self.g_uv = self._empty((nn,), torch.float32)
+        self.g_z = self._empty((nn,), torch.float32)
+        self._grad_key = (n, K)
+
+    def _grad_struct(self) -> N.SsgGradBuffers:
+        g = N.SsgGradBuffers()
+        g.screen, g.d_mu, g.d_log_scale = _ptr(self.g_screen), _ptr(self.g_mu), _ptr(self.g_log_scale)
+        g.d_rot, g.d_sh, g.d_opacity_logits = _ptr(self.g_rot), _ptr(self.g_sh), _ptr(self.g_logits)
+        g.d_eta, g.g_uv, g.g_z = _ptr(self.g_eta), _ptr(self.g_uv), _ptr(self.g_z)
+        return g
+
+    def _stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    # ------------------------------------------------------------- stages
+    def _bin(self, n: int, W: int, H: int) -> int:
+        """bin_prepare -> M (one 8-byte D2H) -> bin_finish."""
+        ntx, nty = grid_dims(W, H)
+        st = self._stream()
+        self._ensure_bins(n, self.capacity, ntx * nty)
+        prim = self._prim_struct()
+        N.check(self.lib.ssg_bin_prepare(n, ctypes.byref(prim), ctypes.byref(self._bins_struct()), st),
+                "ssg_bin_prepare")
+        m = int(self.n_inst_dev.item())
+        self._ensure_bins(n, m, ntx * nty)
+        N.check(self.lib.ssg_bin_finish(n, m, W, H, ctypes.byref(prim), ctypes.byref(self._bins_struct()), st),
+                "ssg_bin_finish")
+        self.last_m = m
+        return m
+
+    def project_and_bin(self, ds: DeviceScene, cam: N.SsgCamera) -> int:
+        W, H = int(cam.width), int(cam.height)
+        if W > 65535 or H > 65535:
+            raise ValueError("image dimension overflow")
+        self._ensure_prim(ds.n)
+        sc = ds.struct()
+        N.check(self.lib.ssg_preprocess_forward(ctypes.byref(sc), ctypes.byref(cam),
+                                                ctypes.byref(self._prim_struct()), self._stream()),
+                "ssg_preprocess_forward")
+        return self._bin(ds.n, W, H)
+
+    def bin_arrays(self, mean2d, radius, depth, valid, W: int, H: int) -> int:
+        """Binning of caller-provided screen arrays (device tensors, fp64/uint8)."""
+        n = int(mean2d.shape[0])
+        self._ensure_prim(n)
+        N.check(self.lib.ssg_bin_rects(n, _ptr(mean2d), _ptr(radius), _ptr(depth), _ptr(valid), W, H,
+                                       ctypes.byref(self._prim_struct()), self._stream()),
+                "ssg_bin_rects")
+        return self._bin(n, W, H)
+
+    def forward(self, ds: DeviceScene, view: CameraView, s: float = 0.3) -> DeviceFrame:
+        cam = camera_struct(view, s)
+        W, H = int(cam.width), int(cam.height)
+        m = self.project_and_bin(ds, cam)
+        self._ensure_frame(W, H)
+        bg = (ctypes.c_float * 3)(*[float(x) for x in ds.background])
+        N.check(self.lib.ssg_blend_forward(m, W, H, bg, _ptr(self.splat), ctypes.byref(self._bins_struct()),
+                                           ctypes.byref(self._frame_struct()), self._stream()),
+                "ssg_blend_forward")
+        return DeviceFrame(self.color, self.final_T, self.n_contrib, self.last_idx, W, H, ds.n, m, s)
+
+    def backward(self, ds: DeviceScene, view: CameraView, s: float, final_T: torch.Tensor,
+                 last_idx: torch.Tensor, dL: torch.Tensor, rebin: bool = True,
+                 expect_m: int | None = None) -> DeviceGrads:
+        """Blend backward + projection backward.  With rebin=True the
+        projection and binning are recomputed first (raster/backward.py:49-53)
+        and `expect_m` is checked against the new instance count."""
+        cam = camera_struct(view, s)
+        W, H = int(cam.width), int(cam.height)
+        if rebin:
+            m = self.project_and_bin(ds, cam)
+        else:
+            m = self.last_m
+        if expect_m is not None and m != expect_m:
+            from .raster.backward import FrameMismatchError
+            raise FrameMismatchError("instance count differs from the forward pass")
+        self._ensure_frame(W, H)
+        self._ensure_grads(ds.n, ds.K)
+        bg = (ctypes.c_float * 3)(*[float(x) for x in ds.background])
+        st = self._stream()
+        gs = self._grad_struct()
+        N.check(self.lib.ssg_blend_backward(ds.n, m, W, H, bg, _ptr(self.splat), ctypes.byref(self._bins_struct()),
+                                            ctypes.byref(self._frame_struct(final_T, last_idx)), _ptr(dL),
+                                            ctypes.byref(gs), st),
+                "ssg_blend_backward")
+        sc = ds.struct()
+        N.check(self.lib.ssg_preprocess_backward(ctypes.byref(sc), ctypes.byref(cam), ctypes.byref(gs), st),
+                "ssg_preprocess_backward")
+        n = ds.n
+        return DeviceGrads(self.g_screen[:n], self.g_mu[:n], self.g_log_scale[:n], self.g_rot[:n],
+                           self.g_sh[:n], self.g_logits[:n], self.g_eta[:n], self.g_uv[:n], self.g_z[:n])
+
+    # ------------------------------------------------------ introspection
+    def grid(self, n_tiles: int):
+        """Sorted instance lists and ranges of the last binning (device)."""
+        m = self.last_m
+        return (self.inst_prim[:m], self.inst_tile[:m], self.ranges[:n_tiles])
+
+    def n_skew_fallback(self) -> int:
+        return int(self.n_fallback.item())
+
+
+_engines: dict = {}
+
+
+def default_engine(device=None) -> Engine:
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    key = str(dev)
+    if key not in _engines:
+        _engines[key] = Engine(dev)
+    return _engines[key]

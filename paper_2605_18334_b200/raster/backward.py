@@ -1,0 +1,100 @@
+"""Backward rendering (drop-in for reference raster/backward.py:77-99).
+
+Like the reference, the backward pass recomputes projection and binning from
+the scene it is given (backward.py:49-53), checks the instance count against
+the frame bundle, replays blending back to front from each pixel's last
+blended instance, reduces per-instance gradients per primitive and chains
+them through the projection.  All of it runs on the GPU.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import torch
+
+from ..camera import CameraView, to_opencv
+from ..engine import DeviceScene, default_engine
+from . import backend
+from .forward import FrameBundle  # noqa: F401
+
+
+class FrameMismatchError(ValueError):
+    """The frame bundle was not produced from this scene/view pair."""
+
+
+@dataclasses.dataclass
+class GradientBundle:
+    d_mu: np.ndarray              # (N,3)
+    d_log_scale: np.ndarray       # (N,3)
+    d_rot: np.ndarray             # (N,4)
+    d_sh: np.ndarray              # (N,K,3)
+    d_opacity_logits: np.ndarray  # (N,2)
+    d_beta: np.ndarray            # (N,3)
+    d_dir: np.ndarray             # (N,3)
+    g_uv: np.ndarray              # (N,) image-plane positional gradient norm
+    g_z: np.ndarray               # (N,) |dL/d camera depth|
+    n_skew_fallback: int
+
+
+def _validate(scene, view, frame, dL_dpixels):
+    """backward.py:80-88."""
+    if (view.width, view.height) != (frame.width, frame.height):
+        raise FrameMismatchError("view dimensions differ from the frame bundle")
+    if len(scene.mu) != frame.n_primitives:
+        raise FrameMismatchError("primitive count differs from the frame bundle")
+    dL = np.ascontiguousarray(dL_dpixels, dtype=np.float64)
+    if dL.shape != (frame.height, frame.width, 3):
+        raise FrameMismatchError(f"dL_dpixels must be ({frame.height}, {frame.width}, 3)")
+    return dL
+
+
+def _device_backward(scene, view, frame, dL):
+    eng = default_engine()
+    dev = eng.device
+    ds = DeviceScene.from_host(scene, dev)
+    final_T = torch.from_numpy(np.ascontiguousarray(frame.final_T, dtype=np.float64)).to(
+        dev, non_blocking=True).float()
+    last_idx = torch.from_numpy(np.ascontiguousarray(frame.last_idx, dtype=np.int64)).to(
+        dev, non_blocking=True).int()
+    dL_dev = torch.from_numpy(dL).to(dev, non_blocking=True).float()
+    g = eng.backward(ds, view, frame.s, final_T, last_idx, dL_dev, rebin=True,
+                     expect_m=frame.n_instances)
+    return eng, g
+
+
+def _host(t: torch.Tensor) -> torch.Tensor:
+    src = t.to(torch.float64)
+    dst = torch.empty(src.shape, dtype=torch.float64, pin_memory=True)
+    dst.copy_(src, non_blocking=True)
+    return dst
+
+
+def screen_gradients(scene, view: CameraView, frame, dL_dpixels) -> dict:
+    """Per-primitive screen-space gradients (mirror of _screen_gradients,
+    backward.py:42-74): d_mean2d, d_conic, d_skew2d, d_opair, d_color."""
+    view = to_opencv(view)
+    dL = _validate(scene, view, frame, dL_dpixels)
+    eng, g = _device_backward(scene, view, frame, dL)
+    sc = _host(g.screen)
+    torch.cuda.current_stream().synchronize()
+    sc = sc.numpy()
+    return {"d_mean2d": sc[:, 0:2], "d_conic": sc[:, 2:5], "d_skew2d": sc[:, 5:7],
+            "d_opair": sc[:, 7:9], "d_color": sc[:, 9:12]}
+
+
+def render_backward(scene, view: CameraView, frame, dL_dpixels: np.ndarray,
+                    backend_name: str | None = None) -> GradientBundle:
+    backend.active_backend(backend_name)
+    view = to_opencv(view)
+    dL = _validate(scene, view, frame, dL_dpixels)
+    eng, g = _device_backward(scene, view, frame, dL)
+    outs = [_host(x) for x in (g.d_mu, g.d_log_scale, g.d_rot, g.d_sh, g.d_opacity_logits,
+                                g.d_eta, g.d_eta, g.g_uv, g.g_z)]
+    n_fb = eng.n_skew_fallback()  # synchronizes the stream
+    torch.cuda.current_stream().synchronize()
+    o = [x.numpy() for x in outs]
+    return GradientBundle(d_mu=o[0], d_log_scale=o[1], d_rot=o[2], d_sh=o[3],
+                          d_opacity_logits=o[4], d_beta=o[5], d_dir=o[6], g_uv=o[7], g_z=o[8],
+                          n_skew_fallback=n_fb)
