@@ -1,0 +1,363 @@
+"""Benchmark: fwd+bwd raster of 1M skew Gaussians at 1080p (BASELINE.json
+config 2), one process per GPU.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step = one forward + backward frame of the G2 workload (SURVEY.md §8(d):
+1M fp32-rounded skew Gaussians, SH degree 3, rotated pose, 1920x1080,
+upstream dL ~ N(0,1)).  `value` is whole-job views/s (frames/s summed over
+ranks; every rank renders its own copy of the frame -- config 2 does not
+shard, so N>1 runs N replicas, weak scaling) with inputs resident in HBM and
+device time from CUDA events, max over ranks.  `e2e` times the same frame
+through the reference-facing drop-in API (render_forward / render_backward)
+with the scene and dL in pinned host memory: host->device and device->host
+copies inside the timed region, wall clock, max over ranks.
+
+--impl reference runs the reference's own CPU implementation (the
+unmodified reference package built into oracle/_ref, Cython+OpenMP blend on
+all host cores; falls back to the C oracle port when oracle/_ref is absent)
+on a bounded homothetic 1/k sample of the same frame (see
+synthetic.homothetic_sample) and reports full-frame views/s = 1/(k * t_sample).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "fwd+bwd raster ms/frame, 1M skew Gaussians @1080p; views/s at 1/2/4/8 GPU"
+UNIT = "views/s"
+N_PRIM, WIDTH, HEIGHT = 1_000_000, 1920, 1080
+# per-pair algorithmic instruction counts (fixed, not tuned)
+FP32_PER_PAIR = {"blend_fwd": 30, "blend_bwd": 90}
+MUFU_PER_PAIR = {"blend_fwd": 3, "blend_bwd": 5}
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def workload():
+    from paper_2605_18334_b200.synthetic import frustum_scene, frustum_view
+    scene = frustum_scene(N_PRIM, width=WIDTH, height=HEIGHT)
+    view = frustum_view(WIDTH, HEIGHT)
+    dL = np.random.default_rng(1).normal(size=(HEIGHT, WIDTH, 3))
+    return scene, view, dL
+
+
+# ------------------------------------------------------------- CPU legs
+def _load_reference():
+    """The unmodified reference package from oracle/_ref, or None."""
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    if not os.path.isdir(os.path.join(ref, "skewsplat")):
+        return None
+    sys.path.insert(0, ref)
+    try:
+        from skewsplat.raster import backend
+        from skewsplat.raster.backward import render_backward
+        from skewsplat.raster.forward import render_forward
+        if backend.active_backend() != "cython":
+            return None
+        return render_forward, render_backward
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def cpu_sample_runner(scene, view, dL_full, k: int):
+    """Returns (kind, run_once, sample_desc) for the bounded CPU sample."""
+    from paper_2605_18334_b200.synthetic import homothetic_sample
+    sub, sv = homothetic_sample(scene, view, k)
+    dL = np.random.default_rng(1).normal(size=(sv.height, sv.width, 3))
+    ref = _load_reference()
+    desc = (f"homothetic 1/{k} sample of the config-2 frame: {len(sub)} primitives, "
+            f"{sv.width}x{sv.height}, scales x sqrt({k}); full-frame time = {k} x sample time")
+    if ref is not None:
+        rf, rb = ref
+
+        def run():
+            fr = rf(sub, sv, 0.3, backend_name="cython")
+            rb(sub, sv, fr, dL, backend_name="cython")
+        return "reference", run, desc
+    from oracle import oracle as O
+    O.set_num_threads(cpu_cores())
+
+    def run():
+        fr = O.render_forward(sub, sv, 0.3)
+        O.render_backward(sub, sv, fr, dL)
+    return "port", run, desc
+
+
+def cpu_baseline(scene, view, dL, k: int, reps: int):
+    kind, run, desc = cpu_sample_runner(scene, view, dL, k)
+    run()  # warm (imports, page-in)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        run()
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts) * k
+    return {"value": 1.0 / t, "unit": UNIT, "cores": cpu_cores(), "kind": kind,
+            "sample": desc + f"; median of {reps}", "ms_per_frame": t * 1e3}
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in self.rows if len(r) >= 7
+                          for j in range(4) if r[3 + j].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ main
+def tile_pairs(frame, ranges, width, height):
+    """sum over tiles of npix(tile) * max(0, max last_idx in
+    the tile - start + 1) -- the tile-synchronous pixel x instance pairs."""
+    import torch
+    ntx, nty = -(-width // 16), -(-height // 16)
+    li = frame.last_idx
+    pad = torch.full((nty * 16, ntx * 16), -1, dtype=torch.int64, device=li.device)
+    pad[:height, :width] = li.long()
+    tmax = pad.view(nty, 16, ntx, 16).amax(dim=(1, 3)).reshape(-1)
+    ones = torch.zeros((nty * 16, ntx * 16), dtype=torch.int64, device=li.device)
+    ones[:height, :width] = 1
+    npix = ones.view(nty, 16, ntx, 16).sum(dim=(1, 3)).reshape(-1)
+    start = ranges[:, 0].long()
+    cnt = torch.clamp(tmax - start + 1, min=0)
+    return int((npix * cnt).sum().item())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-k", type=int, default=16, help="homothetic CPU sample factor")
+    ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    config = {"workload": "config 2: G2 synthetic 1M skew Gaussians (SH3, fp32-rounded), 1920x1080, "
+                          "rotated pose, forward+backward per frame",
+              "n_primitives": N_PRIM, "width": WIDTH, "height": HEIGHT,
+              "parallelism": f"replicas x{world} (config 2 does not shard)",
+              "l2": "inputs larger than L2 (scene 304 MB, instance lists ~110 MB per frame)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        scene, view, dL = workload()
+        steps = []
+        kind, run, desc = cpu_sample_runner(scene, view, dL, args.cpu_k)
+        for _ in range(args.warmup):
+            run()
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            run()
+            steps.append(time.perf_counter() - t0)
+        t = statistics.median(steps) * args.cpu_k
+        v = 1.0 / t
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": kind,
+                             "sample": desc + f"; median of {args.steps} steps"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2605_18334_b200.engine import DeviceScene, Engine
+    from paper_2605_18334_b200.raster import render_backward, render_forward
+
+    scene, view, dL_host = workload()
+    eng = Engine(torch.device("cuda", local))
+    ds = DeviceScene.from_host(scene)
+    dL = torch.from_numpy(dL_host).cuda().float()
+
+    def step():
+        f = eng.forward(ds, view, 0.3)
+        eng.backward(ds, view, 0.3, f.final_T, f.last_idx, dL, rebin=False)
+        return f
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(args.warmup, 3)):
+        f = step()
+    barrier()
+    m = f.n_instances
+    pairs = tile_pairs(f, eng.ranges, WIDTH, HEIGHT)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    eng.stage_events = {}
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    barrier()
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    stage_ms = {k: statistics.mean(a.elapsed_time(b) for a, b in v) for k, v in eng.stage_events.items()}
+    eng.stage_events = None
+    value = world * 1000.0 / ms
+
+    # ---- e2e through the drop-in API with pinned host buffers
+    from paper_2605_18334_b200.scene import Scene
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+        t.numpy()[...] = a
+        return t.numpy()
+    pscene = Scene(*(pinned(getattr(scene, f)) for f in Scene.ARRAY_FIELDS),
+                   background=scene.background, sh_degree=scene.sh_degree)
+    pdL = pinned(dL_host)
+    fr = render_forward(pscene, view)
+    render_backward(pscene, view, fr, pdL)
+    barrier()
+    e2e_t = []
+    for _ in range(args.e2e_steps):
+        barrier()
+        t0 = time.perf_counter()
+        fr = render_forward(pscene, view)
+        g = render_backward(pscene, view, fr, pdL)
+        torch.cuda.synchronize()
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = max_over_ranks(statistics.median(e2e_t))
+    n = len(scene)
+    K = 16
+    scene_bytes = n * (3 + 3 + 4 + 3 * K + 2 + 3 + 3) * 8
+    h2d = 2 * scene_bytes + HEIGHT * WIDTH * (8 + 8 + 24)  # fwd + bwd uploads, final_T, last_idx, dL
+    d2h = HEIGHT * WIDTH * (24 + 8 + 4 + 8) + n * (3 + 3 + 4 + 3 * K + 2 + 3 + 3 + 1 + 1) * 8
+    e2e = {"value": world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
+           "path": "paper_2605_18334_b200.raster.render_forward + render_backward, numpy fp64 "
+                   "scene/dL in pinned host memory, fp64 outputs back to host; backward "
+                   "recomputes projection+binning like the reference"}
+
+    # ---- roofline of the dominant kernel (blend backward): FP32 issue bound
+    import torch.cuda as tc
+    props = tc.get_device_properties(local)
+    n_sm = props.multi_processor_count
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+        peaks = json.load(fh)
+    f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    r_fp32 = n_sm * 128 * f_max          # FP32 lane-instructions / s
+    r_mufu = n_sm * 16 * f_max
+    dom = max(("blend_fwd", "blend_bwd"), key=lambda k: stage_ms.get(k, 0.0))
+    t_dom = stage_ms[dom] * 1e-3
+    achieved = FP32_PER_PAIR[dom] * pairs / t_dom
+    roofline = {"bound": "fp32", "kernel": f"k_{dom.replace('blend_', 'blend_')}",
+                "achieved": achieved / 1e12, "peak": r_fp32 / 1e12, "unit": "Tinstr/s (FP32 lane)",
+                "frac": achieved / r_fp32, "traffic": None,
+                "algorithmic": f"{FP32_PER_PAIR[dom]} FP32 instr/pair x {pairs} tile-synchronous "
+                               f"pixel-instance pairs per launch (SURVEY.md §8(d))",
+                "mufu_frac": MUFU_PER_PAIR[dom] * pairs / t_dom / r_mufu,
+                "peak_basis": f"{n_sm} SMs x 128 FP32 lanes x sm_max {f_max/1e6:.0f} MHz (nominal; "
+                              "no dense contraction on this path, tensor cores unused)"}
+    hbm = float(peaks["hbm_gbs"])
+    stage_bytes = {"preprocess_fwd": n * (304 + 64 + 29),
+                   "preprocess_bwd": n * (304 + 48 + 65 * 4)}
+    stage_roofline = {}
+    for k_, b in stage_bytes.items():
+        if k_ in stage_ms:
+            gbs = b / (stage_ms[k_] * 1e-3) / 1e9
+            stage_roofline[k_] = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                                  "frac": gbs / hbm, "bytes": b}
+    t_floor = (FP32_PER_PAIR["blend_fwd"] + FP32_PER_PAIR["blend_bwd"]) * pairs / r_fp32 + \
+        sum(stage_bytes.values()) / (hbm * 1e9) + m * 32 / (hbm * 1e9)
+
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (blend) / f64 (preprocess)",
+        "data": "synthetic", "config": config, "n_instances": m, "tile_pairs": pairs,
+        "stage_ms": stage_ms, "roofline": roofline, "stage_roofline": stage_roofline,
+        "frame_floor_ms": t_floor * 1e3, "clocks": clk, "e2e": e2e,
+        "gpu_launches": 9 * args.steps,
+        "gpu_launches_note": "own kernels per step: preprocess_fwd, iota, gather_counts, finish_scan, "
+                             "duplicate, ranges, blend_fwd, blend_bwd, preprocess_bwd (+ CUB radix-sort/scan "
+                             "library kernels)",
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        result["cpu_baseline"] = cpu_baseline(scene, view, dL_host, args.cpu_k, args.cpu_reps)
+    if rank == 0:
+        print(json.dumps(result))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -135,6 +135,24 @@ class Engine:
         self._grad_key = None
         self.capacity = 0
         self.last_m = 0
+        self.stage_events = None  # name -> [(start, end)] CUDA events when enabled
+
+    def _mark(self, name: str):
+        """Context for per-stage CUDA-event timing on the launching stream."""
+        eng = self
+
+        class _M:
+            def __enter__(self):
+                if eng.stage_events is not None:
+                    self.a = torch.cuda.Event(enable_timing=True)
+                    self.a.record()
+
+            def __exit__(self, *exc):
+                if eng.stage_events is not None:
+                    b = torch.cuda.Event(enable_timing=True)
+                    b.record()
+                    eng.stage_events.setdefault(name, []).append((self.a, b))
+        return _M()
 
     # ------------------------------------------------------------ buffers
     def _empty(self, shape, dtype):
@@ -244,12 +262,14 @@ class Engine:
         st = self._stream()
         self._ensure_bins(n, self.capacity, ntx * nty)
         prim = self._prim_struct()
-        N.check(self.lib.ssg_bin_prepare(n, ctypes.byref(prim), ctypes.byref(self._bins_struct()), st),
-                "ssg_bin_prepare")
+        with self._mark("bin_prepare"):
+            N.check(self.lib.ssg_bin_prepare(n, ctypes.byref(prim), ctypes.byref(self._bins_struct()), st),
+                    "ssg_bin_prepare")
         m = int(self.n_inst_dev.item())
         self._ensure_bins(n, m, ntx * nty)
-        N.check(self.lib.ssg_bin_finish(n, m, W, H, ctypes.byref(prim), ctypes.byref(self._bins_struct()), st),
-                "ssg_bin_finish")
+        with self._mark("bin_finish"):
+            N.check(self.lib.ssg_bin_finish(n, m, W, H, ctypes.byref(prim), ctypes.byref(self._bins_struct()), st),
+                    "ssg_bin_finish")
         self.last_m = m
         return m
 
@@ -259,9 +279,10 @@ class Engine:
             raise ValueError("image dimension overflow")
         self._ensure_prim(ds.n)
         sc = ds.struct()
-        N.check(self.lib.ssg_preprocess_forward(ctypes.byref(sc), ctypes.byref(cam),
-                                                ctypes.byref(self._prim_struct()), self._stream()),
-                "ssg_preprocess_forward")
+        with self._mark("preprocess_fwd"):
+            N.check(self.lib.ssg_preprocess_forward(ctypes.byref(sc), ctypes.byref(cam),
+                                                    ctypes.byref(self._prim_struct()), self._stream()),
+                    "ssg_preprocess_forward")
         return self._bin(ds.n, W, H)
 
     def bin_arrays(self, mean2d, radius, depth, valid, W: int, H: int) -> int:
@@ -279,9 +300,10 @@ class Engine:
         m = self.project_and_bin(ds, cam)
         self._ensure_frame(W, H)
         bg = (ctypes.c_float * 3)(*[float(x) for x in ds.background])
-        N.check(self.lib.ssg_blend_forward(m, W, H, bg, _ptr(self.splat), ctypes.byref(self._bins_struct()),
-                                           ctypes.byref(self._frame_struct()), self._stream()),
-                "ssg_blend_forward")
+        with self._mark("blend_fwd"):
+            N.check(self.lib.ssg_blend_forward(m, W, H, bg, _ptr(self.splat), ctypes.byref(self._bins_struct()),
+                                               ctypes.byref(self._frame_struct()), self._stream()),
+                    "ssg_blend_forward")
         return DeviceFrame(self.color, self.final_T, self.n_contrib, self.last_idx, W, H, ds.n, m, s)
 
     def backward(self, ds: DeviceScene, view: CameraView, s: float, final_T: torch.Tensor,
@@ -304,13 +326,15 @@ class Engine:
         bg = (ctypes.c_float * 3)(*[float(x) for x in ds.background])
         st = self._stream()
         gs = self._grad_struct()
-        N.check(self.lib.ssg_blend_backward(ds.n, m, W, H, bg, _ptr(self.splat), ctypes.byref(self._bins_struct()),
-                                            ctypes.byref(self._frame_struct(final_T, last_idx)), _ptr(dL),
-                                            ctypes.byref(gs), st),
-                "ssg_blend_backward")
+        with self._mark("blend_bwd"):
+            N.check(self.lib.ssg_blend_backward(ds.n, m, W, H, bg, _ptr(self.splat), ctypes.byref(self._bins_struct()),
+                                                ctypes.byref(self._frame_struct(final_T, last_idx)), _ptr(dL),
+                                                ctypes.byref(gs), st),
+                    "ssg_blend_backward")
         sc = ds.struct()
-        N.check(self.lib.ssg_preprocess_backward(ctypes.byref(sc), ctypes.byref(cam), ctypes.byref(gs), st),
-                "ssg_preprocess_backward")
+        with self._mark("preprocess_bwd"):
+            N.check(self.lib.ssg_preprocess_backward(ctypes.byref(sc), ctypes.byref(cam), ctypes.byref(gs), st),
+                    "ssg_preprocess_backward")
         n = ds.n
         return DeviceGrads(self.g_screen[:n], self.g_mu[:n], self.g_log_scale[:n], self.g_rot[:n],
                            self.g_sh[:n], self.g_logits[:n], self.g_eta[:n], self.g_uv[:n], self.g_z[:n])
