@@ -33,6 +33,7 @@ def main():
     ds = DeviceScene.from_host(scene)
     dL = torch.from_numpy(np.random.default_rng(1).normal(size=(a.h, a.w, 3))).cuda().float()
     for rep in range(a.reps):
+        eng.stage_events = {}
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         ev[0].record()
         f = eng.forward(ds, view, 0.3)
@@ -41,7 +42,9 @@ def main():
         ev[2].record()
         torch.cuda.synchronize()
         print(f"rep {rep}: M={f.n_instances} fwd {ev[0].elapsed_time(ev[1]):.3f} ms "
-              f"bwd {ev[1].elapsed_time(ev[2]):.3f} ms", flush=True)
+              f"bwd {ev[1].elapsed_time(ev[2]):.3f} ms | " +
+              " ".join(f"{k} {a.elapsed_time(b):.3f}" for k, v in eng.stage_events.items() for a, b in v),
+              flush=True)
     print("img mean", float(f.color.mean()), "nc mean", float(f.n_contrib.float().mean()),
           "g_mu absmax", float(g.d_mu.abs().max()))
 
