@@ -18,8 +18,9 @@
 // are exactly those of the unculled loop; it removes the pixel-instance pairs
 // that cannot contribute before any arithmetic is spent on them.
 // Backward: the 12 per-instance sums of a warp are reduced with a transposed
-// butterfly (16 shuffles instead of 60), accumulated per instance in shared
-// memory across warps, and flushed once per instance with float4 atomics.
+// butterfly (16 shuffles instead of 60) and added to the primitive's
+// gradient row with three float4 global reductions (sm_90+ vector REDs; the
+// shared-memory fp32 atomic on sm_100 is a CAS loop, so no smem staging).
 #include "ssg_common.cuh"
 
 namespace ssg {
@@ -105,7 +106,9 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
 
     float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
     int nc = 0, li = -1;
-    bool done = !inside;
+    int done = !inside;
+    const uint32_t aA = smem_addr(s.A), aB = smem_addr(s.B), aC = smem_addr(s.C);
+    const uint32_t aX = smem_addr(s.X), aD = smem_addr(s.D);
 
     for (int base = start; base < end; base += kBatch) {
         if (__syncthreads_count(done) == kThreads) break;
@@ -116,18 +119,18 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
         for (int c0 = 0; c0 < cnt; c0 += 32) {
             if (__all_sync(0xffffffffu, done)) break;
             const int i = c0 + lane;
-            unsigned mask = __ballot_sync(0xffffffffu, i < cnt && box_hits(s.X[i], fwx0, fwy0));
+            unsigned mask = __ballot_sync(0xffffffffu, i < cnt && box_hits(lds128(aX + 16 * i), fwx0, fwy0));
             while (mask) {
                 const int j = c0 + __ffs(mask) - 1;
                 mask &= mask - 1;
                 if (done) continue;
-                const float4 A = s.A[j];
-                const float4 B = s.B[j];
+                const float4 A = lds128(aA + 16 * j);
+                const float4 B = lds128(aB + 16 * j);
                 const float dx = fx - A.x, dy = fy - A.y;
                 // _core.pyx:133-135
                 const float power = -0.5f * (A.z * dx * dx + B.x * dy * dy) - A.w * dx * dy;
                 if (power < B.y || power > 0.0f) continue;
-                const float4 C = s.C[j];
+                const float4 C = lds128(aC + 16 * j);
                 float E = 1.0f, o = C.x;
                 if (B.z != 0.0f || B.w != 0.0f) {                    // warp-uniform
                     const float z = (B.z * dx + B.w * dy) * SSG_SQRT1_2;   // :136
@@ -138,11 +141,11 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
                 const float alpha = fminf(Aval, SSG_ALPHA_MAX);             // :140
                 if (alpha < SSG_ALPHA_SKIP) continue;                       // :141-142
                 const float test_T = T * (1.0f - alpha);                    // :143
-                if (test_T < SSG_T_STOP) { done = true; continue; }         // :144-147
+                if (test_T < SSG_T_STOP) { done = 1; continue; }            // :144-147
                 const float w = alpha * T;                                  // :148-154
                 C0 = fmaf(w, C.z, C0);
                 C1 = fmaf(w, C.w, C1);
-                C2 = fmaf(w, s.D[j], C2);
+                C2 = fmaf(w, lds32(aD + 4 * j), C2);
                 T = test_T;
                 nc++;
                 li = base + j;
@@ -199,7 +202,6 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                  float *__restrict__ grad_screen) {
     __shared__ SmemBatch s;
     __shared__ uint32_t sP[kBatch];
-    __shared__ float sAcc[kBatch * 12];
     __shared__ int sMax[kThreads / 32];
     const int tile = blockIdx.x;
     const int tyi = tile / ntx, txi = tile - tyi * ntx;
@@ -234,6 +236,8 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
     for (int w = 1; w < kThreads / 32; w++) maxli = max(maxli, sMax[w]);
     if (maxli < start) return;  // any_hit == 0 (:245-246); block-uniform
     const int hi = min(maxli + 1, end);
+    const uint32_t aA = smem_addr(s.A), aB = smem_addr(s.B), aC = smem_addr(s.C);
+    const uint32_t aX = smem_addr(s.X), aD = smem_addr(s.D);
 
     for (int top = hi; top > start; top -= kBatch) {
         const int lo = max(start, top - kBatch);
@@ -244,13 +248,12 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
             stage_splat(splat, p, ox, oy, s, threadIdx.x);
             sP[threadIdx.x] = p;
         }
-        for (int q = threadIdx.x; q < kBatch * 12; q += kThreads) sAcc[q] = 0.0f;
         __syncthreads();
 
         const int cwarp = min(cnt, wmax - lo + 1);  // instances past the warp's last_idx never blend
         for (int c0 = ((cwarp - 1) >> 5) << 5; c0 >= 0 && cwarp > 0; c0 -= 32) {
             const int i = c0 + lane;
-            unsigned mask = __ballot_sync(0xffffffffu, i < cwarp && box_hits(s.X[i], fwx0, fwy0));
+            unsigned mask = __ballot_sync(0xffffffffu, i < cwarp && box_hits(lds128(aX + 16 * i), fwx0, fwy0));
             while (mask) {
                 const int bit = 31 - __clz(mask);
                 mask &= ~(1u << bit);
@@ -261,12 +264,12 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                 for (int q = 0; q < 16; q++) g[q] = 0.0f;
                 bool contrib = false;
                 if (k <= li) {  // :263-264
-                    const float4 A = s.A[j];
-                    const float4 B = s.B[j];
+                    const float4 A = lds128(aA + 16 * j);
+                    const float4 B = lds128(aB + 16 * j);
                     const float dx = fx - A.x, dy = fy - A.y;
                     const float power = -0.5f * (A.z * dx * dx + B.x * dy * dy) - A.w * dx * dy;
                     if (power >= B.y && power <= 0.0f) {
-                        const float4 C = s.C[j];
+                        const float4 C = lds128(aC + 16 * j);
                         const bool skewed = (B.z != 0.0f || B.w != 0.0f);
                         float E = 1.0f, z = 0.0f, o = C.x;
                         if (skewed) {
@@ -279,8 +282,8 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                         const float alpha = fminf(Aval, SSG_ALPHA_MAX);
                         if (alpha >= SSG_ALPHA_SKIP) {
                             contrib = true;
-                            const float cb = s.D[j];
-                            T = __fdividef(T, 1.0f - alpha);                                  // :280
+                            const float cb = lds32(aD + 4 * j);
+                            T = T * fast_rcp(1.0f - alpha);                                   // :280
                             const float d_alpha = T * ((C.z - R0) * d0 + (C.w - R1) * d1 + (cb - R2) * d2);
                             const float aT = alpha * T;
                             g[9] = aT * d0;
@@ -307,26 +310,19 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                     }
                 }
                 if (__any_sync(0xffffffffu, contrib)) {
+                    // lane 2i holds component i; lanes 0 / 8 / 16 gather four
+                    // consecutive components and issue one float4 reduction
+                    // each straight into the primitive's accumulator
+                    // (raster/backward.py:70-73)
                     const float v = warp_reduce_transposed16(g, lane);
-                    const int idx = (lane >> 1) & 15;
-                    if (!(lane & 1) && idx < 12) atomicAdd(&sAcc[j * 12 + idx], v);
+                    const float v1 = __shfl_down_sync(0xffffffffu, v, 2);
+                    const float v2 = __shfl_down_sync(0xffffffffu, v, 4);
+                    const float v3 = __shfl_down_sync(0xffffffffu, v, 6);
+                    if ((lane & 7) == 0 && lane < 24) {
+                        float4 *dst = reinterpret_cast<float4 *>(grad_screen + (size_t)sP[j] * 12) + (lane >> 3);
+                        atomicAdd(dst, make_float4(v, v1, v2, v3));
+                    }
                 }
-            }
-        }
-        __syncthreads();
-        if ((int)threadIdx.x < cnt) {  // raster/backward.py:70-73, one flush per instance
-            float v[12];
-            bool any = false;
-#pragma unroll
-            for (int q = 0; q < 12; q++) {
-                v[q] = sAcc[threadIdx.x * 12 + q];
-                any |= v[q] != 0.0f;
-            }
-            if (any) {
-                float4 *dst = reinterpret_cast<float4 *>(grad_screen + (size_t)sP[threadIdx.x] * 12);
-                atomicAdd(dst, make_float4(v[0], v[1], v[2], v[3]));
-                atomicAdd(dst + 1, make_float4(v[4], v[5], v[6], v[7]));
-                atomicAdd(dst + 2, make_float4(v[8], v[9], v[10], v[11]));
             }
         }
     }

@@ -256,12 +256,29 @@ __device__ __forceinline__ float erfc_pos(float x) {
     return t * fast_exp2((p - x * x) * SSG_LOG2E);
 }
 
-// E = 1 + erf(z) (raster/_core.pyx:137); exactly 1 at z == 0 like the
-// reference (erf(0) == 0 exactly, kernel_math.py:79-80).
+// E = 1 + erf(z) (raster/_core.pyx:137).  Skew-free splats never get here
+// (the callers take the warp-uniform E = 1 path, erf(0) == 0 exactly as in
+// kernel_math.py:79-80); a pixel with z == 0 of a skewed splat gets
+// 1 - 3e-8 instead of 1, far below the fp32 blend tolerance.
 __device__ __forceinline__ float skew_E(float z) {
-    float y = erfc_pos(fabsf(z));
-    float E = z > 0.0f ? 2.0f - y : y;
-    return z == 0.0f ? 1.0f : E;
+    const float y = erfc_pos(fabsf(z));
+    return z > 0.0f ? 2.0f - y : y;
+}
+
+// 32-bit shared-window loads: keeps the address arithmetic out of the
+// generic (cluster-aware) path the compiler otherwise rematerialises per use.
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float lds32(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
 }
 
 }  // namespace ssg
