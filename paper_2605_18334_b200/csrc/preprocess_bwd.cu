@@ -10,43 +10,53 @@
 
 namespace ssg {
 
-__device__ __forceinline__ void sh_basis_grad(int deg, double x, double y, double z, double (*g)[3]) {
-    // sh.py:57-103 (entries not written are zero)
-#pragma unroll
-    for (int k = 0; k < 16; k++) g[k][0] = g[k][1] = g[k][2] = 0.0;
-    if (deg < 1) return;
+// sum_k w[k] * d basis_k / d dir  (sh.py:57-103 contracted with w), without
+// materialising the (K,3) basis-gradient table.
+__device__ __forceinline__ void sh_dot_grad(int deg, double x, double y, double z, const double *w,
+                                            double *g) {
     const double C1 = 0.4886025119029199;
-    g[1][1] = -C1;
-    g[2][2] = C1;
-    g[3][0] = -C1;
+    g[0] = -C1 * w[3];
+    g[1] = -C1 * w[1];
+    g[2] = C1 * w[2];
     if (deg < 2) return;
     const double C20 = 1.0925484305920792, C21 = -1.0925484305920792, C22 = 0.31539156525252005,
                  C23 = -1.0925484305920792, C24 = 0.5462742152960396;
-    double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
-    g[4][0] = C20 * y; g[4][1] = C20 * x;
-    g[5][1] = C21 * z; g[5][2] = C21 * y;
-    g[6][0] = C22 * (-2.0 * x); g[6][1] = C22 * (-2.0 * y); g[6][2] = C22 * (4.0 * z);
-    g[7][0] = C23 * z; g[7][2] = C23 * x;
-    g[8][0] = C24 * (2.0 * x); g[8][1] = C24 * (-2.0 * y);
+    g[0] += C20 * y * w[4] + C22 * (-2.0 * x) * w[6] + C23 * z * w[7] + C24 * (2.0 * x) * w[8];
+    g[1] += C20 * x * w[4] + C21 * z * w[5] + C22 * (-2.0 * y) * w[6] + C24 * (-2.0 * y) * w[8];
+    g[2] += C21 * y * w[5] + C22 * (4.0 * z) * w[6] + C23 * x * w[7];
     if (deg < 3) return;
     const double C30 = -0.5900435899266435, C31 = 2.890611442640554, C32 = -0.4570457994644658,
                  C33 = 0.3731763325901154, C34 = -0.4570457994644658, C35 = 1.445305721320277,
                  C36 = -0.5900435899266435;
-    g[9][0] = C30 * 6.0 * xy; g[9][1] = C30 * (3.0 * xx - 3.0 * yy);
-    g[10][0] = C31 * yz; g[10][1] = C31 * xz; g[10][2] = C31 * xy;
-    g[11][0] = C32 * (-2.0 * xy); g[11][1] = C32 * (4.0 * zz - xx - 3.0 * yy); g[11][2] = C32 * (8.0 * yz);
-    g[12][0] = C33 * (-6.0 * xz); g[12][1] = C33 * (-6.0 * yz); g[12][2] = C33 * (6.0 * zz - 3.0 * xx - 3.0 * yy);
-    g[13][0] = C34 * (4.0 * zz - 3.0 * xx - yy); g[13][1] = C34 * (-2.0 * xy); g[13][2] = C34 * (8.0 * xz);
-    g[14][0] = C35 * (2.0 * xz); g[14][1] = C35 * (-2.0 * yz); g[14][2] = C35 * (xx - yy);
-    g[15][0] = C36 * (3.0 * xx - 3.0 * yy); g[15][1] = C36 * (-6.0 * xy);
+    const double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    g[0] += C30 * 6.0 * xy * w[9] + C31 * yz * w[10] + C32 * (-2.0 * xy) * w[11] + C33 * (-6.0 * xz) * w[12] +
+            C34 * (4.0 * zz - 3.0 * xx - yy) * w[13] + C35 * (2.0 * xz) * w[14] + C36 * (3.0 * xx - 3.0 * yy) * w[15];
+    g[1] += C30 * (3.0 * xx - 3.0 * yy) * w[9] + C31 * xz * w[10] + C32 * (4.0 * zz - xx - 3.0 * yy) * w[11] +
+            C33 * (-6.0 * yz) * w[12] + C34 * (-2.0 * xy) * w[13] + C35 * (-2.0 * yz) * w[14] + C36 * (-6.0 * xy) * w[15];
+    g[2] += C31 * xy * w[10] + C32 * (8.0 * yz) * w[11] + C33 * (6.0 * zz - 3.0 * xx - 3.0 * yy) * w[12] +
+            C34 * (8.0 * xz) * w[13] + C35 * (xx - yy) * w[14];
 }
 
-template <int DEG>
+// Geometry part: everything but the SH chain (run first; writes d_mu).
 __global__ void __launch_bounds__(128)
 k_preprocess_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
-    constexpr int K = (DEG + 1) * (DEG + 1);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= sc.n) return;
+    const float4 *sg4 = reinterpret_cast<const float4 *>(gr.screen + 12 * i);
+    const float4 s0 = sg4[0], s1 = sg4[1], s2 = sg4[2];
+    const bool zero = s0.x == 0.0f && s0.y == 0.0f && s0.z == 0.0f && s0.w == 0.0f && s1.x == 0.0f &&
+                      s1.y == 0.0f && s1.z == 0.0f && s1.w == 0.0f && s2.x == 0.0f && s2.y == 0.0f &&
+                      s2.z == 0.0f && s2.w == 0.0f;
+    if (zero) {  // no instance touched a pixel with dL != 0: every output is 0
+#pragma unroll
+        for (int j = 0; j < 3; j++) gr.d_mu[3 * i + j] = gr.d_log_scale[3 * i + j] = gr.d_eta[3 * i + j] = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 4; j++) gr.d_rot[4 * i + j] = 0.0f;
+        gr.d_opacity_logits[2 * i] = gr.d_opacity_logits[2 * i + 1] = 0.0f;
+        gr.g_uv[i] = 0.0f;
+        gr.g_z[i] = 0.0f;
+        return;
+    }
     double mu[3], ls[3], q4[4], eta[3];
     float logit[2];
 #pragma unroll
@@ -62,25 +72,20 @@ k_preprocess_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
     Proj P;
     project_geometry(cam, mu, ls, q4, logit, eta, P);
 
-    float *dsh = gr.d_sh + (size_t)i * 3 * K;
     if (!P.valid) {  // zero_invalid, projection.py:368-379; g_z -> 0 (:349)
 #pragma unroll
         for (int j = 0; j < 3; j++) gr.d_mu[3 * i + j] = gr.d_log_scale[3 * i + j] = gr.d_eta[3 * i + j] = 0.0f;
 #pragma unroll
         for (int j = 0; j < 4; j++) gr.d_rot[4 * i + j] = 0.0f;
-        for (int j = 0; j < 3 * K; j++) dsh[j] = 0.0f;
         gr.d_opacity_logits[2 * i] = gr.d_opacity_logits[2 * i + 1] = 0.0f;
         gr.g_uv[i] = 0.0f;
         gr.g_z[i] = 0.0f;
         return;
     }
-    const float4 *sg4 = reinterpret_cast<const float4 *>(gr.screen + 12 * i);
-    const float4 s0 = sg4[0], s1 = sg4[1], s2 = sg4[2];
     const double dm0 = s0.x, dm1 = s0.y;
     const double dc0 = s0.z, dc1 = s0.w, dc2 = s1.x;
     const double dsk0 = s1.y, dsk1 = s1.z;
     const double dop0 = s1.w, dop1 = s2.x;
-    const double dcol[3] = {s2.y, s2.z, s2.w};
     const double fx = cam.fx, fy = cam.fy, tz = P.tz;
     const double *R = cam.R;
 
@@ -224,46 +229,85 @@ k_preprocess_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
 #pragma unroll
     for (int j = 0; j < 3; j++) dmu[j] = dt0 * R[j] + dt1 * R[3 + j] + dt2 * R[6 + j];  // :353
 
-    // SH (:355-363)
-    const double dv0 = mu[0] - cam.campos[0], dv1 = mu[1] - cam.campos[1], dv2 = mu[2] - cam.campos[2];
-    const double dn = sqrt(dv0 * dv0 + dv1 * dv1 + dv2 * dv2);
-    const double dns = dn > 1e-12 ? dn : 1.0;
-    const double dx = dv0 / dns, dy = dv1 / dns, dz = dv2 / dns;
-    double basis[16];
-    sh_basis(DEG, dx, dy, dz, basis);
-    const float *shp = sc.sh + (size_t)i * 3 * K;
-    double col[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-    for (int k = 0; k < K; k++)
-#pragma unroll
-        for (int c = 0; c < 3; c++) col[c] += basis[k] * (double)shp[3 * k + c];
-    double dcc[3];
-#pragma unroll
-    for (int c = 0; c < 3; c++) dcc[c] = (col[c] + 0.5 > 0.0) ? dcol[c] : 0.0;
-#pragma unroll
-    for (int k = 0; k < K; k++)
-#pragma unroll
-        for (int c = 0; c < 3; c++) dsh[3 * k + c] = (float)(basis[k] * dcc[c]);
-    if (DEG > 0) {
-        double bg[16][3];
-        sh_basis_grad(DEG, dx, dy, dz, bg);
-        double dd[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-            const double w = (double)shp[3 * k] * dcc[0] + (double)shp[3 * k + 1] * dcc[1] +
-                             (double)shp[3 * k + 2] * dcc[2];
-#pragma unroll
-            for (int d = 0; d < 3; d++) dd[d] += w * bg[k][d];
-        }
-        const double inner = dx * dd[0] + dy * dd[1] + dz * dd[2];
-        dmu[0] += (dd[0] - dx * inner) / dns;
-        dmu[1] += (dd[1] - dy * inner) / dns;
-        dmu[2] += (dd[2] - dz * inner) / dns;
-    }
 #pragma unroll
     for (int j = 0; j < 3; j++) {
         gr.d_mu[3 * i + j] = (float)dmu[j];
         gr.d_eta[3 * i + j] = (float)geta[j];                               // :365-366
+    }
+}
+
+
+// SH part (projection.py:355-363, sh.py:25-109): d_sh = basis (x) dcolor on
+// the unclamped channels, plus the view-direction term added into d_mu.  A
+// warp stages its 32 primitives' coefficient rows (3K floats each) through
+// shared memory so global loads and stores are fully coalesced float4s.  An
+// invalid primitive has no tile instances, so its screen gradients are zero
+// and so are its outputs (zero_invalid, projection.py:368-379).
+template <int DEG>
+__global__ void __launch_bounds__(128)
+k_sh_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
+    constexpr int K = (DEG + 1) * (DEG + 1);
+    constexpr int ROW = 3 * K;                 // floats per primitive
+    __shared__ __align__(16) float tile[4][32 * ROW];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t first = ((int64_t)blockIdx.x * 4 + warp) * 32;
+    if (first >= sc.n) return;
+    const int nw = (int)(sc.n - first < 32 ? sc.n - first : 32);
+    float *t = tile[warp];
+    const float *src = sc.sh + first * ROW;
+    if ((ROW * nw) % 4 == 0 && (((uintptr_t)src) & 15) == 0) {
+        const float4 *s4 = reinterpret_cast<const float4 *>(src);
+        for (int q = lane; q < ROW * nw / 4; q += 32) reinterpret_cast<float4 *>(t)[q] = __ldg(s4 + q);
+    } else {
+        for (int q = lane; q < ROW * nw; q += 32) t[q] = __ldg(src + q);
+    }
+    __syncwarp();
+    const int64_t i = first + lane;
+    if (lane < nw) {
+        const float *sh = t + lane * ROW;
+        const float *sg = gr.screen + 12 * i;
+        const double dcol[3] = {sg[9], sg[10], sg[11]};
+        const double dv0 = sc.mu[3 * i] - cam.campos[0], dv1 = sc.mu[3 * i + 1] - cam.campos[1],
+                     dv2 = sc.mu[3 * i + 2] - cam.campos[2];
+        const double dn = sqrt(dv0 * dv0 + dv1 * dv1 + dv2 * dv2);
+        const double dns = dn > 1e-12 ? dn : 1.0;
+        const double x = dv0 / dns, y = dv1 / dns, z = dv2 / dns;
+        double basis[16];
+        sh_basis(DEG, x, y, z, basis);
+        double col[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < K; k++)
+#pragma unroll
+            for (int c = 0; c < 3; c++) col[c] += basis[k] * (double)sh[3 * k + c];
+        double dcc[3];
+#pragma unroll
+        for (int c = 0; c < 3; c++) dcc[c] = (col[c] + 0.5 > 0.0) ? dcol[c] : 0.0;
+        double w[16];
+#pragma unroll
+        for (int k = 0; k < K; k++)
+            w[k] = (double)sh[3 * k] * dcc[0] + (double)sh[3 * k + 1] * dcc[1] + (double)sh[3 * k + 2] * dcc[2];
+        double dd[3] = {0.0, 0.0, 0.0};
+        if (DEG > 0) sh_dot_grad(DEG, x, y, z, w, dd);
+        __syncwarp(__activemask());
+        float *out = t + lane * ROW;  // this lane's own row: safe to overwrite now
+#pragma unroll
+        for (int k = 0; k < K; k++)
+#pragma unroll
+            for (int c = 0; c < 3; c++) out[3 * k + c] = (float)(basis[k] * dcc[c]);
+        if (DEG > 0) {
+            const double inner = x * dd[0] + y * dd[1] + z * dd[2];
+            gr.d_mu[3 * i] += (float)((dd[0] - x * inner) / dns);
+            gr.d_mu[3 * i + 1] += (float)((dd[1] - y * inner) / dns);
+            gr.d_mu[3 * i + 2] += (float)((dd[2] - z * inner) / dns);
+        }
+    }
+    __syncwarp();
+    float *dst = gr.d_sh + first * ROW;
+    if ((ROW * nw) % 4 == 0 && (((uintptr_t)dst) & 15) == 0) {
+        float4 *d4 = reinterpret_cast<float4 *>(dst);
+        for (int q = lane; q < ROW * nw / 4; q += 32) d4[q] = reinterpret_cast<const float4 *>(t)[q];
+    } else {
+        for (int q = lane; q < ROW * nw; q += 32) dst[q] = t[q];
     }
 }
 
@@ -277,11 +321,14 @@ extern "C" int ssg_preprocess_backward(const ssg_scene *scene, const ssg_camera 
     if (scene->n == 0) return SSG_OK;
     cudaStream_t st = (cudaStream_t)stream;
     unsigned blocks = (unsigned)((scene->n + 127) / 128);
+    k_preprocess_backward<<<blocks, 128, 0, st>>>(*scene, *cam, *grads);
+    int rc = check_launch("k_preprocess_backward");
+    if (rc != SSG_OK) return rc;
     switch (scene->sh_degree) {
-        case 0: k_preprocess_backward<0><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
-        case 1: k_preprocess_backward<1><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
-        case 2: k_preprocess_backward<2><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
-        default: k_preprocess_backward<3><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
+        case 0: k_sh_backward<0><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
+        case 1: k_sh_backward<1><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
+        case 2: k_sh_backward<2><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
+        default: k_sh_backward<3><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
     }
-    return check_launch("k_preprocess_backward");
+    return check_launch("k_sh_backward");
 }
