@@ -105,10 +105,11 @@ typedef struct ssg_bin_buffers {
     int64_t capacity;           /* allocated instances */
     uint32_t *inst_prim;        /* (capacity) sorted primitive id per instance */
     uint16_t *inst_tile;        /* (capacity) sorted tile id per instance */
-    uint32_t *inst_prim_tmp;    /* (capacity) */
-    uint16_t *inst_tile_tmp;    /* (capacity) */
+    uint32_t *inst_prim_tmp;    /* unused (kept for layout stability; may be NULL) */
+    uint16_t *inst_tile_tmp;    /* unused (may be NULL) */
     int32_t *ranges;            /* (n_tiles, 2) half-open [start, end) */
-    void *temp;                 /* temporary storage for the sorts */
+    void *temp;                 /* temporary storage for the sorts and scans
+                                   (size from ssg_bin_temp_bytes) */
     size_t temp_bytes;
 } ssg_bin_buffers;
 
@@ -168,6 +169,13 @@ int ssg_blend_backward(int64_t n, int64_t m, int32_t width, int32_t height,
                        const float *dL_dpixels, const ssg_grad_buffers *grads, void *stream);
 int ssg_preprocess_backward(const ssg_scene *scene, const ssg_camera *cam,
                             const ssg_grad_buffers *grads, void *stream);
+
+/* ---- test hooks (used by tests/ only) ----------------------------------- */
+/* the binning radix sort in isolation: stable sort of (key, u32 value) by the
+ * low 8*npass key bits, in place; key_bytes 2 (tile ids) or 8 (depth keys) */
+size_t ssg_test_sort_temp_bytes(int64_t n, int key_bytes);
+int ssg_test_sort(void *keys, uint32_t *vals, int key_bytes, int iota, int64_t n, int npass,
+                  void *temp, void *stream);
 
 #ifdef __cplusplus
 }

@@ -2,110 +2,152 @@
 //
 // Reference: raster/tiles.py:43-79 (bin_arrays).  The reference emits one
 // instance per covered tile and lexsorts by (tile, depth, primitive id).
-// Here the same order is produced in two stable stages:
-//   1. sort primitives by their full 64-bit fp64 depth (stable, so equal
-//      depths keep primitive-id order)               -> depth rank
-//   2. emit each primitive's instances in depth-rank order, then stable-sort
-//      the instances by tile id (13-16 bit key)        -> (tile, depth, id)
-// Ranges are per-tile lower/upper bounds of the sorted tile ids, i.e.
-// exactly np.searchsorted(..., side="left"/"right") (tiles.py:76-78),
-// including the start==end position of empty tiles.
-#include <cub/cub.cuh>
-
+// Here the same order is produced in two stable stages, all hand-written:
+//   1. stable radix sort of primitives by their full 64-bit fp64 depth key
+//      (equal depths keep primitive-id order)            -> depth rank
+//   2. counts in depth-rank order, single-pass look-back scan -> offsets
+//   3. warp-cooperative duplication (coalesced writes) of each primitive's
+//      tiles in depth-rank order, then a stable radix sort of the instances
+//      by tile id (13-16 bit key, two passes)          -> (tile, depth, id)
+// Ranges are the per-tile [first, last+1) of the sorted tile ids with empty
+// tiles set to the insertion point, i.e. exactly np.searchsorted(...,
+// "left"/"right") (tiles.py:76-78).
+#include "radix_sort.cuh"
 #include "ssg_common.cuh"
 
 namespace ssg {
 
-static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
-
-static int tile_bits(int32_t n_tiles) {
+static int tile_passes(int32_t n_tiles) {
     int b = 1;
     while ((1 << b) < n_tiles) b++;
+    return (b + 7) / 8;
+}
+
+constexpr int kScanThreads = 256, kScanIPT = 16, kScanTile = kScanThreads * kScanIPT;
+
+struct BinTemp {
+    size_t sort_depth, sort_tile, scan_lookback, total;
+};
+
+static BinTemp bin_temp(int64_t n, int64_t capacity) {
+    BinTemp b;
+    b.sort_depth = radix::temp_bytes<uint64_t>(n > 0 ? n : 1);
+    b.sort_tile = radix::temp_bytes<uint16_t>(capacity > 0 ? capacity : 1);
+    b.scan_lookback = radix::align256(sizeof(uint64_t) * (size_t)((n + kScanTile - 1) / kScanTile + 1) + 256);
+    size_t m = b.sort_depth > b.sort_tile ? b.sort_depth : b.sort_tile;
+    b.total = m + b.scan_lookback;
     return b;
 }
 
-struct TempLayout {
-    size_t cub_bytes;
-    size_t off_keys, off_iota, off_cnt, total;
-};
-
-static cudaError_t temp_layout(int64_t n, int64_t capacity, int32_t n_tiles, TempLayout &L) {
-    size_t a = 0, b = 0, c = 0;
-    cudaError_t e;
-    int nn = (int)(n > 0 ? n : 1);
-    int cc = (int)(capacity > 0 ? capacity : 1);
-    e = cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint64_t *)nullptr, (uint64_t *)nullptr,
-                                        (const uint32_t *)nullptr, (uint32_t *)nullptr, nn, 0, 64);
-    if (e != cudaSuccess) return e;
-    e = cub::DeviceScan::InclusiveSum(nullptr, b, (const uint64_t *)nullptr, (uint64_t *)nullptr, nn);
-    if (e != cudaSuccess) return e;
-    e = cub::DeviceRadixSort::SortPairs(nullptr, c, (const uint16_t *)nullptr, (uint16_t *)nullptr,
-                                        (const uint32_t *)nullptr, (uint32_t *)nullptr, cc, 0,
-                                        tile_bits(n_tiles));
-    if (e != cudaSuccess) return e;
-    size_t m = a > b ? a : b;
-    m = m > c ? m : c;
-    L.cub_bytes = align256(m);
-    L.off_keys = L.cub_bytes;
-    L.off_iota = L.off_keys + align256(sizeof(uint64_t) * (size_t)nn);
-    L.off_cnt = L.off_iota + align256(sizeof(uint32_t) * (size_t)nn);
-    L.total = L.off_cnt + align256(sizeof(uint64_t) * (size_t)nn);
-    return cudaSuccess;
-}
-
-__global__ void k_iota(uint32_t *v, int64_t n) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) v[i] = (uint32_t)i;
-}
-
-__global__ void k_gather_counts(const uint32_t *order, const uint32_t *count, uint64_t *out, int64_t n) {
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < n) out[r] = count[order[r]];
-}
-
-__global__ void k_finish_scan(uint64_t *rank_offset, int64_t n, int64_t *n_instances) {
-    rank_offset[0] = 0;
-    *n_instances = (int64_t)rank_offset[n];
-}
-
-// tiles.py:59-70: the instances of one primitive in row-major tile order.
-__global__ void k_duplicate(const uint32_t *order, const uint64_t *rank_offset,
-                            const uint64_t *rect, int32_t ntx, int64_t n, uint16_t *inst_tile,
-                            uint32_t *inst_prim) {
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    uint64_t base = rank_offset[r], end = rank_offset[r + 1];
-    if (end == base) return;
-    uint32_t prim = order[r];
-    uint64_t rc = rect[prim];
-    int x0 = (int)(rc & 0xffff), x1 = (int)((rc >> 16) & 0xffff);
-    int y0 = (int)((rc >> 32) & 0xffff), y1 = (int)((rc >> 48) & 0xffff);
-    uint64_t k = base;
-    for (int ty = y0; ty < y1; ty++)
-        for (int tx = x0; tx < x1; tx++) {
-            inst_tile[k] = (uint16_t)(ty * ntx + tx);
-            inst_prim[k] = prim;
-            k++;
+// Counts in depth order + inclusive scan in one pass (decoupled look-back).
+// rank_offset[r+1] = sum of counts of ranks <= r; rank_offset[0] = 0.
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_counts(const uint32_t *__restrict__ order, const uint32_t *__restrict__ count, int64_t n,
+              uint64_t *__restrict__ rank_offset, uint64_t *__restrict__ lookback, int64_t *n_instances) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint64_t s_warp[kScanThreads / 32];
+    __shared__ uint64_t s_prefix;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    uint32_t *counter = reinterpret_cast<uint32_t *>(lookback + (n + kScanTile - 1) / kScanTile);
+    if (t == 0) s_tile = atomicAdd(counter, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t base = tile * kScanTile + (int64_t)t * kScanIPT;
+    uint64_t v[kScanIPT];
+    uint64_t sum = 0;
+#pragma unroll
+    for (int i = 0; i < kScanIPT; i++) {
+        const int64_t r = base + i;
+        v[i] = r < n ? count[order[r]] : 0u;
+        sum += v[i];
+    }
+    // block exclusive scan of the per-thread sums
+    uint64_t x = sum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+    }
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    uint64_t wpre = 0, total = 0;
+#pragma unroll
+    for (int ww = 0; ww < kScanThreads / 32; ww++) {
+        wpre += ww < w ? s_warp[ww] : 0ull;
+        total += s_warp[ww];
+    }
+    if (t == 0) {
+        uint64_t excl = 0;
+        if (tile == 0) {
+            atomicExch(reinterpret_cast<unsigned long long *>(lookback), radix::kFlagPre | total);
+        } else {
+            atomicExch(reinterpret_cast<unsigned long long *>(lookback + tile), radix::kFlagAgg | total);
+            for (int64_t p = tile - 1;; p--) {
+                const volatile uint64_t *q = lookback + p;
+                uint64_t val = *q;
+                while ((val >> 62) == 0) val = *q;
+                excl += val & radix::kValMask;
+                if ((val >> 62) == 2) break;
+            }
+            atomicExch(reinterpret_cast<unsigned long long *>(lookback + tile), radix::kFlagPre | (excl + total));
         }
+        s_prefix = excl;
+        if (base <= n && tile == (n - 1) / kScanTile) *n_instances = (int64_t)(excl + total);
+        if (tile == 0) rank_offset[0] = 0;
+    }
+    __syncthreads();
+    uint64_t run = s_prefix + wpre + x - sum;
+#pragma unroll
+    for (int i = 0; i < kScanIPT; i++) {
+        const int64_t r = base + i;
+        run += v[i];
+        if (r < n) rank_offset[r + 1] = run;
+    }
 }
 
-// np.searchsorted(inst_tile, t, 'left') / (t, 'right') for every tile id
-__global__ void k_ranges(const uint16_t *inst_tile, int64_t m, int32_t n_tiles, int32_t *ranges) {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n_tiles) return;
-    int64_t lo = 0, hi = m;
-    while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        if ((int)inst_tile[mid] < t) lo = mid + 1; else hi = mid;
+// tiles.py:59-70: each primitive's instances in row-major tile order, in
+// depth-rank order.  A warp owns 32 consecutive ranks, whose instances are
+// contiguous in the output; lanes stride over that span (coalesced stores)
+// and find their primitive by a 5-step shuffle binary search.
+__global__ void __launch_bounds__(256)
+k_duplicate(const uint32_t *__restrict__ order, const uint64_t *__restrict__ rank_offset,
+            const uint64_t *__restrict__ rect, int32_t ntx, int64_t n, uint16_t *__restrict__ inst_tile,
+            uint32_t *__restrict__ inst_prim) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane;
+    if (r0 >= n) return;
+    const int64_t r = r0 + lane;
+    const uint64_t off = rank_offset[r < n ? r : n];
+    const uint64_t end = __shfl_sync(0xffffffffu, rank_offset[r0 + 32 < n ? r0 + 32 : n], 0);
+    uint32_t prim = 0;
+    uint64_t rc = 0;
+    if (r < n) {
+        prim = order[r];
+        const uint64_t nxt = rank_offset[r + 1];
+        if (nxt > off) rc = rect[prim];
     }
-    int64_t s = lo;
-    hi = m;
-    while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        if ((int)inst_tile[mid] <= t) lo = mid + 1; else hi = mid;
+    const uint64_t first = __shfl_sync(0xffffffffu, off, 0);
+    const uint32_t rlo = (uint32_t)rc, rhi = (uint32_t)(rc >> 32);
+    for (uint64_t g0 = first; g0 < end; g0 += 32) {  // warp-uniform trip count (shuffles below)
+        const uint64_t g = g0 + lane;
+        int j = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const uint64_t oc = __shfl_sync(0xffffffffu, off, j + step);
+            if (oc <= g) j += step;
+        }
+        const uint64_t oj = __shfl_sync(0xffffffffu, off, j);
+        const uint32_t lo = __shfl_sync(0xffffffffu, rlo, j), hi = __shfl_sync(0xffffffffu, rhi, j);
+        const uint32_t pj = __shfl_sync(0xffffffffu, prim, j);
+        const int x0 = (int)(lo & 0xffff), x1 = (int)(lo >> 16), y0 = (int)(hi & 0xffff);
+        const int nx = x1 - x0;
+        if (g < end) {
+            const int local = (int)(g - oj);
+            const int ty = y0 + local / nx, tx = x0 + local % nx;
+            inst_tile[g] = (uint16_t)(ty * ntx + tx);
+            inst_prim[g] = pj;
+        }
     }
-    ranges[2 * t] = (int32_t)s;
-    ranges[2 * t + 1] = (int32_t)lo;
 }
 
 // Binning from caller-provided screen arrays (tiles.py:43-57 inputs), used by
@@ -119,9 +161,51 @@ __global__ void k_rects_from_arrays(int64_t n, const double *mean2d, const doubl
     bool v = valid[i] != 0;
     count[i] = tile_rect(mean2d[2 * i], mean2d[2 * i + 1], radius[i], v, ntx, nty, rc);
     rect[i] = rc;
-    // order-preserving bits for any finite double (sign flip for negatives)
+    // order-preserving bits for any finite double (sign flip for negatives);
+    // the all-ones pattern is reserved for primitives without instances
     uint64_t b = (uint64_t)__double_as_longlong(depth[i] == 0.0 ? 0.0 : depth[i]);
-    key[i] = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    uint64_t kk = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    key[i] = count[i] ? (kk == ~0ull ? kk - 1 : kk) : ~0ull;
+}
+
+// Per-tile [first, last+1) of the sorted tile ids; empty tiles marked -1.
+__global__ void k_tile_bounds(const uint16_t *__restrict__ tile, int64_t m, int32_t *__restrict__ ranges) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const int t = tile[i];
+    if (i == 0 || tile[i - 1] != t) ranges[2 * t] = (int32_t)i;
+    if (i == m - 1 || tile[i + 1] != t) ranges[2 * t + 1] = (int32_t)(i + 1);
+}
+
+// Empty tiles get start == end == first instance of the next non-empty tile
+// (M if none): a block-wide suffix-min over the tile starts.
+__global__ void __launch_bounds__(1024) k_fill_empty(int32_t *ranges, int32_t n_tiles, int32_t m) {
+    __shared__ int32_t s_min[1024];
+    const int t = threadIdx.x;
+    const int chunk = (n_tiles + 1023) / 1024;
+    const int lo = t * chunk, hi = min(lo + chunk, n_tiles);
+    int32_t mn = INT32_MAX;
+    for (int i = lo; i < hi; i++)
+        if (ranges[2 * i] >= 0) { mn = ranges[2 * i]; break; }
+    s_min[t] = mn;
+    __syncthreads();
+    // suffix min over chunks (Hillis-Steele, right to left)
+    for (int off = 1; off < 1024; off <<= 1) {
+        const int32_t o = t + off < 1024 ? s_min[t + off] : INT32_MAX;
+        __syncthreads();
+        s_min[t] = min(s_min[t], o);
+        __syncthreads();
+    }
+    int32_t next = t + 1 < 1024 ? s_min[t + 1] : INT32_MAX;
+    if (next == INT32_MAX) next = m;
+    for (int i = hi - 1; i >= lo; i--) {
+        if (ranges[2 * i] >= 0) {
+            next = ranges[2 * i];
+        } else {
+            ranges[2 * i] = next;
+            ranges[2 * i + 1] = next;
+        }
+    }
 }
 
 }  // namespace ssg
@@ -141,10 +225,7 @@ extern "C" int ssg_bin_rects(int64_t n, const double *mean2d, const double *radi
 extern "C" int ssg_bin_temp_bytes(int64_t n, int64_t capacity, int32_t n_tiles, size_t *bytes) {
     using namespace ssg;
     if (!bytes || n < 0 || capacity < 0 || n_tiles < 1 || n_tiles > 65536) return SSG_ERR_INVALID_ARGUMENT;
-    TempLayout L;
-    cudaError_t e = temp_layout(n, capacity, n_tiles, L);
-    if (e != cudaSuccess) { set_error("cub temp query", e); return SSG_ERR_CUDA; }
-    *bytes = L.total;
+    *bytes = bin_temp(n, capacity).total;
     return SSG_OK;
 }
 
@@ -159,25 +240,19 @@ extern "C" int ssg_bin_prepare(int64_t n, const ssg_prim_buffers *prim, const ss
         if (e != cudaSuccess) { set_error("memset", e); return SSG_ERR_CUDA; }
         return SSG_OK;
     }
-    TempLayout L;
-    cudaError_t e = temp_layout(n, bins->capacity, 1, L);
-    if (e != cudaSuccess) { set_error("cub temp query", e); return SSG_ERR_CUDA; }
+    const BinTemp L = bin_temp(n, bins->capacity);
     if (bins->temp_bytes < L.total) return SSG_ERR_CAPACITY;
     char *tmp = (char *)bins->temp;
-    uint64_t *keys_sorted = (uint64_t *)(tmp + L.off_keys);
-    uint32_t *iota = (uint32_t *)(tmp + L.off_iota);
-    uint64_t *cnt = (uint64_t *)(tmp + L.off_cnt);
-    unsigned blocks = (unsigned)((n + 255) / 256);
-    k_iota<<<blocks, 256, 0, st>>>(iota, n);
-    size_t cb = L.cub_bytes;
-    e = cub::DeviceRadixSort::SortPairs(tmp, cb, prim->depth_key, keys_sorted, iota, bins->depth_order,
-                                        (int)n, 0, 64, st);
+    // 1. stable sort of primitive ids by depth key (the key buffer is consumed)
+    cudaError_t e = radix::sort_pairs<uint64_t>(prim->depth_key, bins->depth_order, true, n, 8, tmp, st);
     if (e != cudaSuccess) { set_error("depth sort", e); return SSG_ERR_CUDA; }
-    k_gather_counts<<<blocks, 256, 0, st>>>(bins->depth_order, prim->tile_count, cnt, n);
-    cb = L.cub_bytes;
-    e = cub::DeviceScan::InclusiveSum(tmp, cb, cnt, bins->rank_offset + 1, (int)n, st);
-    if (e != cudaSuccess) { set_error("count scan", e); return SSG_ERR_CUDA; }
-    k_finish_scan<<<1, 1, 0, st>>>(bins->rank_offset, n, bins->n_instances);
+    // 2. counts in depth order, scanned
+    uint64_t *lb = (uint64_t *)(tmp + (L.total - L.scan_lookback));
+    const int64_t scan_tiles = (n + kScanTile - 1) / kScanTile;
+    e = cudaMemsetAsync(lb, 0, sizeof(uint64_t) * (scan_tiles + 1), st);
+    if (e != cudaSuccess) { set_error("memset scan", e); return SSG_ERR_CUDA; }
+    k_scan_counts<<<(unsigned)scan_tiles, kScanThreads, 0, st>>>(bins->depth_order, prim->tile_count, n,
+                                                                bins->rank_offset, lb, bins->n_instances);
     return check_launch("ssg_bin_prepare");
 }
 
@@ -190,20 +265,35 @@ extern "C" int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t heigh
     int32_t n_tiles = ntx * nty;
     if (n_tiles > 65536) return SSG_ERR_INVALID_ARGUMENT;
     cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(bins->ranges, 0xff, sizeof(int32_t) * 2 * (size_t)n_tiles, st);
+    if (e != cudaSuccess) { set_error("memset ranges", e); return SSG_ERR_CUDA; }
     if (m > 0) {
-        TempLayout L;
-        cudaError_t e = temp_layout(n, bins->capacity, n_tiles, L);
-        if (e != cudaSuccess) { set_error("cub temp query", e); return SSG_ERR_CUDA; }
+        const BinTemp L = bin_temp(n, bins->capacity);
         if (bins->temp_bytes < L.total) return SSG_ERR_CAPACITY;
-        k_duplicate<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-            bins->depth_order, bins->rank_offset, prim->tile_rect, ntx, n, bins->inst_tile_tmp,
-            bins->inst_prim_tmp);
-        size_t cb = L.cub_bytes;
-        e = cub::DeviceRadixSort::SortPairs(bins->temp, cb, bins->inst_tile_tmp, bins->inst_tile,
-                                            bins->inst_prim_tmp, bins->inst_prim, (int)m, 0,
-                                            tile_bits(n_tiles), st);
+        k_duplicate<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(bins->depth_order, bins->rank_offset,
+                                                                 prim->tile_rect, ntx, n, bins->inst_tile,
+                                                                 bins->inst_prim);
+        e = radix::sort_pairs<uint16_t>(bins->inst_tile, bins->inst_prim, false, m, tile_passes(n_tiles),
+                                        bins->temp, st);
         if (e != cudaSuccess) { set_error("tile sort", e); return SSG_ERR_CUDA; }
+        k_tile_bounds<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(bins->inst_tile, m, bins->ranges);
     }
-    k_ranges<<<(n_tiles + 255) / 256, 256, 0, st>>>(bins->inst_tile, m, n_tiles, bins->ranges);
+    k_fill_empty<<<1, 1024, 0, st>>>(bins->ranges, n_tiles, (int32_t)m);
     return check_launch("ssg_bin_finish");
+}
+
+// ---- test hooks (tests/ only): the radix sort in isolation -------------
+extern "C" size_t ssg_test_sort_temp_bytes(int64_t n, int key_bytes) {
+    using namespace ssg;
+    return key_bytes == 2 ? radix::temp_bytes<uint16_t>(n) : radix::temp_bytes<uint64_t>(n);
+}
+
+extern "C" int ssg_test_sort(void *keys, uint32_t *vals, int key_bytes, int iota, int64_t n, int npass,
+                             void *temp, void *stream) {
+    using namespace ssg;
+    cudaError_t e = key_bytes == 2
+        ? radix::sort_pairs<uint16_t>((uint16_t *)keys, vals, iota != 0, n, npass, temp, (cudaStream_t)stream)
+        : radix::sort_pairs<uint64_t>((uint64_t *)keys, vals, iota != 0, n, npass, temp, (cudaStream_t)stream);
+    if (e != cudaSuccess) { set_error("test sort", e); return SSG_ERR_CUDA; }
+    return SSG_OK;
 }

@@ -193,8 +193,6 @@ class Engine:
         if cap != self.capacity:
             self.inst_prim = self._empty((cap,), torch.int32)
             self.inst_tile = self._empty((cap,), torch.int16)
-            self.inst_prim_tmp = self._empty((cap,), torch.int32)
-            self.inst_tile_tmp = self._empty((cap,), torch.int16)
             self.capacity = cap
         self.ranges = self._empty((n_tiles, 2), torch.int32)
         nbytes = ctypes.c_size_t(0)
@@ -209,7 +207,6 @@ class Engine:
         b.capacity = self.capacity
         if self.capacity > 0:
             b.inst_prim, b.inst_tile = _ptr(self.inst_prim), _ptr(self.inst_tile)
-            b.inst_prim_tmp, b.inst_tile_tmp = _ptr(self.inst_prim_tmp), _ptr(self.inst_tile_tmp)
         if self._bins_key is not None:
             b.ranges, b.temp, b.temp_bytes = _ptr(self.ranges), _ptr(self.temp), self.temp.numel()
         return b

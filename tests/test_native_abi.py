@@ -16,7 +16,7 @@ HEADER = os.path.join(ROOT, "include", "ssg_b200.h")
 
 def declared_functions():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"^(?:int|void|const char \*)\s*\*?\s*(ssg_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^(?:int|void|size_t|const char \*)\s*\*?\s*(ssg_\w+)\s*\(", src, re.M)))
 
 
 def test_header_declares_the_exports():
