@@ -5,13 +5,12 @@
 // of the keys; a one-block scan turns them into bucket bases and drops passes
 // whose digit is the same for every (valid) key (the fp64 depth keys of a
 // scene share their sign/exponent prefix, the 13-bit tile keys need only two
-// passes).  Each pass is then ONE kernel: a CTA takes the next 4096-key tile
-// (tile ids from an atomic counter, so predecessors are always running), ranks
+// passes).  Each pass is reduce-then-scan: a CTA per key tile counts, ranks
 // its keys stably inside shared memory (warp-striped order, __match_any_sync
-// per step), publishes its per-digit counts and resolves its global offsets
-// by decoupled look-back over the preceding tiles (flag and value in one
-// 64-bit word), reorders the tile by digit in shared memory and writes it
-// out in digit runs (coalesced).
+// per step), takes its per-digit global offsets from an upsweep (per-tile
+// digit counts) + per-digit row scan -- no inter-CTA spin waits -- reorders
+// the tile by digit in shared memory and writes it out in digit runs
+// (coalesced).
 #pragma once
 
 #include "ssg_common.cuh"
@@ -20,8 +19,6 @@ namespace ssg {
 namespace radix {
 
 constexpr int kThreads = 256;
-constexpr int kIPT = 16;                      // items per thread
-constexpr int kTile = kThreads * kIPT;        // 4096 keys per tile
 constexpr int kMaxPasses = 8;
 constexpr uint64_t kFlagAgg = 1ull << 62;     // tile aggregate published
 constexpr uint64_t kFlagPre = 2ull << 62;     // inclusive prefix published
@@ -32,11 +29,13 @@ struct KeyTraits;
 template <>
 struct KeyTraits<uint16_t> {
     static constexpr bool has_invalid = false;
+    static constexpr int ipt = 8;              // 2048-key tiles: M ~ 1e7 instances
     static __device__ __forceinline__ bool valid(uint16_t) { return true; }
 };
 template <>
 struct KeyTraits<uint64_t> {
     static constexpr bool has_invalid = true;
+    static constexpr int ipt = 8;              // 2048-key tiles
     // the depth key of a primitive that emits no instances is ~0: its
     // position is irrelevant, so it does not veto skipping a constant digit
     static __device__ __forceinline__ bool valid(uint64_t k) { return k != ~0ull; }
@@ -53,12 +52,15 @@ struct Control {                       // device-side pass schedule
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
-__host__ __device__ inline int64_t num_tiles(int64_t n) { return (n + kTile - 1) / kTile; }
+template <typename K>
+__host__ __device__ constexpr int tile_keys() { return kThreads * KeyTraits<K>::ipt; }
+template <typename K>
+__host__ __device__ inline int64_t num_tiles(int64_t n) { return (n + tile_keys<K>() - 1) / tile_keys<K>(); }
 
-// temp = [Control | lookback kMaxPasses x tiles x 256 u64 | keys_alt | vals_alt]
+// temp = [Control | tile_counts 256 x tiles u32 | keys_alt | vals_alt]
 template <typename K>
 inline size_t temp_bytes(int64_t n) {
-    return align256(sizeof(Control)) + align256(sizeof(uint64_t) * 256 * kMaxPasses * num_tiles(n)) +
+    return align256(sizeof(Control)) + align256(sizeof(uint32_t) * 256 * num_tiles<K>(n)) +
            align256(sizeof(K) * n) + align256(sizeof(uint32_t) * n);
 }
 
@@ -84,6 +86,9 @@ __global__ void __launch_bounds__(256) k_hist(const K *__restrict__ keys, int64_
             if (KeyTraits<K>::has_invalid && v) atomicAdd(&h_val[p][d], 1u);
         }
     }
+    // (the grid-stride loop above is not warp-uniform at the tail, so the
+    // per-key atomics are not warp-aggregated; contention is low because the
+    // keys of neighbouring threads differ in their low digits)
     nv = __reduce_add_sync(0xffffffffu, nv);
     if ((threadIdx.x & 31) == 0 && nv) atomicAdd(&s_nvalid, nv);
     __syncthreads();
@@ -133,21 +138,96 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
-// Pass `k` of the schedule (no-op when k >= n_active).  Ping-pong: even k
-// reads buffer 0, writes buffer 1.  vals_in == nullptr on the first pass
-// means value = input position (iota).
+// Per-tile digit counts of pass k -> tile_counts[digit][tile] (digit-major).
 template <typename K>
-__global__ void __launch_bounds__(kThreads) k_onesweep(K *__restrict__ key0, K *__restrict__ key1,
-                                                       uint32_t *__restrict__ val0, uint32_t *__restrict__ val1,
-                                                       bool iota_vals, int64_t n, int k_pass, Control *ctl,
-                                                       uint64_t *__restrict__ lookback_all) {
+__global__ void __launch_bounds__(kThreads) k_upsweep(const K *__restrict__ key0, const K *__restrict__ key1,
+                                                      int64_t n, int k_pass, const Control *ctl,
+                                                      uint32_t *__restrict__ tile_counts) {
+    if (k_pass >= ctl->n_active) return;
+    constexpr int kIPT = KeyTraits<K>::ipt, kTile = tile_keys<K>();
+    __shared__ uint32_t s_cnt[kThreads / 32][256];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    for (int q = t; q < (kThreads / 32) * 256; q += kThreads) (&s_cnt[0][0])[q] = 0;
+    __syncthreads();
+    const int shift = 8 * ctl->active[k_pass];
+    const K *kin = (k_pass & 1) ? key1 : key0;
+    const int64_t tile = blockIdx.x, base = tile * kTile;
+    const uint32_t lt = lanemask_lt();
+    uint32_t dg[kIPT];
+#pragma unroll
+    for (int i = 0; i < kIPT; i++) {  // all loads in flight before the ranking chain
+        const int64_t idx = base + w * (32 * kIPT) + i * 32 + lane;
+        dg[i] = idx < n ? ((uint32_t)(kin[idx] >> shift) & 255u) : 256u;
+    }
+#pragma unroll
+    for (int i = 0; i < kIPT; i++) {
+        const uint32_t d = dg[i];
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        if (d < 256u && (peers & lt) == 0) s_cnt[w][d] += __popc(peers);  // one writer per digit per warp
+        __syncwarp();
+    }
+    __syncthreads();
+    uint32_t c = 0;
+#pragma unroll
+    for (int ww = 0; ww < kThreads / 32; ww++) c += s_cnt[ww][t];
+    tile_counts[(size_t)t * num_tiles<K>(n) + tile] = c;
+}
+
+// Exclusive scan of each digit row of tile_counts (one block per digit).
+__global__ void __launch_bounds__(1024) k_rowscan(uint32_t *tile_counts, int64_t ntiles, int k_pass,
+                                                  const Control *ctl) {
+    if (k_pass >= ctl->n_active) return;
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_carry;
+    uint32_t *row = tile_counts + (size_t)blockIdx.x * ntiles;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    if (t == 0) s_carry = 0;
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < ntiles; c0 += 1024) {
+        const int64_t i = c0 + t;
+        const uint32_t v = i < ntiles ? row[i] : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+            if (lane >= off) x += y;
+        }
+        if (lane == 31) s_warp[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            uint32_t z = s_warp[lane];
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, z, off);
+                if (lane >= off) z += y;
+            }
+            s_warp[lane] = z;
+        }
+        __syncthreads();
+        const uint32_t carry = s_carry;
+        const uint32_t excl = carry + (w > 0 ? s_warp[w - 1] : 0u) + x - v;
+        if (i < ntiles) row[i] = excl;
+        __syncthreads();
+        if (t == 1023) s_carry = excl + v;
+        __syncthreads();
+    }
+}
+
+// Scatter of pass `k` of the schedule (no-op when k >= n_active).
+// Ping-pong: even k reads buffer 0, writes buffer 1.  With iota_vals the
+// first executed pass generates the values (input positions).
+template <typename K>
+__global__ void __launch_bounds__(kThreads) k_downsweep(K *__restrict__ key0, K *__restrict__ key1,
+                                                        uint32_t *__restrict__ val0, uint32_t *__restrict__ val1,
+                                                        bool iota_vals, int64_t n, int k_pass, const Control *ctl,
+                                                        const uint32_t *__restrict__ tile_counts) {
     if (k_pass >= ctl->n_active) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K *s_keys = reinterpret_cast<K *>(smem_raw);
+    constexpr int kIPT = KeyTraits<K>::ipt, kTile = tile_keys<K>();
     uint32_t *s_vals = reinterpret_cast<uint32_t *>(smem_raw + sizeof(K) * kTile);
     __shared__ uint32_t s_wcnt[kThreads / 32][256];
     __shared__ uint32_t s_excl[256], s_tstart[256], s_warp[8];
-    __shared__ uint32_t s_tile;
 
     const int digit_idx = ctl->active[k_pass];
     const int shift = 8 * digit_idx;
@@ -156,14 +236,12 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(K *__restrict__ key0, K *
     const uint32_t *vin = (k_pass & 1) ? val1 : val0;
     uint32_t *vout = (k_pass & 1) ? val0 : val1;
     const bool gen_vals = iota_vals && k_pass == 0;
-    const int64_t ntiles = num_tiles(n);
-    uint64_t *lookback = lookback_all + (size_t)k_pass * ntiles * 256;
+    const int64_t ntiles = num_tiles<K>(n);
 
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    if (t == 0) s_tile = atomicAdd(&ctl->tile_counter[k_pass], 1u);
     for (int q = t; q < (kThreads / 32) * 256; q += kThreads) (&s_wcnt[0][0])[q] = 0;
     __syncthreads();
-    const int64_t tile = s_tile;
+    const int64_t tile = blockIdx.x;
     const int64_t base = tile * kTile;
     const int tile_n = (int)(n - base < kTile ? n - base : kTile);
 
@@ -200,24 +278,9 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(K *__restrict__ key0, K *
         run += c;
     }
     const uint32_t total = run;
-    // decoupled look-back over the preceding tiles for digit t
-    uint64_t *slot = lookback + (size_t)tile * 256 + t;
-    uint32_t excl = 0;
-    if (tile == 0) {
-        atomicExch(reinterpret_cast<unsigned long long *>(slot), (unsigned long long)(kFlagPre | total));
-    } else {
-        atomicExch(reinterpret_cast<unsigned long long *>(slot), (unsigned long long)(kFlagAgg | total));
-        int64_t p = tile - 1;
-        while (true) {
-            const volatile uint64_t *q = lookback + (size_t)p * 256 + t;
-            uint64_t v = *q;
-            while ((v >> 62) == 0) v = *q;
-            excl += (uint32_t)(v & kValMask);
-            if ((v >> 62) == 2) break;
-            p--;
-        }
-        atomicExch(reinterpret_cast<unsigned long long *>(slot), (unsigned long long)(kFlagPre | (excl + total)));
-    }
+    // offset of this tile's digit-t run among all keys with digit t
+    // (exclusive scan over tiles produced by k_upsweep + k_rowscan)
+    const uint32_t excl = tile_counts[(size_t)t * ntiles + tile];
     s_excl[t] = ctl->base[digit_idx][t] + excl;
     // exclusive scan of the tile's digit counts -> start of each digit run
     uint32_t x = total;
@@ -283,28 +346,30 @@ inline cudaError_t sort_pairs(K *keys0, uint32_t *vals0, bool iota_vals, int64_t
     char *tp = (char *)temp;
     Control *ctl = (Control *)tp;
     tp += align256(sizeof(Control));
-    uint64_t *lookback = (uint64_t *)tp;
-    const size_t lb_bytes = sizeof(uint64_t) * 256 * kMaxPasses * num_tiles(n);
-    tp += align256(lb_bytes);
+    uint32_t *tile_counts = (uint32_t *)tp;
+    const int64_t ntiles = num_tiles<K>(n);
+    tp += align256(sizeof(uint32_t) * 256 * ntiles);
     K *keys1 = (K *)tp;
     tp += align256(sizeof(K) * n);
     uint32_t *vals1 = (uint32_t *)tp;
     cudaError_t e = cudaMemsetAsync(ctl, 0, sizeof(Control), st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(lookback, 0, sizeof(uint64_t) * 256 * npass * num_tiles(n), st);
     if (e != cudaSuccess) return e;
     const int hist_blocks = (int)((n + 255) / 256 < 4 * 148 ? (n + 255) / 256 : 4 * 148);
     k_hist<K><<<hist_blocks, 256, 0, st>>>(keys0, n, npass, ctl);
     k_schedule<<<1, 256, 0, st>>>(ctl, npass, n);
-    const size_t smem = (sizeof(K) + sizeof(uint32_t)) * kTile;
+    const size_t smem = (sizeof(K) + sizeof(uint32_t)) * tile_keys<K>();
     static bool attr_set = false;
     if (!attr_set) {
-        e = cudaFuncSetAttribute(k_onesweep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaFuncSetAttribute(k_downsweep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    const unsigned grid = (unsigned)num_tiles(n);
-    for (int k = 0; k < npass; k++)
-        k_onesweep<K><<<grid, kThreads, smem, st>>>(keys0, keys1, vals0, vals1, iota_vals, n, k, ctl, lookback);
+    for (int k = 0; k < npass; k++) {
+        k_upsweep<K><<<(unsigned)ntiles, kThreads, 0, st>>>(keys0, keys1, n, k, ctl, tile_counts);
+        k_rowscan<<<256, 1024, 0, st>>>(tile_counts, ntiles, k, ctl);
+        k_downsweep<K><<<(unsigned)ntiles, kThreads, smem, st>>>(keys0, keys1, vals0, vals1, iota_vals, n, k,
+                                                                ctl, tile_counts);
+    }
     k_settle<K><<<(unsigned)hist_blocks, 256, 0, st>>>(ctl, keys1, keys0, vals1, vals0, iota_vals, n);
     return cudaGetLastError();
 }
