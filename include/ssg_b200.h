@@ -19,6 +19,8 @@
  *   ssg_blend_backward       raster/_core.pyx:315-343 backward_tiles fused with the
  *                            per-primitive slot reduction of raster/backward.py:70-73
  *   ssg_preprocess_backward  projection.py:255-379 projection_backward
+ *   ssg_blend_backward_slots raster/_core.pyx:315-343 backward_tiles as is (per-instance
+ *                            slots), for the reference's kernel plugin slot
  * The Python host layer (paper_2605_18334_b200.raster) keeps the reference's
  * render_forward / render_backward signatures (raster/forward.py:37-38,
  * raster/backward.py:77-79) on top of these.
@@ -169,6 +171,13 @@ int ssg_blend_backward(int64_t n, int64_t m, int32_t width, int32_t height,
                        const float *dL_dpixels, const ssg_grad_buffers *grads, void *stream);
 int ssg_preprocess_backward(const ssg_scene *scene, const ssg_camera *cam,
                             const ssg_grad_buffers *grads, void *stream);
+/* the reference's blend-backward plugin contract (raster/_core.pyx:315-343,
+ * backward_tiles): per-instance gradient slots (m,12) instead of the fused
+ * per-primitive reduction; slots is zeroed by the call */
+int ssg_blend_backward_slots(int64_t m, int32_t width, int32_t height, const float background[3],
+                             const ssg_splat *splat, const ssg_bin_buffers *bins,
+                             const ssg_frame_buffers *frame, const float *dL_dpixels, float *slots,
+                             void *stream);
 
 /* ---- test hooks (used by tests/ only) ----------------------------------- */
 /* the binning radix sort in isolation: stable sort of (key, u32 value) by the
@@ -176,6 +185,11 @@ int ssg_preprocess_backward(const ssg_scene *scene, const ssg_camera *cam,
 size_t ssg_test_sort_temp_bytes(int64_t n, int key_bytes);
 int ssg_test_sort(void *keys, uint32_t *vals, int key_bytes, int iota, int64_t n, int npass,
                   void *temp, void *stream);
+/* the blend forward compiled without the skew term (plain 3DGS: alpha =
+ * o * G): the config-3 regression reference for skew-free splats */
+int ssg_test_blend_forward_vanilla(int32_t width, int32_t height, const float background[3],
+                                   const ssg_splat *splat, const ssg_bin_buffers *bins,
+                                   const ssg_frame_buffers *frame, void *stream);
 
 #ifdef __cplusplus
 }

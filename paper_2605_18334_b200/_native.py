@@ -20,8 +20,9 @@ SSG_ERR_CUDA = 4
 
 EXPORTS = ("ssg_abi_version", "ssg_last_error", "ssg_grid_dims", "ssg_bin_temp_bytes",
            "ssg_preprocess_forward", "ssg_bin_rects", "ssg_bin_prepare", "ssg_bin_finish", "ssg_blend_forward",
-           "ssg_blend_backward", "ssg_preprocess_backward", "ssg_test_sort_temp_bytes",
-           "ssg_test_sort")
+           "ssg_blend_backward", "ssg_preprocess_backward", "ssg_blend_backward_slots",
+           "ssg_test_sort_temp_bytes",
+           "ssg_test_sort", "ssg_test_blend_forward_vanilla")
 
 _vp = ctypes.c_void_p
 
@@ -101,6 +102,11 @@ def lib():
                                      ctypes.c_int32, P(ctypes.c_float), _vp, P(SsgBinBuffers),
                                      P(SsgFrameBuffers), _vp, P(SsgGradBuffers), _vp]
     L.ssg_preprocess_backward.argtypes = [P(SsgScene), P(SsgCamera), P(SsgGradBuffers), _vp]
+    L.ssg_blend_backward_slots.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                           P(ctypes.c_float), _vp, P(SsgBinBuffers), P(SsgFrameBuffers),
+                                           _vp, _vp, _vp]
+    L.ssg_test_blend_forward_vanilla.argtypes = [ctypes.c_int32, ctypes.c_int32, P(ctypes.c_float), _vp,
+                                                 P(SsgBinBuffers), P(SsgFrameBuffers), _vp]
     L.ssg_test_sort_temp_bytes.restype = ctypes.c_size_t
     L.ssg_test_sort_temp_bytes.argtypes = [ctypes.c_int64, ctypes.c_int]
     L.ssg_test_sort.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int, _vp, _vp]

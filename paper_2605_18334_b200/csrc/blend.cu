@@ -85,6 +85,10 @@ __device__ __forceinline__ bool box_hits(const float4 &box, float wx0, float wy0
 }
 
 // -------------------------------------------------------------- forward
+// kVanilla = true compiles the plain 3DGS blend (no skew term, alpha =
+// o * G): the config-3 regression reference for skew-free splats, which
+// must come out bit-identical from the skew kernel (E = 1, o_sum = o).
+template <bool kVanilla>
 __global__ void __launch_bounds__(kThreads)
 k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float bg2,
                 const ssg_splat *__restrict__ splat, const uint32_t *__restrict__ inst_prim,
@@ -132,12 +136,13 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
                 if (power < B.y || power > 0.0f) continue;
                 const float4 C = lds128(aC + 16 * j);
                 float E = 1.0f, o = C.x;
-                if (B.z != 0.0f || B.w != 0.0f) {                    // warp-uniform
+                if (!kVanilla && (B.z != 0.0f || B.w != 0.0f)) {     // warp-uniform
                     const float z = (B.z * dx + B.w * dy) * SSG_SQRT1_2;   // :136
                     E = skew_E(z);                                          // :137
                     o = fmaf(C.y, E - 1.0f, C.x);                           // :138
                 }
-                const float Aval = o * fast_exp2(power * SSG_LOG2E) * E;   // :139
+                const float Aval = kVanilla ? o * fast_exp2(power * SSG_LOG2E)
+                                            : o * fast_exp2(power * SSG_LOG2E) * E;   // :139
                 const float alpha = fminf(Aval, SSG_ALPHA_MAX);             // :140
                 if (alpha < SSG_ALPHA_SKIP) continue;                       // :141-142
                 const float test_T = T * (1.0f - alpha);                    // :143
@@ -199,7 +204,7 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                  const ssg_splat *__restrict__ splat, const uint32_t *__restrict__ inst_prim,
                  const int32_t *__restrict__ ranges, const float *__restrict__ final_T,
                  const int32_t *__restrict__ last_idx, const float *__restrict__ dL,
-                 float *__restrict__ grad_screen) {
+                 float *__restrict__ grad_screen, float *__restrict__ slots) {
     __shared__ SmemBatch s;
     __shared__ uint32_t sP[kBatch];
     __shared__ int sMax[kThreads / 32];
@@ -319,7 +324,10 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                     const float v2 = __shfl_down_sync(0xffffffffu, v, 4);
                     const float v3 = __shfl_down_sync(0xffffffffu, v, 6);
                     if ((lane & 7) == 0 && lane < 24) {
-                        float4 *dst = reinterpret_cast<float4 *>(grad_screen + (size_t)sP[j] * 12) + (lane >> 3);
+                        // per-primitive accumulator, or (plugin slot mode) the
+                        // per-instance (M,12) slot row of _core.pyx:309-312
+                        float *row = slots ? slots + (size_t)k * 12 : grad_screen + (size_t)sP[j] * 12;
+                        float4 *dst = reinterpret_cast<float4 *>(row) + (lane >> 3);
                         atomicAdd(dst, make_float4(v, v1, v2, v3));
                     }
                 }
@@ -339,11 +347,23 @@ extern "C" int ssg_blend_forward(int64_t m, int32_t width, int32_t height, const
     (void)m;
     int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
     cudaStream_t st = (cudaStream_t)stream;
-    k_blend_forward<<<ntx * nty, kThreads, 0, st>>>(ntx, width, height, background[0], background[1],
-                                                    background[2], splat, bins->inst_prim, bins->ranges,
-                                                    frame->color, frame->final_T, frame->n_contrib,
-                                                    frame->last_idx);
+    k_blend_forward<false><<<ntx * nty, kThreads, 0, st>>>(ntx, width, height, background[0], background[1],
+                                                           background[2], splat, bins->inst_prim, bins->ranges,
+                                                           frame->color, frame->final_T, frame->n_contrib,
+                                                           frame->last_idx);
     return check_launch("k_blend_forward");
+}
+
+extern "C" int ssg_test_blend_forward_vanilla(int32_t width, int32_t height, const float background[3],
+                                              const ssg_splat *splat, const ssg_bin_buffers *bins,
+                                              const ssg_frame_buffers *frame, void *stream) {
+    using namespace ssg;
+    if (!bins || !frame || !background || width < 1 || height < 1) return SSG_ERR_INVALID_ARGUMENT;
+    int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
+    k_blend_forward<true><<<ntx * nty, kThreads, 0, (cudaStream_t)stream>>>(
+        ntx, width, height, background[0], background[1], background[2], splat, bins->inst_prim, bins->ranges,
+        frame->color, frame->final_T, frame->n_contrib, frame->last_idx);
+    return check_launch("k_blend_forward<vanilla>");
 }
 
 extern "C" int ssg_blend_backward(int64_t n, int64_t m, int32_t width, int32_t height,
@@ -361,6 +381,24 @@ extern "C" int ssg_blend_backward(int64_t n, int64_t m, int32_t width, int32_t h
     k_blend_backward<<<ntx * nty, kThreads, 0, st>>>(ntx, width, height, background[0], background[1],
                                                      background[2], splat, bins->inst_prim, bins->ranges,
                                                      frame->final_T, frame->last_idx, dL_dpixels,
-                                                     grads->screen);
+                                                     grads->screen, nullptr);
     return check_launch("k_blend_backward");
+}
+
+extern "C" int ssg_blend_backward_slots(int64_t m, int32_t width, int32_t height, const float background[3],
+                                        const ssg_splat *splat, const ssg_bin_buffers *bins,
+                                        const ssg_frame_buffers *frame, const float *dL_dpixels, float *slots,
+                                        void *stream) {
+    using namespace ssg;
+    if (!bins || !frame || !background || !dL_dpixels || !slots || width < 1 || height < 1 || m < 0)
+        return SSG_ERR_INVALID_ARGUMENT;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(slots, 0, sizeof(float) * 12 * (size_t)m, st);
+    if (e != cudaSuccess) { set_error("memset slots", e); return SSG_ERR_CUDA; }
+    int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
+    k_blend_backward<<<ntx * nty, kThreads, 0, st>>>(ntx, width, height, background[0], background[1],
+                                                     background[2], splat, bins->inst_prim, bins->ranges,
+                                                     frame->final_T, frame->last_idx, dL_dpixels, nullptr,
+                                                     slots);
+    return check_launch("k_blend_backward(slots)");
 }

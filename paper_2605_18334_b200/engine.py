@@ -220,9 +220,9 @@ class Engine:
         self.last_idx = self._empty((H, W), torch.int32)
         self._frame_key = (W, H)
 
-    def _frame_struct(self, final_T=None, last_idx=None) -> N.SsgFrameBuffers:
+    def _frame_struct(self, final_T=None, last_idx=None, color=None) -> N.SsgFrameBuffers:
         f = N.SsgFrameBuffers()
-        f.color, f.n_contrib = _ptr(self.color), _ptr(self.n_contrib)
+        f.color, f.n_contrib = _ptr(self.color if color is None else color), _ptr(self.n_contrib)
         f.final_T = _ptr(self.final_T if final_T is None else final_T)
         f.last_idx = _ptr(self.last_idx if last_idx is None else last_idx)
         return f
@@ -291,17 +291,25 @@ class Engine:
                 "ssg_bin_rects")
         return self._bin(n, W, H)
 
-    def forward(self, ds: DeviceScene, view: CameraView, s: float = 0.3) -> DeviceFrame:
+    def forward(self, ds: DeviceScene, view: CameraView, s: float = 0.3,
+                color_out: torch.Tensor | None = None) -> DeviceFrame:
+        """Project, bin and blend one view.  `color_out` (contiguous f32
+        (H,W,3) on this device) receives the image instead of the engine's
+        own colour buffer (view batches write straight into their slice)."""
         cam = camera_struct(view, s)
         W, H = int(cam.width), int(cam.height)
         m = self.project_and_bin(ds, cam)
         self._ensure_frame(W, H)
+        if color_out is not None and (tuple(color_out.shape) != (H, W, 3) or color_out.dtype != torch.float32
+                                      or not color_out.is_contiguous() or color_out.device != self.device):
+            raise ValueError("color_out must be a contiguous float32 (H, W, 3) tensor on the engine device")
         bg = (ctypes.c_float * 3)(*[float(x) for x in ds.background])
         with self._mark("blend_fwd"):
             N.check(self.lib.ssg_blend_forward(m, W, H, bg, _ptr(self.splat), ctypes.byref(self._bins_struct()),
-                                               ctypes.byref(self._frame_struct()), self._stream()),
+                                               ctypes.byref(self._frame_struct(color=color_out)), self._stream()),
                     "ssg_blend_forward")
-        return DeviceFrame(self.color, self.final_T, self.n_contrib, self.last_idx, W, H, ds.n, m, s)
+        color = self.color if color_out is None else color_out
+        return DeviceFrame(color, self.final_T, self.n_contrib, self.last_idx, W, H, ds.n, m, s)
 
     def backward(self, ds: DeviceScene, view: CameraView, s: float, final_T: torch.Tensor,
                  last_idx: torch.Tensor, dL: torch.Tensor, rebin: bool = True,

@@ -1,0 +1,39 @@
+"""View-batched forward rendering (config 4: one scene, many cameras).
+
+The reference renders trajectories one view at a time
+(trajectory.py:12-31 loops render_forward); there is no batched call.  Here a
+batch of views of one device-resident scene is rendered back to back on one
+GPU, each view writing straight into its slice of a (V,H,W,3) output, and
+`shard_views` splits a batch across ranks (contiguous blocks, views are
+independent, so no collective is needed -- SURVEY.md §8(e)).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from .engine import DeviceScene, Engine, default_engine
+
+
+def shard_views(n_views: int, rank: int, world: int) -> range:
+    """Contiguous block of view indices owned by `rank` (sizes differ by <= 1)."""
+    base, extra = divmod(n_views, world)
+    start = rank * base + min(rank, extra)
+    return range(start, start + base + (1 if rank < extra else 0))
+
+
+def render_views(ds: DeviceScene, views, s: float = 0.3, engine: Engine | None = None,
+                 out: torch.Tensor | None = None) -> torch.Tensor:
+    """Forward-render every view of `views` (same width/height) into
+    out[v] (float32 (V,H,W,3) on the engine's device)."""
+    eng = engine or default_engine()
+    if not views:
+        return torch.empty((0, 0, 0, 3), dtype=torch.float32, device=eng.device)
+    W, H = int(views[0].width), int(views[0].height)
+    if any(int(v.width) != W or int(v.height) != H for v in views):
+        raise ValueError("render_views needs views of one image size")
+    if out is None:
+        out = torch.empty((len(views), H, W, 3), dtype=torch.float32, device=eng.device)
+    for i, v in enumerate(views):
+        eng.forward(ds, v, s, color_out=out[i])
+    return out
