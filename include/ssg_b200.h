@@ -138,6 +138,28 @@ typedef struct ssg_grad_buffers {
     float *g_z;                 /* (n) */
 } ssg_grad_buffers;
 
+/* Mutable parameters for the optimizer (same layout as ssg_scene). */
+typedef struct ssg_params {
+    int64_t n;
+    int32_t sh_degree, sh_coeffs;
+    double *mu, *log_scale, *rot;
+    float *sh, *opacity_logits, *beta, *dir;
+} ssg_params;
+
+/* Adam moments (fp32, one array pair per field; beta and dir share the eta
+ * pair because their gradients are identical) and per-step scratch. */
+typedef struct ssg_adam_state {
+    float *m_mu, *v_mu, *m_log_scale, *v_log_scale, *m_rot, *v_rot;
+    float *m_sh, *v_sh, *m_logits, *v_logits, *m_eta, *v_eta;
+    uint8_t *row_ok;            /* (n) scratch */
+    int32_t *n_skipped;         /* (1) primitives skipped this step (non-finite gradient) */
+} ssg_adam_state;
+
+typedef struct ssg_adam_hparams {
+    int64_t t;                  /* step count after this step (>= 1) */
+    double lr_mu, lr_scale, lr_rot, lr_sh, lr_opacity, lr_beta;
+} ssg_adam_hparams;
+
 /* ---- queries ---------------------------------------------------------- */
 int ssg_abi_version(void);
 const char *ssg_last_error(void);
@@ -178,6 +200,12 @@ int ssg_blend_backward_slots(int64_t m, int32_t width, int32_t height, const flo
                              const ssg_splat *splat, const ssg_bin_buffers *bins,
                              const ssg_frame_buffers *frame, const float *dL_dpixels, float *slots,
                              void *stream);
+
+/* ---- training step (config 5) -------------------------------------------- */
+/* optimize/adam.py:71-97 Adam.step on the device (skip non-finite rows,
+ * bias-corrected moments, per-field learning rates, quaternion renorm) */
+int ssg_adam_step(const ssg_params *params, const ssg_grad_buffers *grads,
+                  const ssg_adam_state *state, const ssg_adam_hparams *hp, void *stream);
 
 /* ---- test hooks (used by tests/ only) ----------------------------------- */
 /* the binning radix sort in isolation: stable sort of (key, u32 value) by the

@@ -22,7 +22,7 @@ EXPORTS = ("ssg_abi_version", "ssg_last_error", "ssg_grid_dims", "ssg_bin_temp_b
            "ssg_preprocess_forward", "ssg_bin_rects", "ssg_bin_prepare", "ssg_bin_finish", "ssg_blend_forward",
            "ssg_blend_backward", "ssg_preprocess_backward", "ssg_blend_backward_slots",
            "ssg_test_sort_temp_bytes",
-           "ssg_test_sort", "ssg_test_blend_forward_vanilla")
+           "ssg_test_sort", "ssg_test_blend_forward_vanilla", "ssg_adam_step")
 
 _vp = ctypes.c_void_p
 
@@ -62,6 +62,22 @@ class SsgGradBuffers(ctypes.Structure):
     _fields_ = [("screen", _vp), ("d_mu", _vp), ("d_log_scale", _vp), ("d_rot", _vp),
                 ("d_sh", _vp), ("d_opacity_logits", _vp), ("d_eta", _vp), ("g_uv", _vp),
                 ("g_z", _vp)]
+
+
+class SsgParams(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("sh_degree", ctypes.c_int32), ("sh_coeffs", ctypes.c_int32),
+                ("mu", _vp), ("log_scale", _vp), ("rot", _vp), ("sh", _vp), ("opacity_logits", _vp),
+                ("beta", _vp), ("dir", _vp)]
+
+
+class SsgAdamState(ctypes.Structure):
+    _fields_ = [(f, _vp) for f in ("m_mu", "v_mu", "m_log_scale", "v_log_scale", "m_rot", "v_rot", "m_sh",
+                                   "v_sh", "m_logits", "v_logits", "m_eta", "v_eta", "row_ok", "n_skipped")]
+
+
+class SsgAdamHparams(ctypes.Structure):
+    _fields_ = [("t", ctypes.c_int64)] + [(f, ctypes.c_double) for f in
+                                          ("lr_mu", "lr_scale", "lr_rot", "lr_sh", "lr_opacity", "lr_beta")]
 
 
 SPLAT_BYTES = 64
@@ -107,6 +123,7 @@ def lib():
                                            _vp, _vp, _vp]
     L.ssg_test_blend_forward_vanilla.argtypes = [ctypes.c_int32, ctypes.c_int32, P(ctypes.c_float), _vp,
                                                  P(SsgBinBuffers), P(SsgFrameBuffers), _vp]
+    L.ssg_adam_step.argtypes = [P(SsgParams), P(SsgGradBuffers), P(SsgAdamState), P(SsgAdamHparams), _vp]
     L.ssg_test_sort_temp_bytes.restype = ctypes.c_size_t
     L.ssg_test_sort_temp_bytes.argtypes = [ctypes.c_int64, ctypes.c_int]
     L.ssg_test_sort.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int, _vp, _vp]

@@ -114,6 +114,7 @@ class DeviceFrame:
 
 @dataclasses.dataclass
 class DeviceGrads:
+    flat: torch.Tensor        # packed SUM-reducible buffer (see Engine._ensure_grads)
     screen: torch.Tensor      # (N,12)
     d_mu: torch.Tensor
     d_log_scale: torch.Tensor
@@ -228,17 +229,27 @@ class Engine:
         return f
 
     def _ensure_grads(self, n: int, K: int):
+        """Parameter gradients live in ONE packed f32 buffer, field-major
+        [d_mu 3N | d_log_scale 3N | d_rot 4N | d_sh 3KN | d_logits 2N |
+        d_eta 3N | g_uv N], so a view-parallel training step reduces them
+        with a single SUM all-reduce; g_z (MAX-reduced) is separate."""
         if self._grad_key == (n, K):
             return
         nn = max(n, 1)
         self.g_screen = self._empty((nn, 12), torch.float32)
-        self.g_mu = self._empty((nn, 3), torch.float32)
-        self.g_log_scale = self._empty((nn, 3), torch.float32)
-        self.g_rot = self._empty((nn, 4), torch.float32)
-        self.g_sh = self._empty((nn, K, 3), torch.float32)
-        self.g_logits = self._empty((nn, 2), torch.float32)
-        self.g_eta = self._empty((nn, 3), torch.float32)
-        self.g_uv = self._empty((nn,), torch.float32)
+        widths = (3, 3, 4, 3 * K, 2, 3, 1)
+        self.g_flat = self._empty((nn * sum(widths),), torch.float32)
+        views, off = [], 0
+        for w in widths:
+            views.append(self.g_flat[off:off + nn * w])
+            off += nn * w
+        self.g_mu = views[0].view(nn, 3)
+        self.g_log_scale = views[1].view(nn, 3)
+        self.g_rot = views[2].view(nn, 4)
+        self.g_sh = views[3].view(nn, K, 3)
+        self.g_logits = views[4].view(nn, 2)
+        self.g_eta = views[5].view(nn, 3)
+        self.g_uv = views[6].view(nn)
         self.g_z = self._empty((nn,), torch.float32)
         self._grad_key = (n, K)
 
@@ -341,7 +352,7 @@ class Engine:
             N.check(self.lib.ssg_preprocess_backward(ctypes.byref(sc), ctypes.byref(cam), ctypes.byref(gs), st),
                     "ssg_preprocess_backward")
         n = ds.n
-        return DeviceGrads(self.g_screen[:n], self.g_mu[:n], self.g_log_scale[:n], self.g_rot[:n],
+        return DeviceGrads(self.g_flat, self.g_screen[:n], self.g_mu[:n], self.g_log_scale[:n], self.g_rot[:n],
                            self.g_sh[:n], self.g_logits[:n], self.g_eta[:n], self.g_uv[:n], self.g_z[:n])
 
     # ------------------------------------------------------ introspection

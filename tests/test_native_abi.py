@@ -40,7 +40,8 @@ def test_grid_dims_query():
 
 
 def test_ctypes_layouts_match_header(tmp_path):
-    structs = {"ssg_scene": N.SsgScene, "ssg_camera": N.SsgCamera,
+    structs = {"ssg_scene": N.SsgScene, "ssg_camera": N.SsgCamera, "ssg_params": N.SsgParams,
+               "ssg_adam_state": N.SsgAdamState, "ssg_adam_hparams": N.SsgAdamHparams,
                "ssg_prim_buffers": N.SsgPrimBuffers, "ssg_bin_buffers": N.SsgBinBuffers,
                "ssg_frame_buffers": N.SsgFrameBuffers, "ssg_grad_buffers": N.SsgGradBuffers}
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void){"]
