@@ -37,6 +37,16 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "fwd+bwd raster ms/frame, 1M skew Gaussians @1080p; views/s at 1/2/4/8 GPU"
+# libssg_b200 kernel launches per fwd+bwd frame (all hand-written, no library
+# kernels): preprocess_fwd 1; depth radix sort = hist + schedule + 8 x
+# (upsweep, rowscan, downsweep) + settle = 27 (passes whose digit is constant
+# exit at entry); scan_counts 1; duplicate 1; tile radix sort = hist +
+# schedule + 2 x 3 + settle = 9; tile_bounds + fill_empty 2; blend_fwd 1;
+# blend_bwd 1; preprocess_bwd + sh_backward 2.
+LAUNCHES_PER_FRAME = 45
+LAUNCHES_NOTE = ("per frame: preprocess_fwd 1, depth radix sort 27, scan_counts 1, duplicate 1, tile radix "
+                 "sort 9, tile_bounds+fill_empty 2, blend_fwd 1, blend_bwd 1, preprocess_bwd+sh_backward 2; "
+                 "no library kernels (cudaMemsetAsync excluded)")
 UNIT = "views/s"
 N_PRIM, WIDTH, HEIGHT = 1_000_000, 1920, 1080
 # per-pair algorithmic instruction counts (fixed, not tuned)
@@ -51,9 +61,12 @@ def cpu_cores() -> int:
         return os.cpu_count() or 1
 
 
+PLAIN_FRACTION = 0.0
+
+
 def workload():
     from paper_2605_18334_b200.synthetic import frustum_scene, frustum_view
-    scene = frustum_scene(N_PRIM, width=WIDTH, height=HEIGHT)
+    scene = frustum_scene(N_PRIM, width=WIDTH, height=HEIGHT, plain_fraction=PLAIN_FRACTION)
     view = frustum_view(WIDTH, HEIGHT)
     dL = np.random.default_rng(1).normal(size=(HEIGHT, WIDTH, 3))
     return scene, view, dL
@@ -187,12 +200,22 @@ def main():
     ap.add_argument("--cpu-k", type=int, default=16, help="homothetic CPU sample factor")
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=2,
+                    help="BASELINE.json config: 2 (default, the headline), 3 (50%% skew-free), "
+                         "4 (3M, 64-view forward batch sharded over ranks), 5 (2M view-parallel training)")
     args = ap.parse_args()
+    if args.config in (4, 5):
+        import bench_configs
+        return bench_configs.main(args)
+    global PLAIN_FRACTION
+    PLAIN_FRACTION = 0.5 if args.config == 3 else 0.0
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    config = {"workload": "config 2: G2 synthetic 1M skew Gaussians (SH3, fp32-rounded), 1920x1080, "
+    config = {"workload": ("config 3: G3 (G2 with a seeded 50% skew-free, tied-opacity half)"
+                           if args.config == 3 else "config 2: G2") +
+                          " synthetic 1M skew Gaussians (SH3, fp32-rounded), 1920x1080, "
                           "rotated pose, forward+backward per frame",
               "n_primitives": N_PRIM, "width": WIDTH, "height": HEIGHT,
               "parallelism": f"replicas x{world} (config 2 does not shard)",
@@ -346,10 +369,8 @@ def main():
         "data": "synthetic", "config": config, "n_instances": m, "tile_pairs": pairs,
         "stage_ms": stage_ms, "roofline": roofline, "stage_roofline": stage_roofline,
         "frame_floor_ms": t_floor * 1e3, "clocks": clk, "e2e": e2e,
-        "gpu_launches": 9 * args.steps,
-        "gpu_launches_note": "own kernels per step: preprocess_fwd, iota, gather_counts, finish_scan, "
-                             "duplicate, ranges, blend_fwd, blend_bwd, preprocess_bwd (+ CUB radix-sort/scan "
-                             "library kernels)",
+        "gpu_launches": LAUNCHES_PER_FRAME * args.steps,
+        "gpu_launches_note": LAUNCHES_NOTE,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(scene, view, dL_host, args.cpu_k, args.cpu_reps)

@@ -1,0 +1,254 @@
+"""bench.py --config 4 / --config 5 (BASELINE.json configs 4 and 5).
+
+config 4: Mip-NeRF360-scale 3M skew Gaussians (G4 ball scene), 64 orbit
+          views at 1297x840, forward only.  The 64-view batch is sharded by
+          view over the ranks (contiguous blocks, no collective): strong
+          scaling of a fixed batch; value = 64 / (max over ranks of the batch
+          time) views/s.
+config 5: view-parallel training step on a 2M G5 scene: per rank one view
+          forward + L1 loss + backward, SUM all-reduce of the packed gradient
+          buffer and MAX of g_z over NCCL, device Adam; value = views trained
+          per second over all ranks (weak scaling: one view per rank per step).
+Timing: CUDA events, max over ranks, nvidia-smi clocks sampled during the
+timed region (see bench.py).
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import statistics
+import time
+
+import numpy as np
+
+import bench as B
+
+N4, W4, H4, V4 = 3_000_000, 1297, 840, 64
+N5 = 2_000_000
+
+
+def _setup(local, world):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return torch, dist
+
+
+def _helpers(torch, dist, world):
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+    return barrier, max_over_ranks
+
+
+def _pinned_scene(torch, scene):
+    from paper_2605_18334_b200.scene import Scene
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+        t.numpy()[...] = a
+        return t.numpy()
+    return Scene(*(pinned(getattr(scene, f)) for f in Scene.ARRAY_FIELDS), background=scene.background,
+                 sh_degree=scene.sh_degree)
+
+
+def config4(args, rank, world, local):
+    torch, dist = _setup(local, world)
+    barrier, max_over_ranks = _helpers(torch, dist, world)
+    from paper_2605_18334_b200.engine import DeviceScene, Engine
+    from paper_2605_18334_b200.raster import render_forward
+    from paper_2605_18334_b200.synthetic import ball_scene, orbit_views
+    from paper_2605_18334_b200.views import render_views, shard_views
+
+    scene = ball_scene(N4, seed=0)
+    views = orbit_views(V4, radius=4.0, elevation=1.2, width=W4, height=H4, fov_x=0.9)
+    mine = [views[i] for i in shard_views(V4, rank, world)]
+    eng = Engine(torch.device("cuda", local))
+    ds = DeviceScene.from_host(scene)
+    out = torch.empty((len(mine), H4, W4, 3), dtype=torch.float32, device="cuda")
+    pairs = 0
+    for v in mine:  # warm-up + per-view work count
+        f = eng.forward(ds, v, 0.3)
+        pairs += B.tile_pairs(f, eng.ranges, W4, H4)
+    for _ in range(max(args.warmup, 3) - 1):
+        render_views(ds, mine, engine=eng, out=out)
+    barrier()
+    clocks = B.ClockSampler(local)
+    clocks.start()
+    eng.stage_events = {}
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        render_views(ds, mine, engine=eng, out=out)
+    e1.record()
+    barrier()
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    stage_ms = {k: statistics.mean(a.elapsed_time(b) for a, b in v) for k, v in eng.stage_events.items()}
+    eng.stage_events = None
+
+    # e2e: the reference-facing call per view (render_forward with the scene in
+    # pinned host memory, fp64 frame back to host), one batch
+    pscene = _pinned_scene(torch, scene)
+    render_forward(pscene, mine[0])
+    barrier()
+    t0 = time.perf_counter()
+    for v in mine:
+        render_forward(pscene, v)
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    scene_bytes = N4 * (3 + 3 + 4 + 48 + 2 + 3 + 3) * 8
+
+    peaks = json.load(open(os.path.join(B.ROOT, "MEASURED_PEAKS.json")))
+    n_sm = torch.cuda.get_device_properties(local).multi_processor_count
+    r_fp32 = n_sm * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    per_view_blend = stage_ms.get("blend_fwd", 0.0) * 1e-3
+    ach = B.FP32_PER_PAIR["blend_fwd"] * pairs / max(len(mine), 1) / max(per_view_blend, 1e-9)
+    result = {
+        "metric": "config 4: 64-view forward batch, 3M skew Gaussians @1297x840, views/s",
+        "value": V4 * 1000.0 / ms, "unit": "views/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32 (blend) / f64 (preprocess)", "data": "synthetic",
+        "config": {"workload": "config 4: G4 ball scene, 3M skew Gaussians (SH3, fp32-rounded), "
+                               "orbit_views(64, r=4, elev=1.2, 1297x840, fov 0.9), forward only",
+                   "parallelism": f"views sharded x{world} (contiguous blocks, no collective)",
+                   "l2": "inputs larger than L2 (scene 912 MB)"},
+        "stage_ms_per_view": stage_ms,
+        "roofline": {"bound": "fp32", "kernel": "k_blend_forward", "achieved": ach / 1e12,
+                     "peak": r_fp32 / 1e12, "unit": "Tinstr/s (FP32 lane)", "frac": ach / r_fp32,
+                     "traffic": None},
+        "clocks": clk,
+        "e2e": {"value": V4 / e2e_s,
+                "unit": "views/s", "h2d_bytes_per_step": len(mine) * scene_bytes,
+                "d2h_bytes_per_step": len(mine) * H4 * W4 * (24 + 8 + 4 + 8),
+                "path": "render_forward per view with the scene in pinned host memory (uploaded per call, "
+                        "like the reference API), fp64 frame bundle back to host"},
+        "gpu_launches": (B.LAUNCHES_PER_FRAME - 3) * len(mine) * args.steps,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        sub_view = views[0]
+        kind, run, desc = _cpu_forward_sample(scene, sub_view, 64)
+        run()
+        t0 = time.perf_counter()
+        run()
+        t = (time.perf_counter() - t0) * 64
+        result["cpu_baseline"] = {"value": 1.0 / t, "unit": "views/s", "cores": B.cpu_cores(), "kind": kind,
+                                  "sample": desc}
+    if rank == 0:
+        print(json.dumps(result))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _cpu_forward_sample(scene, view, k):
+    from paper_2605_18334_b200.synthetic import homothetic_sample
+    sub, sv = homothetic_sample(scene, view, k)
+    ref = B._load_reference()
+    desc = (f"homothetic 1/{k} sample of orbit view 0 (forward only): {len(sub)} primitives, "
+            f"{sv.width}x{sv.height}; per-view time = {k} x sample time")
+    if ref is not None:
+        rf, _ = ref
+        return "reference", (lambda: rf(sub, sv, 0.3, backend_name="cython")), desc
+    from oracle import oracle as O
+    O.set_num_threads(B.cpu_cores())
+    return "port", (lambda: O.render_forward(sub, sv, 0.3)), desc
+
+
+def config5(args, rank, world, local):
+    torch, dist = _setup(local, world)
+    barrier, max_over_ranks = _helpers(torch, dist, world)
+    from paper_2605_18334_b200.engine import DeviceScene, Engine
+    from paper_2605_18334_b200.synthetic import ball_scene, fp32_round, orbit_views
+    from paper_2605_18334_b200.train import DeviceAdam, training_step
+
+    target_scene = ball_scene(N5, seed=0)
+    views = orbit_views(V4, radius=4.0, elevation=1.2, width=W4, height=H4, fov_x=0.9)
+    eng = Engine(torch.device("cuda", local))
+    tgt_ds = DeviceScene.from_host(target_scene)
+    targets = torch.empty((V4, H4, W4, 3), dtype=torch.float32, device="cuda")
+    for i, v in enumerate(views):
+        eng.forward(tgt_ds, v, 0.3, color_out=targets[i])
+    del tgt_ds
+    start = target_scene.copy()
+    start.mu += np.random.default_rng(5).normal(size=start.mu.shape) * 0.01
+    ds = DeviceScene.from_host(fp32_round(start))
+    adam = DeviceAdam(ds)
+    step_no = [0]
+
+    def step(target=None):
+        i = (step_no[0] * world + rank) % V4
+        step_no[0] += 1
+        return training_step(eng, ds, adam, views[i], targets[i] if target is None else target)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    clocks = B.ClockSampler(local)
+    clocks.start()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    barrier()
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    # e2e: the step's input image from pinned host memory, loss read back
+    host_t = torch.empty((H4, W4, 3), dtype=torch.float32, pin_memory=True)
+    host_t.copy_(targets[0].cpu())
+    e2e_t = []
+    for _ in range(max(args.e2e_steps, 1)):
+        barrier()
+        t0 = time.perf_counter()
+        tgt = host_t.to("cuda", non_blocking=True)
+        loss = step(tgt)
+        float(loss.item())
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = max_over_ranks(statistics.median(e2e_t))
+    result = {
+        "metric": "config 5: view-parallel training step, 2M skew Gaussians @1297x840, views/s trained",
+        "value": world * 1000.0 / ms, "unit": "views/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (blend, grads, moments) / f64 (preprocess)", "data": "synthetic",
+        "config": {"workload": "config 5: G5 (ball scene, 2M), targets rendered from it, start perturbed "
+                               "(mu + N(0, 0.01)); per step per rank: fwd, L1, bwd, all-reduce, Adam",
+                   "parallelism": f"view-parallel x{world}, NCCL all-reduce SUM of {N5 * 65 * 4 / 1e6:.0f} MB "
+                                  "packed gradients + MAX of g_z"},
+        "clocks": clk,
+        "e2e": {"value": world / e2e_s, "unit": "views/s", "h2d_bytes_per_step": H4 * W4 * 12,
+                "d2h_bytes_per_step": 4, "path": "training_step with the target image copied from pinned "
+                                                 "host memory and the loss read back each step"},
+        "gpu_launches": (B.LAUNCHES_PER_FRAME + 8) * args.steps,
+        "cpu_baseline": None,
+        "cpu_baseline_note": "not measured for config 5 (the reference training step includes the "
+                             "SSIM loss and densification, outside this path); see config 2",
+    }
+    if rank == 0:
+        print(json.dumps(result))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps({"impl": "reference", "unavailable":
+                              f"--impl reference is defined for the headline config 2 only (got {args.config})"}))
+        return
+    (config4 if args.config == 4 else config5)(args, rank, world, local)
