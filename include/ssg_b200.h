@@ -121,6 +121,12 @@ typedef struct ssg_frame_buffers {
     float *final_T;             /* (H,W) */
     int32_t *n_contrib;         /* (H,W) */
     int32_t *last_idx;          /* (H,W) global sorted index or -1 */
+    uint32_t *blend_mask;       /* optional (NULL = unused), ssg_blend_mask_words(m, tiles)
+                                   words: ssg_blend_forward records which instances each
+                                   8x4 pixel block blended; ssg_blend_backward /
+                                   ssg_blend_backward_slots then visit exactly those.  Only
+                                   valid for the binning, splats and final_T/last_idx of
+                                   the forward call that wrote it. */
 } ssg_frame_buffers;
 
 /* Gradient outputs (raster/backward.py:28-39).  d_beta == d_dir
@@ -181,6 +187,8 @@ int ssg_bin_rects(int64_t n, const double *mean2d, const double *radius, const d
 /* duplicate, stable sort by tile, ranges; m = value of *bins->n_instances */
 int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t height,
                    const ssg_prim_buffers *prim, const ssg_bin_buffers *bins, void *stream);
+/* words of the optional frame blend mask for m instances over n_tiles tiles */
+int64_t ssg_blend_mask_words(int64_t m, int32_t n_tiles);
 int ssg_blend_forward(int64_t m, int32_t width, int32_t height, const float background[3],
                       const ssg_splat *splat, const ssg_bin_buffers *bins,
                       const ssg_frame_buffers *frame, void *stream);

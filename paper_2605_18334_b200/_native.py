@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libssg_b200.so")
+# SSG_B200_LIB selects a diagnostic build of the same library (tools/ only)
+LIB_PATH = os.environ.get("SSG_B200_LIB") or os.path.join(_HERE, "libssg_b200.so")
 
 SSG_OK = 0
 SSG_ERR_INVALID_ARGUMENT = 1
@@ -22,7 +23,7 @@ EXPORTS = ("ssg_abi_version", "ssg_last_error", "ssg_grid_dims", "ssg_bin_temp_b
            "ssg_preprocess_forward", "ssg_bin_rects", "ssg_bin_prepare", "ssg_bin_finish", "ssg_blend_forward",
            "ssg_blend_backward", "ssg_preprocess_backward", "ssg_blend_backward_slots",
            "ssg_test_sort_temp_bytes",
-           "ssg_test_sort", "ssg_test_blend_forward_vanilla", "ssg_adam_step")
+           "ssg_test_sort", "ssg_test_blend_forward_vanilla", "ssg_adam_step", "ssg_blend_mask_words")
 
 _vp = ctypes.c_void_p
 
@@ -55,7 +56,7 @@ class SsgBinBuffers(ctypes.Structure):
 
 
 class SsgFrameBuffers(ctypes.Structure):
-    _fields_ = [("color", _vp), ("final_T", _vp), ("n_contrib", _vp), ("last_idx", _vp)]
+    _fields_ = [("color", _vp), ("final_T", _vp), ("n_contrib", _vp), ("last_idx", _vp), ("blend_mask", _vp)]
 
 
 class SsgGradBuffers(ctypes.Structure):
@@ -81,6 +82,7 @@ class SsgAdamHparams(ctypes.Structure):
 
 
 SPLAT_BYTES = 64
+ABI_VERSION = 2
 
 _lib = None
 
@@ -127,7 +129,9 @@ def lib():
     L.ssg_test_sort_temp_bytes.restype = ctypes.c_size_t
     L.ssg_test_sort_temp_bytes.argtypes = [ctypes.c_int64, ctypes.c_int]
     L.ssg_test_sort.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int, _vp, _vp]
-    if L.ssg_abi_version() != 1:
+    L.ssg_blend_mask_words.restype = ctypes.c_int64
+    L.ssg_blend_mask_words.argtypes = [ctypes.c_int64, ctypes.c_int32]
+    if L.ssg_abi_version() != ABI_VERSION:
         raise NativeError("libssg_b200.so ABI version mismatch; rebuild")
     _lib = L
     return L

@@ -30,24 +30,36 @@ def _newest_input_mtime(src: str) -> float:
     return max(os.path.getmtime(p) for p in paths)
 
 
-def _compile(src: str, force: bool) -> str:
-    obj = os.path.join(OBJ_DIR, src.replace(".cu", ".o"))
+def _compile(src: str, force: bool, obj_dir: str = OBJ_DIR, defines: tuple = ()) -> str:
+    obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= _newest_input_mtime(src):
         return obj
-    cmd = [NVCC, *ARCH, *COMMON, *EXTRA.get(src, []), "-c", os.path.join(CSRC, src), "-o", obj]
+    cmd = [NVCC, *ARCH, *COMMON, *defines, *EXTRA.get(src, []), "-c", os.path.join(CSRC, src), "-o", obj]
     subprocess.run(cmd, check=True)
     return obj
 
 
-def build(force: bool = False) -> str:
-    os.makedirs(OBJ_DIR, exist_ok=True)
+def build(force: bool = False, stats: bool = False, variant: str | None = None, defines: tuple = ()) -> str:
+    """stats=True builds the diagnostic variant libssg_b200_stats.so (blend
+    event counters, tools/blend_stats.py); variant=NAME with extra -D flags
+    builds libssg_b200_NAME.so for A/B timing (tools/); neither is ever
+    loaded by default."""
+    if stats:
+        variant, defines = "stats", ("-DSSG_BLEND_STATS",) + tuple(defines)
+    obj_dir = OBJ_DIR + (f"_{variant}" if variant else "")
+    out = OUT.replace(".so", f"_{variant}.so") if variant else OUT
+    defines = tuple(defines)
+    os.makedirs(obj_dir, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force), SOURCES))
-    if force or not os.path.exists(OUT) or os.path.getmtime(OUT) < max(os.path.getmtime(o) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "--cudart", "static", "-o", OUT, *objs]
+        objs = list(ex.map(lambda s: _compile(s, force, obj_dir, defines), SOURCES))
+    if force or not os.path.exists(out) or os.path.getmtime(out) < max(os.path.getmtime(o) for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "--cudart", "static", "-o", out, *objs]
         subprocess.run(cmd, check=True)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv))
+    args = sys.argv[1:]
+    var = args[args.index("--variant") + 1] if "--variant" in args else None
+    print(build(force="--force" in args, stats="--stats" in args, variant=var,
+                defines=tuple(a for a in args if a.startswith("-D"))))

@@ -23,6 +23,12 @@
 // shared-memory fp32 atomic on sm_100 is a CAS loop, so no smem staging).
 #include "ssg_common.cuh"
 
+#ifdef SSG_BLEND_STATS
+// diagnostic build only (tools/blend_stats.py): warp-level event counters
+__device__ unsigned long long g_blend_stats[32];
+#define SSG_STAT(i, v) atomicAdd(&g_blend_stats[i], (unsigned long long)(v))
+#endif
+
 namespace ssg {
 
 constexpr int kThreads = 256;
@@ -32,14 +38,16 @@ constexpr int kBatch = 256;
 //   A = (mx_local, my_local, conic_a, conic_b)
 //   B = (conic_c, far_thr, skew_x, skew_y)
 //   C = (o_sum, o_diff, r, g),  D = b
-//   X = ellipse box (x_lo, x_hi, y_lo, y_hi), tile-local pixel coordinates
+//   X = (k, h, m, r2m): the ellipse {d : a dx^2 + 2b dx dy + c dy^2 <= r2m}
+//       in completed-square form, k = b/a, h = det/a, m = b/c
 // far_thr is a per-instance lower bound on the Gaussian exponent below which
 // alpha < 1/255 is certain: A = o*G*E <= omax*G*Emax with Emax = 2 (1 for
 // skew-free splats), so power < ln(1/(255*omax*Emax)) implies the reference's
 // ALPHA_SKIP test (_core.pyx:141) fires.  A 1e-4 margin keeps the shortcut
 // strictly inside the region where the full fp32 evaluation also skips.  The
-// box bounds {d : -d'Qd/2 >= far_thr} with a further relative/absolute
-// margin, so pixels outside it are skipped by the per-pair test anyway.
+// ellipse {power >= far_thr} (r2 = -2 far_thr, widened by 1e-3 relative +
+// 1e-4 absolute) is what the per-warp culling tests against the warp's 8x4
+// block of pixel centres, exactly (not via its bounding box).
 struct SmemBatch {
     float4 A[kBatch];
     float4 B[kBatch];
@@ -60,41 +68,72 @@ __device__ __forceinline__ void stage_splat(const ssg_splat *splat, uint32_t p, 
     const float thr = omax > 0.0f ? -logf(255.0f * omax) - 1e-4f : INFINITY;
     const float mx = (float)(m.x - ox), my = (float)(m.y - oy);
     const float a = q1.x, b = q1.y, c = q1.z;
-    const float det = a * c - b * b;
     const float r2 = -2.0f * thr;
-    float4 box;
+    float4 ell;
     if (!(r2 > 0.0f)) {
-        box = make_float4(INFINITY, -INFINITY, INFINITY, -INFINITY);  // never hits
-    } else if (det > 0.0f && a > 0.0f && c > 0.0f) {
-        const float rx = sqrtf(r2 * c / det) * 1.0001f + 1e-3f;
-        const float ry = sqrtf(r2 * a / det) * 1.0001f + 1e-3f;
-        box = make_float4(mx - rx, mx + rx, my - ry, my + ry);
+        ell = make_float4(0.0f, 0.0f, 0.0f, -1.0f);                 // never blends: never hits
     } else {
-        box = make_float4(-INFINITY, INFINITY, -INFINITY, INFINITY);  // always test
+        const double det = (double)a * (double)c - (double)b * (double)b;   // exact products
+        if (a > 0.0f && c > 0.0f && det > 0.0)
+            ell = make_float4(b / a, (float)(det / (double)a), b / c, fmaf(r2, 1.001f, 1e-4f));
+        else
+            ell = make_float4(0.0f, 0.0f, 0.0f, INFINITY);          // degenerate: always evaluate
     }
     s.A[slot] = make_float4(mx, my, a, b);
     s.B[slot] = make_float4(c, thr, q1.w, q2.x);
     s.C[slot] = make_float4(0.5f * (q2.y + q2.z), 0.5f * (q2.y - q2.z), q2.w, q3.x);
     s.D[slot] = q3.y;
-    s.X[slot] = box;
+    s.X[slot] = ell;
 }
 
-__device__ __forceinline__ bool box_hits(const float4 &box, float wx0, float wy0) {
-    // pixel centres of the warp block: [wx0+0.5, wx0+7.5] x [wy0+0.5, wy0+3.5]
-    return box.y >= wx0 + 0.5f && box.x <= wx0 + 7.5f && box.w >= wy0 + 0.5f && box.z <= wy0 + 3.5f;
+// Does the instance's ellipse meet the rectangle spanned by the warp's pixel
+// centres [wx0+0.5, wx0+7.5] x [wy0+0.5, wy0+3.5]?  Minimum of the quadratic
+// form over the rectangle: 0 if the mean is inside, else the least of the
+// four clamped edge minima, each a sum of non-negative terms
+// a (dx + k dy)^2 + h dy^2 (no cancellation).
+__device__ __forceinline__ bool ellipse_meets_block(const float4 A, const float4 X, float wx0, float wy0) {
+    const float X0 = wx0 + 0.5f - A.x, X1 = X0 + 7.0f;
+    const float Y0 = wy0 + 0.5f - A.y, Y1 = Y0 + 3.0f;
+    const float a = A.z, k = X.x, h = X.y, mm = X.z;
+    const float ya = fminf(fmaxf(-mm * X0, Y0), Y1), yb = fminf(fmaxf(-mm * X1, Y0), Y1);
+    const float ua = fmaf(k, ya, X0), ub = fmaf(k, yb, X1);
+    const float xa = fminf(fmaxf(-k * Y0, X0), X1), xb = fminf(fmaxf(-k * Y1, X0), X1);
+    const float va = fmaf(k, Y0, xa), vb = fmaf(k, Y1, xb);
+    const float q = fminf(fminf(fmaf(a * ua, ua, h * ya * ya), fmaf(a * ub, ub, h * yb * yb)),
+                          fminf(fmaf(a * va, va, h * Y0 * Y0), fmaf(a * vb, vb, h * Y1 * Y1)));
+    const bool inside = X0 <= 0.0f && X1 >= 0.0f && Y0 <= 0.0f && Y1 >= 0.0f;
+    return inside ? X.w >= 0.0f : !(q > X.w);
+}
+
+// Word of the per-(tile, warp, 32-instance chunk) blend mask: bit b of word
+// (start/32 + tile + chunk) * 8 + warp is set when some pixel of the warp
+// blended instance start + 32*chunk + b in the forward.  The bases never
+// overlap: consecutive tiles' bases differ by >= ceil(len/32).
+__device__ __forceinline__ size_t mask_word(int start, int tile, int chunk, int warp) {
+    return ((size_t)(start >> 5) + (size_t)tile + (size_t)chunk) * 8 + (size_t)warp;
 }
 
 // -------------------------------------------------------------- forward
 // kVanilla = true compiles the plain 3DGS blend (no skew term, alpha =
 // o * G): the config-3 regression reference for skew-free splats, which
 // must come out bit-identical from the skew kernel (E = 1, o_sum = o).
+// With blend_mask != nullptr the kernel records, per warp and 32-instance
+// chunk, which instances any of the warp's pixels blended; the backward
+// then visits exactly those (same arithmetic, same decisions).
+#ifndef SSG_FWD_MINB
+#define SSG_FWD_MINB 5
+#endif
+#ifndef SSG_BWD_MINB
+#define SSG_BWD_MINB 4
+#endif
+
 template <bool kVanilla>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, SSG_FWD_MINB)
 k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float bg2,
                 const ssg_splat *__restrict__ splat, const uint32_t *__restrict__ inst_prim,
                 const int32_t *__restrict__ ranges, float *__restrict__ color,
                 float *__restrict__ final_T, int32_t *__restrict__ n_contrib,
-                int32_t *__restrict__ last_idx) {
+                int32_t *__restrict__ last_idx, uint32_t *__restrict__ blend_mask) {
     __shared__ SmemBatch s;
     const int tile = blockIdx.x;
     const int tyi = tile / ntx, txi = tile - tyi * ntx;
@@ -123,37 +162,58 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
         for (int c0 = 0; c0 < cnt; c0 += 32) {
             if (__all_sync(0xffffffffu, done)) break;
             const int i = c0 + lane;
-            unsigned mask = __ballot_sync(0xffffffffu, i < cnt && box_hits(lds128(aX + 16 * i), fwx0, fwy0));
+            bool hit = false;
+            if (i < cnt) hit = ellipse_meets_block(lds128(aA + 16 * i), lds128(aX + 16 * i), fwx0, fwy0);
+            unsigned mask = __ballot_sync(0xffffffffu, hit);
+            uint32_t lbits = 0;  // instances of this chunk the lane's pixel blended
+#ifdef SSG_BLEND_STATS
+            if (lane == 0) SSG_STAT(0, __popc(mask));
+#endif
             while (mask) {
-                const int j = c0 + __ffs(mask) - 1;
+                const int bit = __ffs(mask) - 1;
                 mask &= mask - 1;
-                if (done) continue;
-                const float4 A = lds128(aA + 16 * j);
-                const float4 B = lds128(aB + 16 * j);
-                const float dx = fx - A.x, dy = fy - A.y;
-                // _core.pyx:133-135
-                const float power = -0.5f * (A.z * dx * dx + B.x * dy * dy) - A.w * dx * dy;
-                if (power < B.y || power > 0.0f) continue;
-                const float4 C = lds128(aC + 16 * j);
-                float E = 1.0f, o = C.x;
-                if (!kVanilla && (B.z != 0.0f || B.w != 0.0f)) {     // warp-uniform
-                    const float z = (B.z * dx + B.w * dy) * SSG_SQRT1_2;   // :136
-                    E = skew_E(z);                                          // :137
-                    o = fmaf(C.y, E - 1.0f, C.x);                           // :138
+                const int j = c0 + bit;
+                if (!done) {
+                    const float4 A = lds128(aA + 16 * j);
+                    const float4 B = lds128(aB + 16 * j);
+                    const float dx = fx - A.x, dy = fy - A.y;
+                    // _core.pyx:133-135
+                    const float power = -0.5f * (A.z * dx * dx + B.x * dy * dy) - A.w * dx * dy;
+                    if (power >= B.y && power <= 0.0f) {
+                        const float4 C = lds128(aC + 16 * j);
+                        float E = 1.0f, o = C.x;
+                        if (!kVanilla && (B.z != 0.0f || B.w != 0.0f)) {     // warp-uniform
+                            const float z = (B.z * dx + B.w * dy) * SSG_SQRT1_2;   // :136
+                            E = skew_E(z);                                          // :137
+                            o = fmaf(C.y, E - 1.0f, C.x);                           // :138
+                        }
+                        const float Aval = kVanilla ? o * fast_exp2(power * SSG_LOG2E)
+                                                    : o * fast_exp2(power * SSG_LOG2E) * E;   // :139
+                        const float alpha = fminf(Aval, SSG_ALPHA_MAX);             // :140
+                        if (alpha >= SSG_ALPHA_SKIP) {                              // :141-142
+                            const float test_T = T * (1.0f - alpha);                // :143
+                            if (test_T < SSG_T_STOP) {                              // :144-147
+                                done = 1;
+                            } else {                                                // :148-154
+                                const float w = alpha * T;
+                                C0 = fmaf(w, C.z, C0);
+                                C1 = fmaf(w, C.w, C1);
+                                C2 = fmaf(w, lds32(aD + 4 * j), C2);
+                                T = test_T;
+                                nc++;
+                                li = base + j;
+                                lbits |= 1u << bit;
+                            }
+                        }
+                    }
                 }
-                const float Aval = kVanilla ? o * fast_exp2(power * SSG_LOG2E)
-                                            : o * fast_exp2(power * SSG_LOG2E) * E;   // :139
-                const float alpha = fminf(Aval, SSG_ALPHA_MAX);             // :140
-                if (alpha < SSG_ALPHA_SKIP) continue;                       // :141-142
-                const float test_T = T * (1.0f - alpha);                    // :143
-                if (test_T < SSG_T_STOP) { done = 1; continue; }            // :144-147
-                const float w = alpha * T;                                  // :148-154
-                C0 = fmaf(w, C.z, C0);
-                C1 = fmaf(w, C.w, C1);
-                C2 = fmaf(w, lds32(aD + 4 * j), C2);
-                T = test_T;
-                nc++;
-                li = base + j;
+            }
+            if (blend_mask) {
+                const uint32_t bmask = __reduce_or_sync(0xffffffffu, lbits);
+#ifdef SSG_BLEND_STATS
+                if (lane == 0) SSG_STAT(1, __popc(bmask));
+#endif
+                if (lane == 0) blend_mask[mask_word(start, tile, (base - start + c0) >> 5, warp)] = bmask;
             }
         }
     }
@@ -169,42 +229,49 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
 }
 
 // ------------------------------------------------------------- backward
-// Transposed butterfly: v[0..15] per lane -> lane holds the warp sum of
-// component (lane >> 1) & 15 (lanes 2i and 2i+1 both).
-__device__ __forceinline__ float warp_reduce_transposed16(float (&v)[16], int lane) {
+// Transposed butterfly over 12 components: after it, lane L holds the warp
+// sum of component 6*b4 + 3*b3 + c(b2, b1), c = 0 / 1 / 2 for (b2, b1) =
+// (0,0) / (0,1) / (1,0) (bit bk = lane bit k; (1,1) is padding): 13 shuffles
+// instead of 5 x 12.
+__device__ __forceinline__ float warp_reduce_transposed12(float (&v)[12], int lane) {
     const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
-        float send = b4 ? v[i] : v[i + 8];
-        float keep = b4 ? v[i + 8] : v[i];
+    for (int i = 0; i < 6; i++) {
+        const float send = b4 ? v[i] : v[i + 6];
+        const float keep = b4 ? v[i + 6] : v[i];
         v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-        float send = b3 ? v[i] : v[i + 4];
-        float keep = b3 ? v[i + 4] : v[i];
+    for (int i = 0; i < 3; i++) {
+        const float send = b3 ? v[i] : v[i + 3];
+        const float keep = b3 ? v[i + 3] : v[i];
         v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
     }
-#pragma unroll
-    for (int i = 0; i < 2; i++) {
-        float send = b2 ? v[i] : v[i + 2];
-        float keep = b2 ? v[i + 2] : v[i];
-        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    {
+        const float send0 = b2 ? v[0] : v[2], keep0 = b2 ? v[2] : v[0];
+        const float send1 = b2 ? v[1] : 0.0f, keep1 = b2 ? 0.0f : v[1];
+        v[0] = keep0 + __shfl_xor_sync(0xffffffffu, send0, 4);
+        v[1] = keep1 + __shfl_xor_sync(0xffffffffu, send1, 4);
     }
     {
-        float send = b1 ? v[0] : v[1];
-        float keep = b1 ? v[1] : v[0];
+        const float send = b1 ? v[0] : v[1], keep = b1 ? v[1] : v[0];
         v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
     }
     return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
-__global__ void __launch_bounds__(kThreads)
+// lane holding component c after warp_reduce_transposed12
+__device__ __forceinline__ int comp_lane(int c) {
+    const int g = (c * 11) >> 5;  // c / 3 for c < 16
+    return 8 * g + 2 * (c - 3 * g);
+}
+
+__global__ void __launch_bounds__(kThreads, SSG_BWD_MINB)
 k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float bg2,
                  const ssg_splat *__restrict__ splat, const uint32_t *__restrict__ inst_prim,
                  const int32_t *__restrict__ ranges, const float *__restrict__ final_T,
-                 const int32_t *__restrict__ last_idx, const float *__restrict__ dL,
-                 float *__restrict__ grad_screen, float *__restrict__ slots) {
+                 const int32_t *__restrict__ last_idx, const uint32_t *__restrict__ blend_mask,
+                 const float *__restrict__ dL, float *__restrict__ grad_screen, float *__restrict__ slots) {
     __shared__ SmemBatch s;
     __shared__ uint32_t sP[kBatch];
     __shared__ int sMax[kThreads / 32];
@@ -243,11 +310,20 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
     const int hi = min(maxli + 1, end);
     const uint32_t aA = smem_addr(s.A), aB = smem_addr(s.B), aC = smem_addr(s.C);
     const uint32_t aX = smem_addr(s.X), aD = smem_addr(s.D);
+    // the three writer lanes (0, 8, 16) gather components 4w..4w+3
+    const int wsel = min(lane >> 3, 2);
+    const int src0 = comp_lane(4 * wsel), src1 = comp_lane(4 * wsel + 1);
+    const int src2 = comp_lane(4 * wsel + 2), src3 = comp_lane(4 * wsel + 3);
 
-    for (int top = hi; top > start; top -= kBatch) {
-        const int lo = max(start, top - kBatch);
-        const int cnt = top - lo;
-        __syncthreads();  // previous batch fully flushed
+    // batches aligned to the forward's chunk grid (start + 256 b), top down
+    for (int b = (hi - start - 1) / kBatch; b >= 0; b--) {
+        const int lo = start + b * kBatch;
+        const int cnt = min(kBatch, hi - lo);
+        // this warp's mask words of the batch (lane q < 8 holds chunk q)
+        uint32_t words = 0;
+        if (blend_mask && lane < 8 && 32 * lane < cnt)
+            words = blend_mask[mask_word(start, tile, b * (kBatch / 32) + lane, warp)];
+        __syncthreads();  // previous batch fully consumed
         if ((int)threadIdx.x < cnt) {
             const uint32_t p = inst_prim[lo + threadIdx.x];
             stage_splat(splat, p, ox, oy, s, threadIdx.x);
@@ -257,16 +333,27 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
 
         const int cwarp = min(cnt, wmax - lo + 1);  // instances past the warp's last_idx never blend
         for (int c0 = ((cwarp - 1) >> 5) << 5; c0 >= 0 && cwarp > 0; c0 -= 32) {
-            const int i = c0 + lane;
-            unsigned mask = __ballot_sync(0xffffffffu, i < cwarp && box_hits(lds128(aX + 16 * i), fwx0, fwy0));
+            unsigned mask;
+            if (blend_mask) {
+                mask = __shfl_sync(0xffffffffu, words, c0 >> 5);
+                if (cwarp - c0 < 32) mask &= (1u << (cwarp - c0)) - 1u;
+            } else {
+                const int i = c0 + lane;
+                bool hit = false;
+                if (i < cwarp) hit = ellipse_meets_block(lds128(aA + 16 * i), lds128(aX + 16 * i), fwx0, fwy0);
+                mask = __ballot_sync(0xffffffffu, hit);
+            }
+#ifdef SSG_BLEND_STATS
+            if (lane == 0) SSG_STAT(16, __popc(mask));
+#endif
             while (mask) {
                 const int bit = 31 - __clz(mask);
                 mask &= ~(1u << bit);
                 const int j = c0 + bit;
                 const int k = lo + j;
-                float g[16];
+                float g[12];
 #pragma unroll
-                for (int q = 0; q < 16; q++) g[q] = 0.0f;
+                for (int q = 0; q < 12; q++) g[q] = 0.0f;
                 bool contrib = false;
                 if (k <= li) {  // :263-264
                     const float4 A = lds128(aA + 16 * j);
@@ -314,21 +401,32 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                         }
                     }
                 }
-                if (__any_sync(0xffffffffu, contrib)) {
-                    // lane 2i holds component i; lanes 0 / 8 / 16 gather four
-                    // consecutive components and issue one float4 reduction
-                    // each straight into the primitive's accumulator
-                    // (raster/backward.py:70-73)
-                    const float v = warp_reduce_transposed16(g, lane);
-                    const float v1 = __shfl_down_sync(0xffffffffu, v, 2);
-                    const float v2 = __shfl_down_sync(0xffffffffu, v, 4);
-                    const float v3 = __shfl_down_sync(0xffffffffu, v, 6);
+#ifdef SSG_BLEND_STATS
+                {
+                    const unsigned cbal = __ballot_sync(0xffffffffu, contrib);
+                    if (lane == 0) {
+                        SSG_STAT(17, cbal != 0);
+                        SSG_STAT(18, __popc(cbal));
+                    }
+                }
+#endif
+                // with the forward's mask every visited instance has a
+                // contributing pixel; without it, skip empty hits
+                if (blend_mask || __any_sync(0xffffffffu, contrib)) {
+                    // lanes 0 / 8 / 16 gather four consecutive components and
+                    // issue one float4 reduction each straight into the
+                    // primitive's accumulator (raster/backward.py:70-73)
+                    const float v = warp_reduce_transposed12(g, lane);
+                    const float v0 = __shfl_sync(0xffffffffu, v, src0);
+                    const float v1 = __shfl_sync(0xffffffffu, v, src1);
+                    const float v2 = __shfl_sync(0xffffffffu, v, src2);
+                    const float v3 = __shfl_sync(0xffffffffu, v, src3);
                     if ((lane & 7) == 0 && lane < 24) {
                         // per-primitive accumulator, or (plugin slot mode) the
                         // per-instance (M,12) slot row of _core.pyx:309-312
                         float *row = slots ? slots + (size_t)k * 12 : grad_screen + (size_t)sP[j] * 12;
                         float4 *dst = reinterpret_cast<float4 *>(row) + (lane >> 3);
-                        atomicAdd(dst, make_float4(v, v1, v2, v3));
+                        atomicAdd(dst, make_float4(v0, v1, v2, v3));
                     }
                 }
             }
@@ -337,6 +435,11 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
 }
 
 }  // namespace ssg
+
+extern "C" int64_t ssg_blend_mask_words(int64_t m, int32_t n_tiles) {
+    // mask_word(): bases start/32 + tile + chunk, 8 warps each
+    return m < 0 || n_tiles < 0 ? -1 : 8 * (m / 32 + (int64_t)n_tiles + 1);
+}
 
 extern "C" int ssg_blend_forward(int64_t m, int32_t width, int32_t height, const float background[3],
                                  const ssg_splat *splat, const ssg_bin_buffers *bins,
@@ -350,7 +453,7 @@ extern "C" int ssg_blend_forward(int64_t m, int32_t width, int32_t height, const
     k_blend_forward<false><<<ntx * nty, kThreads, 0, st>>>(ntx, width, height, background[0], background[1],
                                                            background[2], splat, bins->inst_prim, bins->ranges,
                                                            frame->color, frame->final_T, frame->n_contrib,
-                                                           frame->last_idx);
+                                                           frame->last_idx, frame->blend_mask);
     return check_launch("k_blend_forward");
 }
 
@@ -362,7 +465,7 @@ extern "C" int ssg_test_blend_forward_vanilla(int32_t width, int32_t height, con
     int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
     k_blend_forward<true><<<ntx * nty, kThreads, 0, (cudaStream_t)stream>>>(
         ntx, width, height, background[0], background[1], background[2], splat, bins->inst_prim, bins->ranges,
-        frame->color, frame->final_T, frame->n_contrib, frame->last_idx);
+        frame->color, frame->final_T, frame->n_contrib, frame->last_idx, nullptr);
     return check_launch("k_blend_forward<vanilla>");
 }
 
@@ -380,8 +483,8 @@ extern "C" int ssg_blend_backward(int64_t n, int64_t m, int32_t width, int32_t h
     int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
     k_blend_backward<<<ntx * nty, kThreads, 0, st>>>(ntx, width, height, background[0], background[1],
                                                      background[2], splat, bins->inst_prim, bins->ranges,
-                                                     frame->final_T, frame->last_idx, dL_dpixels,
-                                                     grads->screen, nullptr);
+                                                     frame->final_T, frame->last_idx, frame->blend_mask,
+                                                     dL_dpixels, grads->screen, nullptr);
     return check_launch("k_blend_backward");
 }
 
@@ -398,7 +501,18 @@ extern "C" int ssg_blend_backward_slots(int64_t m, int32_t width, int32_t height
     int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
     k_blend_backward<<<ntx * nty, kThreads, 0, st>>>(ntx, width, height, background[0], background[1],
                                                      background[2], splat, bins->inst_prim, bins->ranges,
-                                                     frame->final_T, frame->last_idx, dL_dpixels, nullptr,
-                                                     slots);
+                                                     frame->final_T, frame->last_idx, frame->blend_mask,
+                                                     dL_dpixels, nullptr, slots);
     return check_launch("k_blend_backward(slots)");
 }
+
+#ifdef SSG_BLEND_STATS
+extern "C" int ssg_test_blend_stats(unsigned long long *out, int reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_blend_stats, sizeof(unsigned long long) * 32);
+    if (e == cudaSuccess && reset) {
+        static const unsigned long long zero[32] = {0};
+        e = cudaMemcpyToSymbol(g_blend_stats, zero, sizeof(zero));
+    }
+    return e == cudaSuccess ? SSG_OK : SSG_ERR_CUDA;
+}
+#endif

@@ -136,6 +136,9 @@ class Engine:
         self._grad_key = None
         self.capacity = 0
         self.last_m = 0
+        self._bin_gen = 0          # bumped by every binning
+        self._mask_state = None    # (bin_gen, final_T ptr, last_idx ptr) the blend mask belongs to
+        self.blend_mask = None
         self.stage_events = None  # name -> [(start, end)] CUDA events when enabled
 
     def _mark(self, name: str):
@@ -195,6 +198,9 @@ class Engine:
             self.inst_prim = self._empty((cap,), torch.int32)
             self.inst_tile = self._empty((cap,), torch.int16)
             self.capacity = cap
+        words = int(self.lib.ssg_blend_mask_words(cap, max(n_tiles, 1)))
+        if self.blend_mask is None or self.blend_mask.numel() < words:
+            self.blend_mask = self._empty((words,), torch.int32)
         self.ranges = self._empty((n_tiles, 2), torch.int32)
         nbytes = ctypes.c_size_t(0)
         N.check(self.lib.ssg_bin_temp_bytes(self._prim_n, cap, max(n_tiles, 1), ctypes.byref(nbytes)),
@@ -221,8 +227,9 @@ class Engine:
         self.last_idx = self._empty((H, W), torch.int32)
         self._frame_key = (W, H)
 
-    def _frame_struct(self, final_T=None, last_idx=None, color=None) -> N.SsgFrameBuffers:
+    def _frame_struct(self, final_T=None, last_idx=None, color=None, mask=False) -> N.SsgFrameBuffers:
         f = N.SsgFrameBuffers()
+        f.blend_mask = _ptr(self.blend_mask) if mask else None
         f.color, f.n_contrib = _ptr(self.color if color is None else color), _ptr(self.n_contrib)
         f.final_T = _ptr(self.final_T if final_T is None else final_T)
         f.last_idx = _ptr(self.last_idx if last_idx is None else last_idx)
@@ -279,6 +286,7 @@ class Engine:
             N.check(self.lib.ssg_bin_finish(n, m, W, H, ctypes.byref(prim), ctypes.byref(self._bins_struct()), st),
                     "ssg_bin_finish")
         self.last_m = m
+        self._bin_gen += 1
         return m
 
     def project_and_bin(self, ds: DeviceScene, cam: N.SsgCamera) -> int:
@@ -317,8 +325,10 @@ class Engine:
         bg = (ctypes.c_float * 3)(*[float(x) for x in ds.background])
         with self._mark("blend_fwd"):
             N.check(self.lib.ssg_blend_forward(m, W, H, bg, _ptr(self.splat), ctypes.byref(self._bins_struct()),
-                                               ctypes.byref(self._frame_struct(color=color_out)), self._stream()),
+                                               ctypes.byref(self._frame_struct(color=color_out, mask=True)),
+                                               self._stream()),
                     "ssg_blend_forward")
+        self._mask_state = (self._bin_gen, _ptr(self.final_T), _ptr(self.last_idx))
         color = self.color if color_out is None else color_out
         return DeviceFrame(color, self.final_T, self.n_contrib, self.last_idx, W, H, ds.n, m, s)
 
@@ -342,10 +352,13 @@ class Engine:
         bg = (ctypes.c_float * 3)(*[float(x) for x in ds.background])
         st = self._stream()
         gs = self._grad_struct()
+        # the forward's blend mask is reusable only for the same binning and
+        # the same frame buffers that forward wrote
+        use_mask = self._mask_state == (self._bin_gen, _ptr(final_T), _ptr(last_idx))
         with self._mark("blend_bwd"):
             N.check(self.lib.ssg_blend_backward(ds.n, m, W, H, bg, _ptr(self.splat), ctypes.byref(self._bins_struct()),
-                                                ctypes.byref(self._frame_struct(final_T, last_idx)), _ptr(dL),
-                                                ctypes.byref(gs), st),
+                                                ctypes.byref(self._frame_struct(final_T, last_idx, mask=use_mask)),
+                                                _ptr(dL), ctypes.byref(gs), st),
                     "ssg_blend_backward")
         sc = ds.struct()
         with self._mark("preprocess_bwd"):

@@ -16,7 +16,7 @@ HEADER = os.path.join(ROOT, "include", "ssg_b200.h")
 
 def declared_functions():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"^(?:int|void|size_t|const char \*)\s*\*?\s*(ssg_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^(?:int|int64_t|void|size_t|const char \*)\s*\*?\s*(ssg_\w+)\s*\(", src, re.M)))
 
 
 def test_header_declares_the_exports():
@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     L = N.lib()
     for name in declared_functions():
         assert hasattr(L, name), name
-    assert L.ssg_abi_version() == 1
+    assert L.ssg_abi_version() == N.ABI_VERSION
 
 
 def test_grid_dims_query():
