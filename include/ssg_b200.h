@@ -171,7 +171,7 @@ int ssg_abi_version(void);
 const char *ssg_last_error(void);
 void ssg_grid_dims(int32_t width, int32_t height, int32_t *tiles_x, int32_t *tiles_y);
 /* temporary storage needed by ssg_bin_prepare / ssg_bin_finish */
-int ssg_bin_temp_bytes(int64_t n, int64_t capacity, int32_t n_tiles, size_t *bytes);
+int ssg_bin_temp_bytes(int64_t n, int64_t capacity, int32_t width, int32_t height, size_t *bytes);
 
 /* ---- forward ------------------------------------------------------------ */
 int ssg_preprocess_forward(const ssg_scene *scene, const ssg_camera *cam,

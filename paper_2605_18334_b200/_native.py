@@ -105,7 +105,7 @@ def lib():
     L.ssg_abi_version.restype = ctypes.c_int
     P = ctypes.POINTER
     L.ssg_grid_dims.argtypes = [ctypes.c_int32, ctypes.c_int32, P(ctypes.c_int32), P(ctypes.c_int32)]
-    L.ssg_bin_temp_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+    L.ssg_bin_temp_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                      P(ctypes.c_size_t)]
     L.ssg_preprocess_forward.argtypes = [P(SsgScene), P(SsgCamera), P(SsgPrimBuffers), _vp]
     L.ssg_bin_rects.argtypes = [ctypes.c_int64, _vp, _vp, _vp, _vp, ctypes.c_int32,

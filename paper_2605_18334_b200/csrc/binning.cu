@@ -2,40 +2,39 @@
 //
 // Reference: raster/tiles.py:43-79 (bin_arrays).  The reference emits one
 // instance per covered tile and lexsorts by (tile, depth, primitive id).
-// Here the same order is produced in two stable stages, all hand-written:
+// Here the same order is produced without ever sorting the instances:
 //   1. stable radix sort of primitives by their full 64-bit fp64 depth key
-//      (equal depths keep primitive-id order)            -> depth rank
-//   2. counts in depth-rank order, single-pass look-back scan -> offsets
-//   3. warp-cooperative duplication (coalesced writes) of each primitive's
-//      tiles in depth-rank order, then a stable radix sort of the instances
-//      by tile id (13-16 bit key, two passes)          -> (tile, depth, id)
-// Ranges are the per-tile [first, last+1) of the sorted tile ids with empty
-// tiles set to the insertion point, i.e. exactly np.searchsorted(...,
-// "left"/"right") (tiles.py:76-78).
+//      (equal depths keep primitive-id order)                 -> depth rank
+//   2. counts in depth-rank order, single-pass look-back scan -> M
+//   3. two-level stable counting scatter of the depth-ordered primitives:
+//      tile rows, then the tiles of each row (see below)  -> (tile, depth, id)
+// The ranges fall out of step 3 as the exclusive scan of the per-tile counts:
+// [start, start + count), empty tiles at the insertion point, i.e. exactly
+// np.searchsorted(..., "left"/"right") (tiles.py:76-78).
 #include "radix_sort.cuh"
 #include "ssg_common.cuh"
 
 namespace ssg {
 
-static int tile_passes(int32_t n_tiles) {
-    int b = 1;
-    while ((1 << b) < n_tiles) b++;
-    return (b + 7) / 8;
-}
-
 constexpr int kScanThreads = 256, kScanIPT = 16, kScanTile = kScanThreads * kScanIPT;
 
+// temp = [scan look-back | work area]; the work area holds the depth sort
+// (bin_prepare), then the counting-scatter tables or the tile sort
+// (bin_finish).  n_tiles < 1 sizes the bin_prepare part only.
 struct BinTemp {
     size_t sort_depth, sort_tile, scan_lookback, total;
 };
 
-static BinTemp bin_temp(int64_t n, int64_t capacity) {
+static size_t cs_temp_bytes(int64_t n, int64_t capacity, int32_t width, int32_t height);
+
+// width < 1 sizes the bin_prepare part only
+static BinTemp bin_temp(int64_t n, int64_t capacity, int32_t width, int32_t height) {
     BinTemp b;
     b.sort_depth = radix::temp_bytes<uint64_t>(n > 0 ? n : 1);
-    b.sort_tile = radix::temp_bytes<uint16_t>(capacity > 0 ? capacity : 1);
+    b.sort_tile = width < 1 ? 0 : cs_temp_bytes(n, capacity, width, height);
     b.scan_lookback = radix::align256(sizeof(uint64_t) * (size_t)((n + kScanTile - 1) / kScanTile + 1) + 256);
-    size_t m = b.sort_depth > b.sort_tile ? b.sort_depth : b.sort_tile;
-    b.total = m + b.scan_lookback;
+    const size_t m = b.sort_depth > b.sort_tile ? b.sort_depth : b.sort_tile;
+    b.total = b.scan_lookback + m;
     return b;
 }
 
@@ -105,48 +104,500 @@ k_scan_counts(const uint32_t *__restrict__ order, const uint32_t *__restrict__ c
     }
 }
 
-// tiles.py:59-70: each primitive's instances in row-major tile order, in
-// depth-rank order.  A warp owns 32 consecutive ranks, whose instances are
-// contiguous in the output; lanes stride over that span (coalesced stores)
-// and find their primitive by a 5-step shuffle binary search.
-__global__ void __launch_bounds__(256)
-k_duplicate(const uint32_t *__restrict__ order, const uint64_t *__restrict__ rank_offset,
-            const uint64_t *__restrict__ rect, int32_t ntx, int64_t n, uint16_t *__restrict__ inst_tile,
-            uint32_t *__restrict__ inst_prim) {
-    const int lane = threadIdx.x & 31;
-    const int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane;
-    if (r0 >= n) return;
-    const int64_t r = r0 + lane;
-    const uint64_t off = rank_offset[r < n ? r : n];
-    const uint64_t end = __shfl_sync(0xffffffffu, rank_offset[r0 + 32 < n ? r0 + 32 : n], 0);
-    uint32_t prim = 0;
-    uint64_t rc = 0;
-    if (r < n) {
-        prim = order[r];
-        const uint64_t nxt = rank_offset[r + 1];
-        if (nxt > off) rc = rect[prim];
-    }
-    const uint64_t first = __shfl_sync(0xffffffffu, off, 0);
-    const uint32_t rlo = (uint32_t)rc, rhi = (uint32_t)(rc >> 32);
-    for (uint64_t g0 = first; g0 < end; g0 += 32) {  // warp-uniform trip count (shuffles below)
-        const uint64_t g = g0 + lane;
-        int j = 0;
+// ------------------------------------------------------------------------
+// Two-level counting scatter (default path for step 3).
+//
+// Level 1 splits every primitive's tile rectangle into row segments and
+// scatters them, stably, into per-row lists (buckets = tile rows); level 2
+// scatters each row list, stably, into per-tile lists (buckets = the row's
+// tiles).  Both levels are the same stable counting scatter over an ordered
+// item stream where each item covers a contiguous bucket range [b0, b1):
+//   count    per (chunk of items, bucket) counts            (smem atomics)
+//   scan     per bucket over chunks, then over buckets      (-> bases, ranges)
+//   scatter  one warp per chunk walks its items in order, 32 per step; the
+//            lanes of a step rank themselves inside each bucket by an
+//            atomicOr lane mask (rank = popcount of lower lanes), the lowest
+//            lane advances the warp's per-bucket cursor.
+// Bucket counts per level are <= 4096 (rows or tiles of one row), so each
+// warp's cursors and masks live in shared memory and every item costs a few
+// instructions per covered bucket -- no instance sort.
+#ifndef SSG_CS_C1
+#define SSG_CS_C1 256
+#endif
+#ifndef SSG_CS_C2
+#define SSG_CS_C2 256
+#endif
+#ifndef SSG_CS_STAGE
+#define SSG_CS_STAGE 1024
+#endif
+constexpr int kCsWarps = 4;                  // chunk workers per CTA
+constexpr int kCsC1 = SSG_CS_C1;             // primitives per level-1 chunk
+constexpr int kCsC2 = SSG_CS_C2;             // row segments per level-2 chunk
+constexpr int kCsStage = SSG_CS_STAGE;       // staged outputs per warp (coalesced flush)
+
+struct CsLayout {
+    int64_t nch1;                            // level-1 chunks
+    int64_t max_ch2;                         // bound on level-2 chunks
+    size_t cnt1, row_total, row_start, chunk_base, ctl, cnt2, tile_total, tile_start, rowlist, total;
+};
+
+static CsLayout cs_layout(int64_t n, int64_t capacity, int32_t ntx, int32_t nty) {
+    CsLayout L;
+    L.nch1 = (n + kCsC1 - 1) / kCsC1;
+    if (L.nch1 < 1) L.nch1 = 1;
+    const int64_t cap = capacity > 0 ? capacity : 1;
+    L.max_ch2 = cap / kCsC2 + nty + 1;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { const size_t at = o; o += radix::align256(bytes); return at; };
+    L.cnt1 = take(sizeof(uint32_t) * (size_t)nty * L.nch1);
+    L.row_total = take(sizeof(uint32_t) * (size_t)(nty + 1));
+    L.row_start = take(sizeof(uint32_t) * (size_t)(nty + 1));
+    L.chunk_base = take(sizeof(uint32_t) * (size_t)(nty + 1));
+    L.ctl = take(sizeof(uint32_t) * 4);
+    L.cnt2 = take(sizeof(uint32_t) * (size_t)ntx * L.max_ch2);
+    L.tile_total = take(sizeof(uint32_t) * (size_t)ntx * nty);
+    L.tile_start = take(sizeof(uint32_t) * (size_t)ntx * nty);
+    L.rowlist = take(sizeof(uint64_t) * (size_t)cap);
+    L.total = o;
+    return L;
+}
+
+static size_t cs_temp_bytes(int64_t n, int64_t capacity, int32_t width, int32_t height) {
+    const int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
+    return cs_layout(n, capacity, ntx, nty).total;
+}
+
+// shared memory per scatter warp: staging (u64 / u32 payload + u16 bucket)
+// then two u32 arrays over the buckets (cursor, flush delta)
+template <typename P>
+__host__ __device__ constexpr size_t cs_stage_bytes() { return (sizeof(P) + sizeof(uint16_t)) * kCsStage; }
+template <typename P>
+__host__ __device__ inline size_t cs_warp_smem(int nb) { return cs_stage_bytes<P>() + 8 * (size_t)nb; }
+
+__device__ __forceinline__ void rect_unpack(uint64_t rc, int &x0, int &x1, int &y0, int &y1) {
+    x0 = (int)(rc & 0xffff);
+    x1 = (int)((rc >> 16) & 0xffff);
+    y0 = (int)((rc >> 32) & 0xffff);
+    y1 = (int)(rc >> 48);
+}
+
+// Warp-wide exclusive scan, in place, of a[0, len) (sequential 32-wide blocks).
+__device__ __forceinline__ uint32_t warp_exclusive_scan(uint32_t *a, int len, int lane) {
+    uint32_t carry = 0;
+    for (int b = 0; b < len; b += 32) {
+        const int i = b + lane;
+        const uint32_t v = i < len ? a[i] : 0u;
+        uint32_t x = v;
 #pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-            const uint64_t oc = __shfl_sync(0xffffffffu, off, j + step);
-            if (oc <= g) j += step;
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+            if (lane >= off) x += y;
         }
-        const uint64_t oj = __shfl_sync(0xffffffffu, off, j);
-        const uint32_t lo = __shfl_sync(0xffffffffu, rlo, j), hi = __shfl_sync(0xffffffffu, rhi, j);
-        const uint32_t pj = __shfl_sync(0xffffffffu, prim, j);
-        const int x0 = (int)(lo & 0xffff), x1 = (int)(lo >> 16), y0 = (int)(hi & 0xffff);
-        const int nx = x1 - x0;
-        if (g < end) {
-            const int local = (int)(g - oj);
-            const int ty = y0 + local / nx, tx = x0 + local % nx;
-            inst_tile[g] = (uint16_t)(ty * ntx + tx);
-            inst_prim[g] = pj;
+        if (i < len) a[i] = carry + x - v;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    return carry;
+}
+
+// Ordered walk of one warp's items [i0, i1): each item covers buckets
+// [b0, b1) and carries a payload.  Items are expanded 32 instances per step
+// (item-major, bucket-minor: the output order); equal buckets inside a step
+// are ranked by lane (match_any), across steps by the warp's cursors scur[].
+template <typename P, typename Load, typename Emit>
+__device__ __forceinline__ void cs_walk(int64_t i0, int64_t i1, int lane, uint32_t *scur, Load &&load, Emit &&emit) {
+    const uint32_t lt = radix::lanemask_lt();
+    for (int64_t a = i0; a < i1; a += 32) {
+        const int64_t i = a + lane;
+        int b0 = 0, b1 = 0;
+        P pay = 0;
+        if (i < i1) load(i, b0, b1, pay);
+        const uint32_t len = (uint32_t)(b1 - b0);
+        uint32_t inc = len;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, off);
+            if (lane >= off) inc += y;
         }
+        const uint32_t pre = inc - len, tot = __shfl_sync(0xffffffffu, inc, 31);
+        for (uint32_t g0 = 0; g0 < tot; g0 += 32) {
+            const uint32_t g = g0 + lane;
+            int j = 0;
+#pragma unroll
+            for (int step = 16; step >= 1; step >>= 1)
+                if (__shfl_sync(0xffffffffu, pre, j + step) <= g) j += step;
+            const uint32_t pj = __shfl_sync(0xffffffffu, pre, j);
+            const int bj = __shfl_sync(0xffffffffu, b0, j);
+            P payj;
+            if constexpr (sizeof(P) == 8) {
+                const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)pay, j);
+                const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)((uint64_t)pay >> 32), j);
+                payj = (P)(((uint64_t)hi << 32) | lo);
+            } else {
+                payj = __shfl_sync(0xffffffffu, pay, j);
+            }
+            const bool v = g < tot;
+            const int b = bj + (int)(g - pj);
+            const uint32_t peers = __match_any_sync(0xffffffffu, v ? (uint32_t)b : 0xffffffffu);
+            const uint32_t base = v ? scur[b] : 0u;
+            __syncwarp();
+            if (v && (peers & lt) == 0) scur[b] = base + (uint32_t)__popc(peers);
+            __syncwarp();
+            if (v) emit(b, base + (uint32_t)__popc(peers & lt), payj);
+        }
+    }
+}
+
+// Per-chunk cursor setup shared by both scatters.  count_of(b) = the chunk's
+// items in bucket b, gbase_of(b) = its first global output position.  The
+// chunk's outputs are staged in shared memory (bucket-major) when they fit
+// and flushed in coalesced runs; otherwise written in place.
+// Returns the chunk's output count; staged iff it is <= kCsStage.
+template <typename CountOf, typename GbaseOf>
+__device__ __forceinline__ uint32_t cs_setup(uint32_t *scur, uint32_t *delta, int nb, int lane, CountOf &&count_of,
+                                             GbaseOf &&gbase_of) {
+    for (int b = lane; b < nb; b += 32) scur[b] = count_of(b);
+    __syncwarp();
+    const uint32_t total = warp_exclusive_scan(scur, nb, lane);  // local starts
+    const bool staged = total <= (uint32_t)kCsStage;
+    for (int b = lane; b < nb; b += 32) {
+        const uint32_t g = gbase_of(b), l = scur[b];
+        delta[b] = g - l;
+        if (!staged) scur[b] = g;
+    }
+    __syncwarp();
+    return total;
+}
+
+// level 1, count (difference array over rows): cnt1[row][chunk]
+__global__ void __launch_bounds__(32 * kCsWarps) k_cs1_count(const uint32_t *__restrict__ order,
+                                                             const uint32_t *__restrict__ count,
+                                                             const uint64_t *__restrict__ rect, int64_t n,
+                                                             int64_t nch1, int32_t nty, uint32_t *__restrict__ cnt1) {
+    extern __shared__ uint32_t s_cs[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t *h = s_cs + (size_t)w * (nty + 1);
+    const int64_t c = (int64_t)blockIdx.x * kCsWarps + w;
+    if (c >= nch1) return;
+    for (int y = lane; y <= nty; y += 32) h[y] = 0;
+    __syncwarp();
+    const int64_t r1 = min(n, (c + 1) * kCsC1);
+    for (int64_t r = c * kCsC1 + lane; r < r1; r += 32) {
+        const uint32_t p = order[r];
+        if (count[p] == 0) continue;
+        int x0, x1, y0, y1;
+        rect_unpack(rect[p], x0, x1, y0, y1);
+        atomicAdd(&h[y0], 1u);
+        atomicAdd(&h[y1], 0xffffffffu);
+    }
+    __syncwarp();
+    uint32_t carry = 0;
+    for (int b = 0; b < nty; b += 32) {
+        const int y = b + lane;
+        uint32_t x = y < nty ? h[y] : 0u;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, x, off);
+            if (lane >= off) x += u;
+        }
+        if (y < nty) cnt1[(size_t)y * nch1 + c] = carry + x;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+}
+
+// Exclusive scan, in place, of `len` u32 at a (one CTA); returns the total.
+__device__ __forceinline__ uint32_t cta_exclusive_scan(uint32_t *a, int64_t len, uint32_t *s_warp, uint32_t &s_carry) {
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
+    if (t == 0) s_carry = 0;
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < len; c0 += blockDim.x) {
+        const int64_t i = c0 + t;
+        const uint32_t v = i < len ? a[i] : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+            if (lane >= off) x += y;
+        }
+        if (lane == 31) s_warp[w] = x;
+        __syncthreads();
+        uint32_t wpre = 0, tot = 0;
+        for (int ww = 0; ww < nw; ww++) {
+            const uint32_t sw = s_warp[ww];
+            wpre += ww < w ? sw : 0u;
+            tot += sw;
+        }
+        const uint32_t carry = s_carry;
+        if (i < len) a[i] = carry + wpre + x - v;
+        __syncthreads();
+        if (t == 0) s_carry = carry + tot;
+        __syncthreads();
+    }
+    return s_carry;
+}
+
+// Exclusive scan with one CTA of 1024 threads, each owning a contiguous run
+// (read twice): src -> dst (may alias); returns the total.
+__device__ __forceinline__ uint32_t cta_scan_runs(const uint32_t *src, uint32_t *dst, int len, uint32_t *s_warp) {
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int per = (len + 1023) / 1024;
+    const int lo = min(len, t * per), hi = min(len, lo + per);
+    uint32_t sum = 0;
+    for (int q = lo; q < hi; q++) sum += src[q];
+    uint32_t x = sum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+    }
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t z = s_warp[lane];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, z, off);
+            if (lane >= off) z += y;
+        }
+        s_warp[lane] = z;
+    }
+    __syncthreads();
+    uint32_t run = (w > 0 ? s_warp[w - 1] : 0u) + x - sum;
+    const uint32_t total = s_warp[31];
+    for (int q = lo; q < hi; q++) {
+        const uint32_t v = src[q];
+        dst[q] = run;
+        run += v;
+    }
+    return total;
+}
+
+// level 1, per-row scan over chunks (one CTA per row)
+__global__ void __launch_bounds__(256) k_cs1_rowscan(uint32_t *__restrict__ cnt1, int64_t nch1,
+                                                     uint32_t *__restrict__ row_total) {
+    __shared__ uint32_t s_warp[8];
+    __shared__ uint32_t s_carry;
+    const uint32_t tot = cta_exclusive_scan(cnt1 + (size_t)blockIdx.x * nch1, nch1, s_warp, s_carry);
+    if (threadIdx.x == 0) row_total[blockIdx.x] = tot;
+}
+
+// one CTA: row starts (exclusive scan of row totals) and level-2 chunk bases
+// (exclusive scan of ceil(total / C2)); ctl[0] = number of level-2 chunks
+__global__ void __launch_bounds__(1024) k_cs1_rowstart(const uint32_t *__restrict__ row_total, int32_t nty,
+                                                       uint32_t *__restrict__ row_start,
+                                                       uint32_t *__restrict__ chunk_base, uint32_t *__restrict__ ctl) {
+    __shared__ uint32_t s_warp[32];
+    for (int y = threadIdx.x; y < nty; y += blockDim.x) chunk_base[y] = (row_total[y] + kCsC2 - 1) / kCsC2;
+    __syncthreads();
+    const uint32_t rt = cta_scan_runs(row_total, row_start, nty, s_warp);
+    __syncthreads();
+    const uint32_t ct = cta_scan_runs(chunk_base, chunk_base, nty, s_warp);
+    if (threadIdx.x == 0) {
+        row_start[nty] = rt;
+        chunk_base[nty] = ct;
+        ctl[0] = ct;
+    }
+}
+
+// level 1, scatter: row segments (prim | x0 << 32 | x1 << 48) into per-row lists
+__global__ void __launch_bounds__(32 * kCsWarps) k_cs1_scatter(const uint32_t *__restrict__ order,
+                                                               const uint32_t *__restrict__ count,
+                                                               const uint64_t *__restrict__ rect, int64_t n,
+                                                               int64_t nch1, int32_t nty,
+                                                               const uint32_t *__restrict__ cnt1,
+                                                               const uint32_t *__restrict__ row_total,
+                                                               const uint32_t *__restrict__ row_start,
+                                                               uint64_t *__restrict__ rowlist) {
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned char *base = s_raw + (size_t)w * cs_warp_smem<uint64_t>(nty);
+    uint64_t *st_pay = reinterpret_cast<uint64_t *>(base);
+    uint16_t *st_b = reinterpret_cast<uint16_t *>(base + sizeof(uint64_t) * kCsStage);
+    uint32_t *scur = reinterpret_cast<uint32_t *>(base + cs_stage_bytes<uint64_t>()), *delta = scur + nty;
+    const int64_t c = (int64_t)blockIdx.x * kCsWarps + w;
+    if (c >= nch1) return;
+    const uint32_t total = cs_setup(
+        scur, delta, nty, lane,
+        [&](int y) {
+            const uint32_t e = c + 1 < nch1 ? cnt1[(size_t)y * nch1 + c + 1] : row_total[y];
+            return e - cnt1[(size_t)y * nch1 + c];
+        },
+        [&](int y) { return row_start[y] + cnt1[(size_t)y * nch1 + c]; });
+    const bool staged = total <= (uint32_t)kCsStage;
+    const int64_t r1 = min(n, (c + 1) * kCsC1);
+    cs_walk<uint64_t>(
+        c * kCsC1, r1, lane, scur,
+        [&](int64_t r, int &b0, int &b1, uint64_t &pay) {
+            const uint32_t p = order[r];
+            if (count[p] == 0) return;
+            int x0, x1;
+            rect_unpack(rect[p], x0, x1, b0, b1);
+            pay = (uint64_t)p | ((uint64_t)x0 << 32) | ((uint64_t)x1 << 48);
+        },
+        [&](int y, uint32_t pos, uint64_t pay) {
+            if (staged) {
+                st_pay[pos] = pay;
+                st_b[pos] = (uint16_t)y;
+            } else {
+                rowlist[pos] = pay;
+            }
+        });
+    if (staged) {  // bucket-major local order: runs of one row are contiguous in rowlist
+        __syncwarp();
+        for (uint32_t i = lane; i < total; i += 32) rowlist[delta[st_b[i]] + i] = st_pay[i];
+    }
+}
+
+// level-2 chunk id -> row by binary search of chunk_base
+__device__ __forceinline__ int cs2_row_of(const uint32_t *__restrict__ chunk_base, int32_t nty, uint32_t c) {
+    int lo = 0, hi = nty;  // chunk_base[lo] <= c < chunk_base[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (chunk_base[mid] <= c) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// level 2, count (difference array over the row's tiles): cnt2 block of row y
+// laid out [x][k] (tile-major, chunk-minor)
+__global__ void __launch_bounds__(32 * kCsWarps) k_cs2_count(const uint64_t *__restrict__ rowlist,
+                                                             const uint32_t *__restrict__ row_start,
+                                                             const uint32_t *__restrict__ chunk_base,
+                                                             const uint32_t *__restrict__ ctl, int32_t ntx,
+                                                             int32_t nty, uint32_t *__restrict__ cnt2) {
+    extern __shared__ uint32_t s_cs[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t *h = s_cs + (size_t)w * (ntx + 1);
+    const uint32_t nch2 = ctl[0];
+    for (uint32_t c = blockIdx.x * kCsWarps + w; c < nch2; c += gridDim.x * kCsWarps) {
+        const int y = cs2_row_of(chunk_base, nty, c);
+        const uint32_t k = c - chunk_base[y], nk = chunk_base[y + 1] - chunk_base[y];
+        for (int x = lane; x <= ntx; x += 32) h[x] = 0;
+        __syncwarp();
+        const uint32_t i0 = row_start[y] + k * kCsC2, i1 = min(row_start[y + 1], i0 + kCsC2);
+        for (uint32_t i = i0 + lane; i < i1; i += 32) {
+            const uint64_t seg = rowlist[i];
+            atomicAdd(&h[(int)((seg >> 32) & 0xffff)], 1u);
+            atomicAdd(&h[(int)(seg >> 48)], 0xffffffffu);
+        }
+        __syncwarp();
+        uint32_t *blk = cnt2 + (size_t)chunk_base[y] * ntx;
+        uint32_t carry = 0;
+        for (int b = 0; b < ntx; b += 32) {
+            const int x = b + lane;
+            uint32_t v = x < ntx ? h[x] : 0u;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xffffffffu, v, off);
+                if (lane >= off) v += u;
+            }
+            if (x < ntx) blk[(size_t)x * nk + k] = carry + v;
+            carry += __shfl_sync(0xffffffffu, v, 31);
+        }
+        __syncwarp();
+    }
+}
+
+// level 2, per-tile exclusive scan over the row's chunks (one warp per tile)
+__global__ void __launch_bounds__(256) k_cs2_tilescan(uint32_t *__restrict__ cnt2,
+                                                      const uint32_t *__restrict__ chunk_base, int32_t ntx,
+                                                      int32_t nty, uint32_t *__restrict__ tile_total) {
+    const int lane = threadIdx.x & 31;
+    const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (t >= (int64_t)ntx * nty) return;
+    const int y = (int)(t / ntx), x = (int)(t - (int64_t)y * ntx);
+    const uint32_t nk = chunk_base[y + 1] - chunk_base[y];
+    uint32_t *a = cnt2 + (size_t)chunk_base[y] * ntx + (size_t)x * nk;
+    uint32_t carry = 0;
+    for (uint32_t k0 = 0; k0 < nk; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        const uint32_t v = k < nk ? a[k] : 0u;
+        uint32_t s = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, s, off);
+            if (lane >= off) s += u;
+        }
+        if (k < nk) a[k] = carry + s - v;
+        carry += __shfl_sync(0xffffffffu, s, 31);
+    }
+    if (lane == 0) tile_total[t] = carry;
+}
+
+// one CTA: tile starts (exclusive scan of the totals) and ranges
+// [start, start + total): empty tiles sit at the insertion point, exactly
+// np.searchsorted left/right (tiles.py:76-78)
+__global__ void __launch_bounds__(1024) k_cs2_tilestart(const uint32_t *__restrict__ tile_total, int32_t n_tiles,
+                                                        uint32_t *__restrict__ tile_start,
+                                                        int32_t *__restrict__ ranges) {
+    __shared__ uint32_t s_warp[32];
+    cta_scan_runs(tile_total, tile_start, n_tiles, s_warp);
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+        const uint32_t st = tile_start[t];
+        ranges[2 * t] = (int32_t)st;
+        ranges[2 * t + 1] = (int32_t)(st + tile_total[t]);
+    }
+}
+
+// level 2, scatter: per-tile instance lists (inst_prim, inst_tile)
+__global__ void __launch_bounds__(32 * kCsWarps) k_cs2_scatter(const uint64_t *__restrict__ rowlist,
+                                                               const uint32_t *__restrict__ row_start,
+                                                               const uint32_t *__restrict__ chunk_base,
+                                                               const uint32_t *__restrict__ ctl,
+                                                               const uint32_t *__restrict__ cnt2,
+                                                               const uint32_t *__restrict__ tile_total,
+                                                               const uint32_t *__restrict__ tile_start,
+                                                               int32_t ntx, int32_t nty,
+                                                               uint32_t *__restrict__ inst_prim,
+                                                               uint16_t *__restrict__ inst_tile) {
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned char *base = s_raw + (size_t)w * cs_warp_smem<uint32_t>(ntx);
+    uint32_t *st_pay = reinterpret_cast<uint32_t *>(base);
+    uint16_t *st_b = reinterpret_cast<uint16_t *>(base + sizeof(uint32_t) * kCsStage);
+    uint32_t *scur = reinterpret_cast<uint32_t *>(base + cs_stage_bytes<uint32_t>()), *delta = scur + ntx;
+    const uint32_t nch2 = ctl[0];
+    for (uint32_t c = blockIdx.x * kCsWarps + w; c < nch2; c += gridDim.x * kCsWarps) {
+        const int y = cs2_row_of(chunk_base, nty, c);
+        const uint32_t k = c - chunk_base[y], nk = chunk_base[y + 1] - chunk_base[y];
+        const uint32_t *blk = cnt2 + (size_t)chunk_base[y] * ntx;
+        const uint32_t trow = (uint32_t)y * (uint32_t)ntx;
+        const uint32_t total = cs_setup(
+            scur, delta, ntx, lane,
+            [&](int x) {
+                const uint32_t e = k + 1 < nk ? blk[(size_t)x * nk + k + 1] : tile_total[trow + x];
+                return e - blk[(size_t)x * nk + k];
+            },
+            [&](int x) { return tile_start[trow + x] + blk[(size_t)x * nk + k]; });
+        const bool staged = total <= (uint32_t)kCsStage;
+        const uint32_t i0 = row_start[y] + k * kCsC2, i1 = min(row_start[y + 1], i0 + kCsC2);
+        cs_walk<uint32_t>(
+            i0, i1, lane, scur,
+            [&](int64_t i, int &b0, int &b1, uint32_t &pay) {
+                const uint64_t seg = rowlist[i];
+                pay = (uint32_t)seg;
+                b0 = (int)((seg >> 32) & 0xffff);
+                b1 = (int)(seg >> 48);
+            },
+            [&](int x, uint32_t pos, uint32_t p) {
+                if (staged) {
+                    st_pay[pos] = p;
+                    st_b[pos] = (uint16_t)x;
+                } else {
+                    inst_prim[pos] = p;
+                    if (inst_tile) inst_tile[pos] = (uint16_t)(trow + x);
+                }
+            });
+        if (staged) {
+            __syncwarp();
+            for (uint32_t i = lane; i < total; i += 32) {
+                const int x = st_b[i];
+                const uint32_t pos = delta[x] + i;
+                inst_prim[pos] = st_pay[i];
+                if (inst_tile) inst_tile[pos] = (uint16_t)(trow + x);
+            }
+        }
+        __syncwarp();
     }
 }
 
@@ -168,46 +619,6 @@ __global__ void k_rects_from_arrays(int64_t n, const double *mean2d, const doubl
     key[i] = count[i] ? (kk == ~0ull ? kk - 1 : kk) : ~0ull;
 }
 
-// Per-tile [first, last+1) of the sorted tile ids; empty tiles marked -1.
-__global__ void k_tile_bounds(const uint16_t *__restrict__ tile, int64_t m, int32_t *__restrict__ ranges) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= m) return;
-    const int t = tile[i];
-    if (i == 0 || tile[i - 1] != t) ranges[2 * t] = (int32_t)i;
-    if (i == m - 1 || tile[i + 1] != t) ranges[2 * t + 1] = (int32_t)(i + 1);
-}
-
-// Empty tiles get start == end == first instance of the next non-empty tile
-// (M if none): a block-wide suffix-min over the tile starts.
-__global__ void __launch_bounds__(1024) k_fill_empty(int32_t *ranges, int32_t n_tiles, int32_t m) {
-    __shared__ int32_t s_min[1024];
-    const int t = threadIdx.x;
-    const int chunk = (n_tiles + 1023) / 1024;
-    const int lo = t * chunk, hi = min(lo + chunk, n_tiles);
-    int32_t mn = INT32_MAX;
-    for (int i = lo; i < hi; i++)
-        if (ranges[2 * i] >= 0) { mn = ranges[2 * i]; break; }
-    s_min[t] = mn;
-    __syncthreads();
-    // suffix min over chunks (Hillis-Steele, right to left)
-    for (int off = 1; off < 1024; off <<= 1) {
-        const int32_t o = t + off < 1024 ? s_min[t + off] : INT32_MAX;
-        __syncthreads();
-        s_min[t] = min(s_min[t], o);
-        __syncthreads();
-    }
-    int32_t next = t + 1 < 1024 ? s_min[t + 1] : INT32_MAX;
-    if (next == INT32_MAX) next = m;
-    for (int i = hi - 1; i >= lo; i--) {
-        if (ranges[2 * i] >= 0) {
-            next = ranges[2 * i];
-        } else {
-            ranges[2 * i] = next;
-            ranges[2 * i + 1] = next;
-        }
-    }
-}
-
 }  // namespace ssg
 
 extern "C" int ssg_bin_rects(int64_t n, const double *mean2d, const double *radius,
@@ -222,10 +633,11 @@ extern "C" int ssg_bin_rects(int64_t n, const double *mean2d, const double *radi
     return check_launch("k_rects_from_arrays");
 }
 
-extern "C" int ssg_bin_temp_bytes(int64_t n, int64_t capacity, int32_t n_tiles, size_t *bytes) {
+extern "C" int ssg_bin_temp_bytes(int64_t n, int64_t capacity, int32_t width, int32_t height, size_t *bytes) {
     using namespace ssg;
-    if (!bytes || n < 0 || capacity < 0 || n_tiles < 1 || n_tiles > 65536) return SSG_ERR_INVALID_ARGUMENT;
-    *bytes = bin_temp(n, capacity).total;
+    if (!bytes || n < 0 || capacity < 0 || width < 1 || height < 1) return SSG_ERR_INVALID_ARGUMENT;
+    if (width > SSG_MAX_IMAGE_DIM || height > SSG_MAX_IMAGE_DIM) return SSG_ERR_DIM_OVERFLOW;
+    *bytes = bin_temp(n, capacity, width, height).total;
     return SSG_OK;
 }
 
@@ -240,14 +652,15 @@ extern "C" int ssg_bin_prepare(int64_t n, const ssg_prim_buffers *prim, const ss
         if (e != cudaSuccess) { set_error("memset", e); return SSG_ERR_CUDA; }
         return SSG_OK;
     }
-    const BinTemp L = bin_temp(n, bins->capacity);
+    const BinTemp L = bin_temp(n, bins->capacity, 0, 0);
     if (bins->temp_bytes < L.total) return SSG_ERR_CAPACITY;
     char *tmp = (char *)bins->temp;
     // 1. stable sort of primitive ids by depth key (the key buffer is consumed)
-    cudaError_t e = radix::sort_pairs<uint64_t>(prim->depth_key, bins->depth_order, true, n, 8, tmp, st);
+    cudaError_t e = radix::sort_pairs<uint64_t>(prim->depth_key, bins->depth_order, true, n, 8,
+                                                tmp + L.scan_lookback, st);
     if (e != cudaSuccess) { set_error("depth sort", e); return SSG_ERR_CUDA; }
     // 2. counts in depth order, scanned
-    uint64_t *lb = (uint64_t *)(tmp + (L.total - L.scan_lookback));
+    uint64_t *lb = (uint64_t *)tmp;
     const int64_t scan_tiles = (n + kScanTile - 1) / kScanTile;
     e = cudaMemsetAsync(lb, 0, sizeof(uint64_t) * (scan_tiles + 1), st);
     if (e != cudaSuccess) { set_error("memset scan", e); return SSG_ERR_CUDA; }
@@ -259,26 +672,53 @@ extern "C" int ssg_bin_prepare(int64_t n, const ssg_prim_buffers *prim, const ss
 extern "C" int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t height,
                               const ssg_prim_buffers *prim, const ssg_bin_buffers *bins, void *stream) {
     using namespace ssg;
-    if (!prim || !bins || n < 0 || m < 0) return SSG_ERR_INVALID_ARGUMENT;
+    if (!prim || !bins || n < 0 || m < 0 || width < 1 || height < 1) return SSG_ERR_INVALID_ARGUMENT;
     if (m > bins->capacity || m >= (int64_t)INT32_MAX) return SSG_ERR_CAPACITY;
-    int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
-    int32_t n_tiles = ntx * nty;
-    if (n_tiles > 65536) return SSG_ERR_INVALID_ARGUMENT;
+    if (width > SSG_MAX_IMAGE_DIM || height > SSG_MAX_IMAGE_DIM) return SSG_ERR_DIM_OVERFLOW;
+    const int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
+    const int32_t n_tiles = ntx * nty;
+    if (n_tiles > 65536) return SSG_ERR_INVALID_ARGUMENT;  // inst_tile is u16
     cudaStream_t st = (cudaStream_t)stream;
-    cudaError_t e = cudaMemsetAsync(bins->ranges, 0xff, sizeof(int32_t) * 2 * (size_t)n_tiles, st);
-    if (e != cudaSuccess) { set_error("memset ranges", e); return SSG_ERR_CUDA; }
-    if (m > 0) {
-        const BinTemp L = bin_temp(n, bins->capacity);
-        if (bins->temp_bytes < L.total) return SSG_ERR_CAPACITY;
-        k_duplicate<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(bins->depth_order, bins->rank_offset,
-                                                                 prim->tile_rect, ntx, n, bins->inst_tile,
-                                                                 bins->inst_prim);
-        e = radix::sort_pairs<uint16_t>(bins->inst_tile, bins->inst_prim, false, m, tile_passes(n_tiles),
-                                        bins->temp, st);
-        if (e != cudaSuccess) { set_error("tile sort", e); return SSG_ERR_CUDA; }
-        k_tile_bounds<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(bins->inst_tile, m, bins->ranges);
+    const BinTemp T = bin_temp(n, bins->capacity, width, height);
+    if (bins->temp_bytes < T.total) return SSG_ERR_CAPACITY;
+    char *work = (char *)bins->temp + T.scan_lookback;
+    const CsLayout L = cs_layout(n, bins->capacity, ntx, nty);
+    uint32_t *cnt1 = (uint32_t *)(work + L.cnt1), *row_total = (uint32_t *)(work + L.row_total);
+    uint32_t *row_start = (uint32_t *)(work + L.row_start), *chunk_base = (uint32_t *)(work + L.chunk_base);
+    uint32_t *ctl = (uint32_t *)(work + L.ctl), *cnt2 = (uint32_t *)(work + L.cnt2);
+    uint32_t *tile_total = (uint32_t *)(work + L.tile_total);
+    uint64_t *rowlist = (uint64_t *)(work + L.rowlist);
+    uint32_t *tile_start = (uint32_t *)(work + L.tile_start);
+    const size_t sm1 = kCsWarps * cs_warp_smem<uint64_t>(nty), sm2 = kCsWarps * cs_warp_smem<uint32_t>(ntx);
+    const size_t smc1 = sizeof(uint32_t) * kCsWarps * (nty + 1), smc2 = sizeof(uint32_t) * kCsWarps * (ntx + 1);
+    static bool attr = false;
+    if (!attr) {  // the largest grids (4096 tiles per side) need > 48 KB
+        const int mx = (int)(kCsWarps * cs_warp_smem<uint64_t>(4096));
+        cudaFuncSetAttribute(k_cs1_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_cs2_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_cs1_count, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_cs2_count, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        attr = true;
     }
-    k_fill_empty<<<1, 1024, 0, st>>>(bins->ranges, n_tiles, (int32_t)m);
+    const unsigned g1 = (unsigned)((L.nch1 + kCsWarps - 1) / kCsWarps);
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned g2 = (unsigned)(sms * 8);
+    // level 1: row segments in per-row lists
+    k_cs1_count<<<g1, 32 * kCsWarps, smc1, st>>>(bins->depth_order, prim->tile_count, prim->tile_rect, n, L.nch1,
+                                                 nty, cnt1);
+    k_cs1_rowscan<<<nty, 256, 0, st>>>(cnt1, L.nch1, row_total);
+    k_cs1_rowstart<<<1, 1024, 0, st>>>(row_total, nty, row_start, chunk_base, ctl);
+    if (n > 0)
+        k_cs1_scatter<<<g1, 32 * kCsWarps, sm1, st>>>(bins->depth_order, prim->tile_count, prim->tile_rect, n,
+                                                      L.nch1, nty, cnt1, row_total, row_start, rowlist);
+    // level 2: per-tile lists of each row
+    k_cs2_count<<<g2, 32 * kCsWarps, smc2, st>>>(rowlist, row_start, chunk_base, ctl, ntx, nty, cnt2);
+    k_cs2_tilescan<<<(unsigned)(((int64_t)n_tiles * 32 + 255) / 256), 256, 0, st>>>(cnt2, chunk_base, ntx, nty,
+                                                                                    tile_total);
+    k_cs2_tilestart<<<1, 1024, 0, st>>>(tile_total, n_tiles, tile_start, bins->ranges);
+    k_cs2_scatter<<<g2, 32 * kCsWarps, sm2, st>>>(rowlist, row_start, chunk_base, ctl, cnt2, tile_total, tile_start,
+                                                  ntx, nty, bins->inst_prim, bins->inst_tile);
     return check_launch("ssg_bin_finish");
 }
 

@@ -187,11 +187,13 @@ class Engine:
         p.radius, p.n_skew_fallback = _ptr(self.radius), _ptr(self.n_fallback)
         return p
 
-    def _ensure_bins(self, n: int, m: int, n_tiles: int):
+    def _ensure_bins(self, n: int, m: int, W: int, H: int):
+        ntx, nty = grid_dims(W, H)
+        n_tiles = ntx * nty
         cap = self.capacity
         if m > cap:
             cap = max(int(m * 1.25) + 1024, 1024)
-        key = (self._prim_n, cap, n_tiles)
+        key = (self._prim_n, cap, W, H)
         if key == self._bins_key:
             return
         if cap != self.capacity:
@@ -203,7 +205,7 @@ class Engine:
             self.blend_mask = self._empty((words,), torch.int32)
         self.ranges = self._empty((n_tiles, 2), torch.int32)
         nbytes = ctypes.c_size_t(0)
-        N.check(self.lib.ssg_bin_temp_bytes(self._prim_n, cap, max(n_tiles, 1), ctypes.byref(nbytes)),
+        N.check(self.lib.ssg_bin_temp_bytes(self._prim_n, cap, W, H, ctypes.byref(nbytes)),
                 "ssg_bin_temp_bytes")
         self.temp = self._empty((max(int(nbytes.value), 1),), torch.uint8)
         self._bins_key = key
@@ -275,13 +277,13 @@ class Engine:
         """bin_prepare -> M (one 8-byte D2H) -> bin_finish."""
         ntx, nty = grid_dims(W, H)
         st = self._stream()
-        self._ensure_bins(n, self.capacity, ntx * nty)
+        self._ensure_bins(n, self.capacity, W, H)
         prim = self._prim_struct()
         with self._mark("bin_prepare"):
             N.check(self.lib.ssg_bin_prepare(n, ctypes.byref(prim), ctypes.byref(self._bins_struct()), st),
                     "ssg_bin_prepare")
         m = int(self.n_inst_dev.item())
-        self._ensure_bins(n, m, ntx * nty)
+        self._ensure_bins(n, m, W, H)
         with self._mark("bin_finish"):
             N.check(self.lib.ssg_bin_finish(n, m, W, H, ctypes.byref(prim), ctypes.byref(self._bins_struct()), st),
                     "ssg_bin_finish")
