@@ -216,8 +216,9 @@ int ssg_adam_step(const ssg_params *params, const ssg_grad_buffers *grads,
                   const ssg_adam_state *state, const ssg_adam_hparams *hp, void *stream);
 
 /* ---- test hooks (used by tests/ only) ----------------------------------- */
-/* the binning radix sort in isolation: stable sort of (key, u32 value) by the
- * low 8*npass key bits, in place; key_bytes 2 (tile ids) or 8 (depth keys) */
+/* the depth sort of ssg_bin_prepare in isolation: stable sort of u64 keys
+ * (not modified), vals <- the ids 0..n-1 in sorted order; key_bytes must be 8,
+ * iota 1 and npass 8 (any other combination: SSG_ERR_INVALID_ARGUMENT) */
 size_t ssg_test_sort_temp_bytes(int64_t n, int key_bytes);
 int ssg_test_sort(void *keys, uint32_t *vals, int key_bytes, int iota, int64_t n, int npass,
                   void *temp, void *stream);

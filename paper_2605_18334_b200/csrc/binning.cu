@@ -11,97 +11,25 @@
 // The ranges fall out of step 3 as the exclusive scan of the per-tile counts:
 // [start, start + count), empty tiles at the insertion point, i.e. exactly
 // np.searchsorted(..., "left"/"right") (tiles.py:76-78).
-#include "radix_sort.cuh"
+#include "depth_sort.cuh"
 #include "ssg_common.cuh"
 
 namespace ssg {
 
-constexpr int kScanThreads = 256, kScanIPT = 16, kScanTile = kScanThreads * kScanIPT;
-
-// temp = [scan look-back | work area]; the work area holds the depth sort
-// (bin_prepare), then the counting-scatter tables or the tile sort
-// (bin_finish).  n_tiles < 1 sizes the bin_prepare part only.
+// temp = one work area: the depth sort (bin_prepare), then the counting-
+// scatter tables (bin_finish).  width < 1 sizes the bin_prepare part only.
 struct BinTemp {
-    size_t sort_depth, sort_tile, scan_lookback, total;
+    size_t sort_depth, sort_tile, total;
 };
 
 static size_t cs_temp_bytes(int64_t n, int64_t capacity, int32_t width, int32_t height);
 
-// width < 1 sizes the bin_prepare part only
 static BinTemp bin_temp(int64_t n, int64_t capacity, int32_t width, int32_t height) {
     BinTemp b;
-    b.sort_depth = radix::temp_bytes<uint64_t>(n > 0 ? n : 1);
+    b.sort_depth = dsort::temp_bytes(n > 0 ? n : 1);
     b.sort_tile = width < 1 ? 0 : cs_temp_bytes(n, capacity, width, height);
-    b.scan_lookback = radix::align256(sizeof(uint64_t) * (size_t)((n + kScanTile - 1) / kScanTile + 1) + 256);
-    const size_t m = b.sort_depth > b.sort_tile ? b.sort_depth : b.sort_tile;
-    b.total = b.scan_lookback + m;
+    b.total = b.sort_depth > b.sort_tile ? b.sort_depth : b.sort_tile;
     return b;
-}
-
-// Counts in depth order + inclusive scan in one pass (decoupled look-back).
-// rank_offset[r+1] = sum of counts of ranks <= r; rank_offset[0] = 0.
-__global__ void __launch_bounds__(kScanThreads)
-k_scan_counts(const uint32_t *__restrict__ order, const uint32_t *__restrict__ count, int64_t n,
-              uint64_t *__restrict__ rank_offset, uint64_t *__restrict__ lookback, int64_t *n_instances) {
-    __shared__ uint32_t s_tile;
-    __shared__ uint64_t s_warp[kScanThreads / 32];
-    __shared__ uint64_t s_prefix;
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    uint32_t *counter = reinterpret_cast<uint32_t *>(lookback + (n + kScanTile - 1) / kScanTile);
-    if (t == 0) s_tile = atomicAdd(counter, 1u);
-    __syncthreads();
-    const int64_t tile = s_tile;
-    const int64_t base = tile * kScanTile + (int64_t)t * kScanIPT;
-    uint64_t v[kScanIPT];
-    uint64_t sum = 0;
-#pragma unroll
-    for (int i = 0; i < kScanIPT; i++) {
-        const int64_t r = base + i;
-        v[i] = r < n ? count[order[r]] : 0u;
-        sum += v[i];
-    }
-    // block exclusive scan of the per-thread sums
-    uint64_t x = sum;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const uint64_t y = __shfl_up_sync(0xffffffffu, x, off);
-        if (lane >= off) x += y;
-    }
-    if (lane == 31) s_warp[w] = x;
-    __syncthreads();
-    uint64_t wpre = 0, total = 0;
-#pragma unroll
-    for (int ww = 0; ww < kScanThreads / 32; ww++) {
-        wpre += ww < w ? s_warp[ww] : 0ull;
-        total += s_warp[ww];
-    }
-    if (t == 0) {
-        uint64_t excl = 0;
-        if (tile == 0) {
-            atomicExch(reinterpret_cast<unsigned long long *>(lookback), radix::kFlagPre | total);
-        } else {
-            atomicExch(reinterpret_cast<unsigned long long *>(lookback + tile), radix::kFlagAgg | total);
-            for (int64_t p = tile - 1;; p--) {
-                const volatile uint64_t *q = lookback + p;
-                uint64_t val = *q;
-                while ((val >> 62) == 0) val = *q;
-                excl += val & radix::kValMask;
-                if ((val >> 62) == 2) break;
-            }
-            atomicExch(reinterpret_cast<unsigned long long *>(lookback + tile), radix::kFlagPre | (excl + total));
-        }
-        s_prefix = excl;
-        if (base <= n && tile == (n - 1) / kScanTile) *n_instances = (int64_t)(excl + total);
-        if (tile == 0) rank_offset[0] = 0;
-    }
-    __syncthreads();
-    uint64_t run = s_prefix + wpre + x - sum;
-#pragma unroll
-    for (int i = 0; i < kScanIPT; i++) {
-        const int64_t r = base + i;
-        run += v[i];
-        if (r < n) rank_offset[r + 1] = run;
-    }
 }
 
 // ------------------------------------------------------------------------
@@ -654,18 +582,11 @@ extern "C" int ssg_bin_prepare(int64_t n, const ssg_prim_buffers *prim, const ss
     }
     const BinTemp L = bin_temp(n, bins->capacity, 0, 0);
     if (bins->temp_bytes < L.total) return SSG_ERR_CAPACITY;
-    char *tmp = (char *)bins->temp;
-    // 1. stable sort of primitive ids by depth key (the key buffer is consumed)
-    cudaError_t e = radix::sort_pairs<uint64_t>(prim->depth_key, bins->depth_order, true, n, 8,
-                                                tmp + L.scan_lookback, st);
+    // 1+2. stable sort of the ids by depth key, counts in depth order, scan
+    cudaError_t e = dsort::sort_and_scan(prim->depth_key, bins->depth_order, prim->tile_count, bins->rank_offset,
+                                         bins->n_instances, n, bins->temp,
+                                         (cudaStream_t)stream);
     if (e != cudaSuccess) { set_error("depth sort", e); return SSG_ERR_CUDA; }
-    // 2. counts in depth order, scanned
-    uint64_t *lb = (uint64_t *)tmp;
-    const int64_t scan_tiles = (n + kScanTile - 1) / kScanTile;
-    e = cudaMemsetAsync(lb, 0, sizeof(uint64_t) * (scan_tiles + 1), st);
-    if (e != cudaSuccess) { set_error("memset scan", e); return SSG_ERR_CUDA; }
-    k_scan_counts<<<(unsigned)scan_tiles, kScanThreads, 0, st>>>(bins->depth_order, prim->tile_count, n,
-                                                                bins->rank_offset, lb, bins->n_instances);
     return check_launch("ssg_bin_prepare");
 }
 
@@ -681,7 +602,7 @@ extern "C" int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t heigh
     cudaStream_t st = (cudaStream_t)stream;
     const BinTemp T = bin_temp(n, bins->capacity, width, height);
     if (bins->temp_bytes < T.total) return SSG_ERR_CAPACITY;
-    char *work = (char *)bins->temp + T.scan_lookback;
+    char *work = (char *)bins->temp;
     const CsLayout L = cs_layout(n, bins->capacity, ntx, nty);
     uint32_t *cnt1 = (uint32_t *)(work + L.cnt1), *row_total = (uint32_t *)(work + L.row_total);
     uint32_t *row_start = (uint32_t *)(work + L.row_start), *chunk_base = (uint32_t *)(work + L.chunk_base);
@@ -722,18 +643,19 @@ extern "C" int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t heigh
     return check_launch("ssg_bin_finish");
 }
 
-// ---- test hooks (tests/ only): the radix sort in isolation -------------
+// ---- test hooks (tests/ only): the depth sort in isolation ---------------
 extern "C" size_t ssg_test_sort_temp_bytes(int64_t n, int key_bytes) {
     using namespace ssg;
-    return key_bytes == 2 ? radix::temp_bytes<uint16_t>(n) : radix::temp_bytes<uint64_t>(n);
+    return key_bytes == 8 ? dsort::temp_bytes(n) : 0;
 }
 
+// stable sort of u64 keys (not modified): vals <- ids in sorted order
 extern "C" int ssg_test_sort(void *keys, uint32_t *vals, int key_bytes, int iota, int64_t n, int npass,
                              void *temp, void *stream) {
     using namespace ssg;
-    cudaError_t e = key_bytes == 2
-        ? radix::sort_pairs<uint16_t>((uint16_t *)keys, vals, iota != 0, n, npass, temp, (cudaStream_t)stream)
-        : radix::sort_pairs<uint64_t>((uint64_t *)keys, vals, iota != 0, n, npass, temp, (cudaStream_t)stream);
+    if (key_bytes != 8 || !iota || npass != 8) return SSG_ERR_INVALID_ARGUMENT;
+    cudaError_t e = dsort::sort_and_scan((const uint64_t *)keys, vals, nullptr, nullptr, nullptr, n, temp,
+                                         (cudaStream_t)stream);
     if (e != cudaSuccess) { set_error("test sort", e); return SSG_ERR_CUDA; }
     return SSG_OK;
 }

@@ -1,5 +1,5 @@
-"""The hand-written onesweep radix sort (binning K3) against numpy's stable
-argsort, through the ssg_test_sort hook of the C ABI."""
+"""The cooperative depth radix sort (binning steps 1-2) against numpy's
+stable argsort, through the ssg_test_sort hook of the C ABI."""
 
 import ctypes
 
@@ -26,27 +26,7 @@ def _sort(keys: np.ndarray, npass: int, iota: bool, vals=None):
     return dk.cpu().numpy().view(keys.dtype), dv.cpu().numpy().view(np.uint32)
 
 
-@pytest.mark.parametrize("n", [1, 50, 4095, 4096, 4097, 100_003, 2_000_000])
-def test_u16_tile_keys_stable(n):
-    rng = np.random.default_rng(n)
-    keys = rng.integers(0, 8160, n).astype(np.uint16)
-    k, v = _sort(keys, 2, iota=False)
-    order = np.argsort(keys, kind="stable")
-    np.testing.assert_array_equal(k, keys[order])
-    np.testing.assert_array_equal(v, order.astype(np.uint32))
-
-
-def test_u16_single_pass_and_constant_high_digit():
-    rng = np.random.default_rng(3)
-    keys = rng.integers(0, 200, 30000).astype(np.uint16)
-    for npass in (1, 2):
-        k, v = _sort(keys, npass, iota=False)
-        order = np.argsort(keys, kind="stable")
-        np.testing.assert_array_equal(v, order.astype(np.uint32))
-        np.testing.assert_array_equal(k, keys[order])
-
-
-@pytest.mark.parametrize("n", [7, 5000, 1_000_000])
+@pytest.mark.parametrize("n", [1, 7, 5000, 8191, 8192, 8193, 1_000_000, 3_000_000])
 def test_u64_depth_keys_with_ties_and_invalid(n):
     rng = np.random.default_rng(n + 1)
     depth = rng.choice(np.linspace(2.0, 12.0, max(n // 4, 2)), n)       # many exact ties
@@ -60,3 +40,35 @@ def test_u64_depth_keys_with_ties_and_invalid(n):
     got = v[valid[v]]
     want = np.nonzero(valid)[0][np.argsort(keys[valid], kind="stable")]
     np.testing.assert_array_equal(got, want.astype(np.uint32))
+
+
+def test_u64_all_equal_and_all_invalid():
+    for keys in (np.full(20000, np.float64(5.0)).view(np.uint64).copy(),
+                 np.full(777, 0xFFFFFFFFFFFFFFFF, dtype=np.uint64)):
+        k, v = _sort(keys, 8, iota=True)
+        np.testing.assert_array_equal(v, np.arange(keys.size, dtype=np.uint32))  # stable: identity
+
+
+def test_u64_full_width_keys():
+    rng = np.random.default_rng(5)
+    keys = rng.integers(0, 2**63, 300_000, dtype=np.int64).view(np.uint64)
+    keys[::7] = keys[3]  # ties across tiles
+    k, v = _sort(keys, 8, iota=True)
+    np.testing.assert_array_equal(v, np.argsort(keys, kind="stable").astype(np.uint32))
+
+
+def test_u64_fixup_short_runs_and_long_run_fallback():
+    rng = np.random.default_rng(9)
+    base = np.uint64(0xC010000000000000)
+    # wide range (nbits ~ 46: the 32-bit window leaves 14 low bits to the
+    # fix-up) with many keys sharing their window bits -> short fix-up runs
+    hi = rng.integers(0, 2**14, 200_000).astype(np.uint64) << np.uint64(32)
+    lo = rng.integers(0, 2**14, 200_000).astype(np.uint64)
+    keys = base + hi + lo
+    k, v = _sort(keys, 8, iota=True)
+    np.testing.assert_array_equal(v, np.argsort(keys, kind="stable").astype(np.uint32))
+    # one run of 5000 keys equal in the window but not below it -> exact fallback
+    keys2 = base + rng.integers(0, 2**9, 5000).astype(np.uint64)
+    keys2[0] = base + np.uint64(2**40)
+    k, v = _sort(keys2, 8, iota=True)
+    np.testing.assert_array_equal(v, np.argsort(keys2, kind="stable").astype(np.uint32))
