@@ -38,15 +38,14 @@ import numpy as np  # noqa: E402
 
 METRIC = "fwd+bwd raster ms/frame, 1M skew Gaussians @1080p; views/s at 1/2/4/8 GPU"
 # libssg_b200 kernel launches per fwd+bwd frame (all hand-written, no library
-# kernels): preprocess_fwd 1; depth radix sort = hist + schedule + 8 x
-# (upsweep, rowscan, downsweep) + settle = 27 (passes whose digit is constant
-# exit at entry); scan_counts 1; duplicate 1; tile radix sort = hist +
-# schedule + 2 x 3 + settle = 9; tile_bounds + fill_empty 2; blend_fwd 1;
-# blend_bwd 1; preprocess_bwd + sh_backward 2.
-LAUNCHES_PER_FRAME = 45
-LAUNCHES_NOTE = ("per frame: preprocess_fwd 1, depth radix sort 27, scan_counts 1, duplicate 1, tile radix "
-                 "sort 9, tile_bounds+fill_empty 2, blend_fwd 1, blend_bwd 1, preprocess_bwd+sh_backward 2; "
-                 "no library kernels (cudaMemsetAsync excluded)")
+# kernels): preprocess_fwd 1; depth sort + count scan 1 (cooperative);
+# two-level counting scatter 8 (rows: count, rowscan, rowstart, scatter;
+# tiles: count, tilescan, tilestart, scatter); blend_fwd 1; blend_bwd 1;
+# preprocess_bwd + sh_backward 2.
+LAUNCHES_PER_FRAME = 14
+LAUNCHES_NOTE = ("per frame: k_preprocess_forward 1, k_depth_sort 1, k_cs1_{count,rowscan,rowstart,scatter} 4, "
+                 "k_cs2_{count,tilescan,tilestart,scatter} 4, k_blend_forward 1, k_blend_backward 1, "
+                 "k_preprocess_backward + k_sh_backward 2; no library kernels (cudaMemsetAsync excluded)")
 UNIT = "views/s"
 N_PRIM, WIDTH, HEIGHT = 1_000_000, 1920, 1080
 # per-pair algorithmic instruction counts (fixed, not tuned)
@@ -348,6 +347,10 @@ def main():
                 "algorithmic": f"{FP32_PER_PAIR[dom]} FP32 instr/pair x {pairs} tile-synchronous "
                                f"pixel-instance pairs per launch (SURVEY.md §8(d))",
                 "mufu_frac": MUFU_PER_PAIR[dom] * pairs / t_dom / r_mufu,
+                "frac_note": "frac > 1 is possible: the SURVEY model charges every tile-synchronous pair, "
+                             "while the kernels cull pairs per 8x4-pixel warp block by an exact ellipse test "
+                             "and the backward visits only (warp, instance) pairs the forward blended; "
+                             "profiles/ has the measured issue-slot utilisation",
                 "peak_basis": f"{n_sm} SMs x 128 FP32 lanes x sm_max {f_max/1e6:.0f} MHz (nominal; "
                               "no dense contraction on this path, tensor cores unused)"}
     hbm = float(peaks["hbm_gbs"])

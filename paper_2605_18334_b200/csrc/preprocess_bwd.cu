@@ -37,8 +37,38 @@ __device__ __forceinline__ void sh_dot_grad(int deg, double x, double y, double 
             C34 * (8.0 * xz) * w[13] + C35 * (xx - yy) * w[14];
 }
 
+// fp32 twin of sh_dot_grad (the SH chain runs in fp32, like the forward colour)
+__device__ __forceinline__ void sh_dot_grad_f(int deg, float x, float y, float z, const float *w,
+                                              float *g) {
+    const float C1 = 0.4886025119029199f;
+    g[0] = -C1 * w[3];
+    g[1] = -C1 * w[1];
+    g[2] = C1 * w[2];
+    if (deg < 2) return;
+    const float C20 = 1.0925484305920792f, C21 = -1.0925484305920792f, C22 = 0.31539156525252005f,
+                 C23 = -1.0925484305920792f, C24 = 0.5462742152960396f;
+    g[0] += C20 * y * w[4] + C22 * (-2.0f * x) * w[6] + C23 * z * w[7] + C24 * (2.0f * x) * w[8];
+    g[1] += C20 * x * w[4] + C21 * z * w[5] + C22 * (-2.0f * y) * w[6] + C24 * (-2.0f * y) * w[8];
+    g[2] += C21 * y * w[5] + C22 * (4.0f * z) * w[6] + C23 * x * w[7];
+    if (deg < 3) return;
+    const float C30 = -0.5900435899266435f, C31 = 2.890611442640554f, C32 = -0.4570457994644658f,
+                 C33 = 0.3731763325901154f, C34 = -0.4570457994644658f, C35 = 1.445305721320277f,
+                 C36 = -0.5900435899266435f;
+    const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    g[0] += C30 * 6.0f * xy * w[9] + C31 * yz * w[10] + C32 * (-2.0f * xy) * w[11] + C33 * (-6.0f * xz) * w[12] +
+            C34 * (4.0f * zz - 3.0f * xx - yy) * w[13] + C35 * (2.0f * xz) * w[14] + C36 * (3.0f * xx - 3.0f * yy) * w[15];
+    g[1] += C30 * (3.0f * xx - 3.0f * yy) * w[9] + C31 * xz * w[10] + C32 * (4.0f * zz - xx - 3.0f * yy) * w[11] +
+            C33 * (-6.0f * yz) * w[12] + C34 * (-2.0f * xy) * w[13] + C35 * (-2.0f * yz) * w[14] + C36 * (-6.0f * xy) * w[15];
+    g[2] += C31 * xy * w[10] + C32 * (8.0f * yz) * w[11] + C33 * (6.0f * zz - 3.0f * xx - 3.0f * yy) * w[12] +
+            C34 * (8.0f * xz) * w[13] + C35 * (xx - yy) * w[14];
+}
+
+#ifndef SSG_PB_MINB
+#define SSG_PB_MINB 4
+#endif
+
 // Geometry part: everything but the SH chain (run first; writes d_mu).
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, SSG_PB_MINB)
 k_preprocess_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= sc.n) return;
@@ -266,39 +296,41 @@ k_sh_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
     if (lane < nw) {
         const float *sh = t + lane * ROW;
         const float *sg = gr.screen + 12 * i;
-        const double dcol[3] = {sg[9], sg[10], sg[11]};
+        const float dcol[3] = {sg[9], sg[10], sg[11]};
+        // the forward's fp32 colour (preprocess_fwd.cu), recomputed bit for bit
+        // so the clamp mask of projection.py:221-223 / :356 is the forward's
         const double dv0 = sc.mu[3 * i] - cam.campos[0], dv1 = sc.mu[3 * i + 1] - cam.campos[1],
                      dv2 = sc.mu[3 * i + 2] - cam.campos[2];
         const double dn = sqrt(dv0 * dv0 + dv1 * dv1 + dv2 * dv2);
         const double dns = dn > 1e-12 ? dn : 1.0;
-        const double x = dv0 / dns, y = dv1 / dns, z = dv2 / dns;
-        double basis[16];
-        sh_basis(DEG, x, y, z, basis);
-        double col[3] = {0.0, 0.0, 0.0};
+        const float x = (float)(dv0 / dns), y = (float)(dv1 / dns), z = (float)(dv2 / dns);
+        float basis[16];
+        sh_basis_f(DEG, x, y, z, basis);
+        float col[3] = {0.0f, 0.0f, 0.0f};
 #pragma unroll
         for (int k = 0; k < K; k++)
 #pragma unroll
-            for (int c = 0; c < 3; c++) col[c] += basis[k] * (double)sh[3 * k + c];
-        double dcc[3];
+            for (int c = 0; c < 3; c++) col[c] = fmaf(basis[k], sh[3 * k + c], col[c]);
+        float dcc[3];
 #pragma unroll
-        for (int c = 0; c < 3; c++) dcc[c] = (col[c] + 0.5 > 0.0) ? dcol[c] : 0.0;
-        double w[16];
+        for (int c = 0; c < 3; c++) dcc[c] = (col[c] + 0.5f > 0.0f) ? dcol[c] : 0.0f;
+        float w[16];
 #pragma unroll
-        for (int k = 0; k < K; k++)
-            w[k] = (double)sh[3 * k] * dcc[0] + (double)sh[3 * k + 1] * dcc[1] + (double)sh[3 * k + 2] * dcc[2];
-        double dd[3] = {0.0, 0.0, 0.0};
-        if (DEG > 0) sh_dot_grad(DEG, x, y, z, w, dd);
+        for (int k = 0; k < K; k++) w[k] = sh[3 * k] * dcc[0] + sh[3 * k + 1] * dcc[1] + sh[3 * k + 2] * dcc[2];
+        float dd[3] = {0.0f, 0.0f, 0.0f};
+        if (DEG > 0) sh_dot_grad_f(DEG, x, y, z, w, dd);
         __syncwarp(__activemask());
         float *out = t + lane * ROW;  // this lane's own row: safe to overwrite now
 #pragma unroll
         for (int k = 0; k < K; k++)
 #pragma unroll
-            for (int c = 0; c < 3; c++) out[3 * k + c] = (float)(basis[k] * dcc[c]);
+            for (int c = 0; c < 3; c++) out[3 * k + c] = basis[k] * dcc[c];
         if (DEG > 0) {
-            const double inner = x * dd[0] + y * dd[1] + z * dd[2];
-            gr.d_mu[3 * i] += (float)((dd[0] - x * inner) / dns);
-            gr.d_mu[3 * i + 1] += (float)((dd[1] - y * inner) / dns);
-            gr.d_mu[3 * i + 2] += (float)((dd[2] - z * inner) / dns);
+            const float inner = x * dd[0] + y * dd[1] + z * dd[2];
+            const float rdn = (float)(1.0 / dns);
+            gr.d_mu[3 * i] += (dd[0] - x * inner) * rdn;
+            gr.d_mu[3 * i + 1] += (dd[1] - y * inner) * rdn;
+            gr.d_mu[3 * i + 2] += (dd[2] - z * inner) * rdn;
         }
     }
     __syncwarp();

@@ -12,8 +12,12 @@
 
 namespace ssg {
 
+#ifndef SSG_PF_MINB
+#define SSG_PF_MINB 4
+#endif
+
 template <int DEG>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, SSG_PF_MINB)
 k_preprocess_forward(ssg_scene sc, ssg_camera cam, ssg_prim_buffers out, int ntx, int nty) {
     constexpr int K = (DEG + 1) * (DEG + 1);
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -36,19 +40,30 @@ k_preprocess_forward(ssg_scene sc, ssg_camera cam, ssg_prim_buffers out, int ntx
         project_geometry(cam, mu, ls, q4, logit, eta, P);
         fb = P.fallback;
 
-        // colour (projection.py:217-223): view direction, SH, +0.5, floor at 0
+        // colour (projection.py:217-223): view direction (fp64), SH in fp32
+        // (the colour only feeds the fp32 blend: ~1e-7 relative), +0.5,
+        // floor at 0.  The (K,3) row is 16-byte aligned: float4 loads.
         double dv0 = mu[0] - cam.campos[0], dv1 = mu[1] - cam.campos[1], dv2 = mu[2] - cam.campos[2];
         double dn = sqrt(dv0 * dv0 + dv1 * dv1 + dv2 * dv2);
         double dns = dn > 1e-12 ? dn : 1.0;
-        double basis[16];
-        sh_basis(DEG, dv0 / dns, dv1 / dns, dv2 / dns, basis);
-        const float *shp = sc.sh + (size_t)i * (3 * K);
-        double col[3] = {0.0, 0.0, 0.0};
+        float basis[16];
+        sh_basis_f(DEG, (float)(dv0 / dns), (float)(dv1 / dns), (float)(dv2 / dns), basis);
+        float col[3] = {0.0f, 0.0f, 0.0f};
+        if constexpr ((3 * K) % 4 == 0) {
+            const float4 *shp4 = reinterpret_cast<const float4 *>(sc.sh + (size_t)i * (3 * K));
 #pragma unroll
-        for (int k = 0; k < K; k++) {
-            col[0] += basis[k] * (double)shp[3 * k];
-            col[1] += basis[k] * (double)shp[3 * k + 1];
-            col[2] += basis[k] * (double)shp[3 * k + 2];
+            for (int q = 0; q < 3 * K / 4; q++) {
+                const float4 v = __ldg(shp4 + q);
+                const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int u = 0; u < 4; u++) col[(4 * q + u) % 3] = fmaf(basis[(4 * q + u) / 3], e[u], col[(4 * q + u) % 3]);
+            }
+        } else {
+            const float *shp = sc.sh + (size_t)i * (3 * K);
+#pragma unroll
+            for (int k = 0; k < K; k++)
+#pragma unroll
+                for (int c = 0; c < 3; c++) col[c] = fmaf(basis[k], __ldg(shp + 3 * k + c), col[c]);
         }
 
         ssg_splat s;
@@ -61,10 +76,9 @@ k_preprocess_forward(ssg_scene sc, ssg_camera cam, ssg_prim_buffers out, int ntx
         s.skew_y = (float)P.skew[1];
         s.o1 = (float)(P.sig[0] * P.comp);
         s.o2 = (float)(P.sig[1] * P.comp);
-        double c0 = col[0] + 0.5, c1 = col[1] + 0.5, c2 = col[2] + 0.5;
-        s.r = (float)(c0 > 0.0 ? c0 : 0.0);
-        s.g = (float)(c1 > 0.0 ? c1 : 0.0);
-        s.b = (float)(c2 > 0.0 ? c2 : 0.0);
+        s.r = fmaxf(col[0] + 0.5f, 0.0f);
+        s.g = fmaxf(col[1] + 0.5f, 0.0f);
+        s.b = fmaxf(col[2] + 0.5f, 0.0f);
         s.pad0 = 0;
         s.pad1 = 0;
         // 64-byte record as four 16-byte stores

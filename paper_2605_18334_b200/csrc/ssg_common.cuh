@@ -51,6 +51,30 @@ __device__ __forceinline__ void sh_basis(int deg, double x, double y, double z, 
     out[15] = -0.5900435899266435 * x * (xx - 3.0 * yy);
 }
 
+// fp32 twin of sh_basis for the colour of the forward splat record
+__device__ __forceinline__ void sh_basis_f(int deg, float x, float y, float z, float *out) {
+    out[0] = 0.28209479177387814f;
+    if (deg < 1) return;
+    out[1] = -0.4886025119029199f * y;
+    out[2] = 0.4886025119029199f * z;
+    out[3] = -0.4886025119029199f * x;
+    if (deg < 2) return;
+    const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    out[4] = 1.0925484305920792f * xy;
+    out[5] = -1.0925484305920792f * yz;
+    out[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+    out[7] = -1.0925484305920792f * xz;
+    out[8] = 0.5462742152960396f * (xx - yy);
+    if (deg < 3) return;
+    out[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
+    out[10] = 2.890611442640554f * xy * z;
+    out[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
+    out[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+    out[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
+    out[14] = 1.445305721320277f * z * (xx - yy);
+    out[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
+}
+
 // ------------------------------------------------------ projection (fp64)
 // Everything project_scene computes for one primitive that the forward and
 // backward kernels need (projection.py:41-79 minus what can be rebuilt).
