@@ -142,6 +142,8 @@ typedef struct ssg_grad_buffers {
     float *d_eta;               /* (n,3) */
     float *g_uv;                /* (n) */
     float *g_z;                 /* (n) */
+    float *d_beta;              /* optional (n,3): d_eta plus the beta regularizer
+                                   (ssg_regularize); NULL = d_eta (ssg_adam_step only) */
 } ssg_grad_buffers;
 
 /* Mutable parameters for the optimizer (same layout as ssg_scene). */
@@ -152,13 +154,14 @@ typedef struct ssg_params {
     float *sh, *opacity_logits, *beta, *dir;
 } ssg_params;
 
-/* Adam moments (fp32, one array pair per field; beta and dir share the eta
- * pair because their gradients are identical) and per-step scratch. */
+/* Adam moments (fp32, one array pair per scene field, adam.py:60-61) and
+ * per-step scratch. */
 typedef struct ssg_adam_state {
     float *m_mu, *v_mu, *m_log_scale, *v_log_scale, *m_rot, *v_rot;
-    float *m_sh, *v_sh, *m_logits, *v_logits, *m_eta, *v_eta;
+    float *m_sh, *v_sh, *m_logits, *v_logits, *m_beta, *v_beta, *m_dir, *v_dir;
     uint8_t *row_ok;            /* (n) scratch */
-    int32_t *n_skipped;         /* (1) primitives skipped this step (non-finite gradient) */
+    int32_t *n_skipped;         /* (1) skipped primitive-steps (non-finite gradient), accumulated
+                                   across steps like adam.py:79; the caller zeroes it once */
 } ssg_adam_state;
 
 typedef struct ssg_adam_hparams {
@@ -209,7 +212,26 @@ int ssg_blend_backward_slots(int64_t m, int32_t width, int32_t height, const flo
                              const ssg_frame_buffers *frame, const float *dL_dpixels, float *slots,
                              void *stream);
 
-/* ---- training step (config 5) -------------------------------------------- */
+/* ---- training step (config 5) ------------------------ */
+/* floats of scratch ssg_image_loss needs for a width x height image */
+int64_t ssg_loss_scratch_floats(int32_t width, int32_t height);
+/* optimize/losses.py:103-113 image_loss: (1-l) L1 + l (1 - SSIM) of rendered
+ * vs target ((H,W,3) f32) and its pixel gradient dL_dpixels (H,W,3);
+ * sums[0] = sum |x - y|, sums[1] = sum of SSIM over the valid windows x 3
+ * channels (value = (1-l) sums[0]/(3HW) + l (1 - sums[1]/(3 (H-10)(W-10)))).
+ * l == 0: L1 only (scratch may be NULL); l > 0 needs W, H >= 11 */
+int ssg_image_loss(const float *rendered, const float *target, int32_t width, int32_t height,
+                   float lambda_ssim, float *scratch, float *dL_dpixels, double *sums, void *stream);
+/* optimize/losses.py:116-136 scene_regularizers folded into the gradients:
+ * d_beta = d_eta + 2 lambda_beta beta, d_logits += the opacity-gap term,
+ * sums[2] = the penalty value */
+int ssg_regularize(int64_t n, const float *beta, const float *opacity_logits, const float *d_eta,
+                   float lambda_beta, float lambda_opacity, float *d_beta, float *d_logits, double *sums,
+                   void *stream);
+/* trainer.py:49-53 _IntervalStats.add: uv_sum += g_uv, z_max = max(z_max, g_z),
+ * mu_sum += d_mu */
+int ssg_interval_stats_add(int64_t n, const float *g_uv, const float *g_z, const float *d_mu,
+                           double *uv_sum, float *z_max, double *mu_sum, void *stream);
 /* optimize/adam.py:71-97 Adam.step on the device (skip non-finite rows,
  * bias-corrected moments, per-field learning rates, quaternion renorm) */
 int ssg_adam_step(const ssg_params *params, const ssg_grad_buffers *grads,

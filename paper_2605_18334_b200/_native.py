@@ -23,7 +23,8 @@ EXPORTS = ("ssg_abi_version", "ssg_last_error", "ssg_grid_dims", "ssg_bin_temp_b
            "ssg_preprocess_forward", "ssg_bin_rects", "ssg_bin_prepare", "ssg_bin_finish", "ssg_blend_forward",
            "ssg_blend_backward", "ssg_preprocess_backward", "ssg_blend_backward_slots",
            "ssg_test_sort_temp_bytes",
-           "ssg_test_sort", "ssg_test_blend_forward_vanilla", "ssg_adam_step", "ssg_blend_mask_words")
+           "ssg_test_sort", "ssg_test_blend_forward_vanilla", "ssg_adam_step", "ssg_blend_mask_words",
+           "ssg_loss_scratch_floats", "ssg_image_loss", "ssg_regularize", "ssg_interval_stats_add")
 
 _vp = ctypes.c_void_p
 
@@ -62,7 +63,7 @@ class SsgFrameBuffers(ctypes.Structure):
 class SsgGradBuffers(ctypes.Structure):
     _fields_ = [("screen", _vp), ("d_mu", _vp), ("d_log_scale", _vp), ("d_rot", _vp),
                 ("d_sh", _vp), ("d_opacity_logits", _vp), ("d_eta", _vp), ("g_uv", _vp),
-                ("g_z", _vp)]
+                ("g_z", _vp), ("d_beta", _vp)]
 
 
 class SsgParams(ctypes.Structure):
@@ -73,7 +74,8 @@ class SsgParams(ctypes.Structure):
 
 class SsgAdamState(ctypes.Structure):
     _fields_ = [(f, _vp) for f in ("m_mu", "v_mu", "m_log_scale", "v_log_scale", "m_rot", "v_rot", "m_sh",
-                                   "v_sh", "m_logits", "v_logits", "m_eta", "v_eta", "row_ok", "n_skipped")]
+                                   "v_sh", "m_logits", "v_logits", "m_beta", "v_beta", "m_dir", "v_dir",
+                                   "row_ok", "n_skipped")]
 
 
 class SsgAdamHparams(ctypes.Structure):
@@ -129,6 +131,11 @@ def lib():
     L.ssg_test_sort_temp_bytes.restype = ctypes.c_size_t
     L.ssg_test_sort_temp_bytes.argtypes = [ctypes.c_int64, ctypes.c_int]
     L.ssg_test_sort.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int, _vp, _vp]
+    L.ssg_loss_scratch_floats.restype = ctypes.c_int64
+    L.ssg_loss_scratch_floats.argtypes = [ctypes.c_int32, ctypes.c_int32]
+    L.ssg_image_loss.argtypes = [_vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_float, _vp, _vp, _vp, _vp]
+    L.ssg_regularize.argtypes = [ctypes.c_int64, _vp, _vp, _vp, ctypes.c_float, ctypes.c_float, _vp, _vp, _vp, _vp]
+    L.ssg_interval_stats_add.argtypes = [ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
     L.ssg_blend_mask_words.restype = ctypes.c_int64
     L.ssg_blend_mask_words.argtypes = [ctypes.c_int64, ctypes.c_int32]
     if L.ssg_abi_version() != ABI_VERSION:

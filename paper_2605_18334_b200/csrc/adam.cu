@@ -6,8 +6,9 @@
 // rates (config.py:19-25, lr_beta shared by beta and dir); quaternions
 // renormalised afterwards where they drifted (|norm - 1| > 1e-12), set to
 // the identity where degenerate (norm <= 1e-12).
-// d_beta == d_dir (projection.py:365-366) and both moments start at zero,
-// so the beta and dir moments are identical: one (m, v) pair drives both.
+// beta and dir keep separate moments: their rendered gradients are equal
+// (projection.py:365-366) but the training step adds the beta regularizer to
+// d_beta only (fit2d.py:75, losses.py:127).
 // Three passes, all HBM-bound and coalesced: a row check over the packed
 // gradient buffer, one element-wise update per field, the quaternion fix-up.
 #include "ssg_common.cuh"
@@ -22,7 +23,8 @@ __global__ void k_adam_rowcheck(int64_t n, int K, ssg_grad_buffers g, uint8_t *r
     if (i < n) {
 #pragma unroll
         for (int j = 0; j < 3; j++) ok &= isfinite(g.d_mu[3 * i + j]) && isfinite(g.d_log_scale[3 * i + j]) &&
-                                          isfinite(g.d_eta[3 * i + j]);
+                                          isfinite(g.d_eta[3 * i + j]) &&
+                                          (!g.d_beta || isfinite(g.d_beta[3 * i + j]));
 #pragma unroll
         for (int j = 0; j < 4; j++) ok &= isfinite(g.d_rot[4 * i + j]);
         ok &= isfinite(g.d_opacity_logits[2 * i]) && isfinite(g.d_opacity_logits[2 * i + 1]);
@@ -34,10 +36,9 @@ __global__ void k_adam_rowcheck(int64_t n, int K, ssg_grad_buffers g, uint8_t *r
 }
 
 // param[e] -= lr * (m/c1) / (sqrt(v/c2) + eps) for every element e of a
-// (n, width) field whose row is finite; P2 is an optional second parameter
-// array that receives the same update (dir next to beta).
+// (n, width) field whose row is finite.
 template <typename P>
-__global__ void k_adam_field(int64_t n, int width, P *__restrict__ p, P *__restrict__ p2,
+__global__ void k_adam_field(int64_t n, int width, P *__restrict__ p,
                              const float *__restrict__ g, float *__restrict__ m, float *__restrict__ v,
                              const uint8_t *__restrict__ row_ok, double lr, double c1, double c2) {
     const int64_t total = n * width;
@@ -51,7 +52,6 @@ __global__ void k_adam_field(int64_t n, int width, P *__restrict__ p, P *__restr
         v[e] = (float)vv;
         const double upd = lr * (mm / c1) / (sqrt(vv / c2) + kEps);
         p[e] = (P)((double)p[e] - upd);
-        if (p2) p2[e] = (P)((double)p2[e] - upd);
     }
 }
 
@@ -80,23 +80,25 @@ extern "C" int ssg_adam_step(const ssg_params *p, const ssg_grad_buffers *g, con
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = p->n;
     const int K = p->sh_coeffs;
-    cudaError_t e = cudaMemsetAsync(s->n_skipped, 0, sizeof(int32_t), st);
-    if (e != cudaSuccess) { set_error("memset skipped", e); return SSG_ERR_CUDA; }
     k_adam_rowcheck<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, K, *g, s->row_ok, s->n_skipped);
     const double c1 = 1.0 - pow(kBeta1, (double)hp->t), c2 = 1.0 - pow(kBeta2, (double)hp->t);
     const unsigned grid = 148 * 8;
-    k_adam_field<double><<<grid, 256, 0, st>>>(n, 3, p->mu, nullptr, g->d_mu, s->m_mu, s->v_mu, s->row_ok,
-                                               hp->lr_mu, c1, c2);
-    k_adam_field<double><<<grid, 256, 0, st>>>(n, 3, p->log_scale, nullptr, g->d_log_scale, s->m_log_scale,
-                                               s->v_log_scale, s->row_ok, hp->lr_scale, c1, c2);
-    k_adam_field<double><<<grid, 256, 0, st>>>(n, 4, p->rot, nullptr, g->d_rot, s->m_rot, s->v_rot, s->row_ok,
-                                               hp->lr_rot, c1, c2);
-    k_adam_field<float><<<grid, 256, 0, st>>>(n, 3 * K, p->sh, nullptr, g->d_sh, s->m_sh, s->v_sh, s->row_ok,
-                                              hp->lr_sh, c1, c2);
-    k_adam_field<float><<<grid, 256, 0, st>>>(n, 2, p->opacity_logits, nullptr, g->d_opacity_logits, s->m_logits,
+    k_adam_field<double><<<grid, 256, 0, st>>>(n, 3, p->mu, g->d_mu, s->m_mu, s->v_mu, s->row_ok, hp->lr_mu, c1,
+                                               c2);
+    k_adam_field<double><<<grid, 256, 0, st>>>(n, 3, p->log_scale, g->d_log_scale, s->m_log_scale, s->v_log_scale,
+                                               s->row_ok, hp->lr_scale, c1, c2);
+    k_adam_field<double><<<grid, 256, 0, st>>>(n, 4, p->rot, g->d_rot, s->m_rot, s->v_rot, s->row_ok, hp->lr_rot,
+                                               c1, c2);
+    k_adam_field<float><<<grid, 256, 0, st>>>(n, 3 * K, p->sh, g->d_sh, s->m_sh, s->v_sh, s->row_ok, hp->lr_sh, c1,
+                                              c2);
+    k_adam_field<float><<<grid, 256, 0, st>>>(n, 2, p->opacity_logits, g->d_opacity_logits, s->m_logits,
                                               s->v_logits, s->row_ok, hp->lr_opacity, c1, c2);
-    k_adam_field<float><<<grid, 256, 0, st>>>(n, 3, p->beta, p->dir, g->d_eta, s->m_eta, s->v_eta, s->row_ok,
-                                              hp->lr_beta, c1, c2);
+    if (hp->lr_beta != 0.0) {  // adam.py:63-69: lr_beta drives beta and dir
+        k_adam_field<float><<<grid, 256, 0, st>>>(n, 3, p->beta, g->d_beta ? g->d_beta : g->d_eta, s->m_beta,
+                                                  s->v_beta, s->row_ok, hp->lr_beta, c1, c2);
+        k_adam_field<float><<<grid, 256, 0, st>>>(n, 3, p->dir, g->d_eta, s->m_dir, s->v_dir, s->row_ok,
+                                                  hp->lr_beta, c1, c2);
+    }
     k_quat_renorm<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, p->rot);
     return check_launch("ssg_adam_step");
 }

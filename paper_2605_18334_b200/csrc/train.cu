@@ -1,0 +1,298 @@
+// train.cu -- the training-step glue around the rasterizer, on the device
+// (SURVEY.md §8(f) row 1): the photometric loss with its analytic pixel
+// gradient, the scene regularizers, and the densification interval
+// statistics.
+//
+// Reference:
+//   optimize/losses.py:38-41    l1_loss: mean |x - y|, grad sign(x - y) / size
+//   optimize/losses.py:44-100   ssim: mean SSIM over 'valid' 11x11 Gaussian
+//                               windows (sigma 1.5, C1 = 0.01^2, C2 = 0.03^2),
+//                               channels averaged, and its adjoint through
+//                               'full' convolutions
+//   optimize/losses.py:103-113  image_loss: (1 - l) L1 + l (1 - SSIM)
+//   optimize/losses.py:116-136  scene_regularizers: lambda_beta * sum |beta|^2,
+//                               lambda_opacity * sum |sig(l1) - sig(l2)|
+//   trainer.py:40-58            _IntervalStats: sum g_uv, max g_z, sum d_mu
+//
+// The 11x11 window is the outer product of one normalised 1-D Gaussian, so
+// every windowed mean is two 11-tap passes over a shared-memory tile.  One
+// CTA produces a 16x16 block of outputs for all three channels; the loss
+// values are accumulated in fp64 with one atomic per CTA.
+#include "ssg_common.cuh"
+
+namespace ssg {
+
+constexpr int kWin = 11, kHalo = kWin - 1, kLT = 16, kLR = kLT + kHalo;  // tile, tile + halo
+constexpr float kC1 = 0.01f * 0.01f, kC2 = 0.03f * 0.03f;
+
+__constant__ float c_gauss[kWin];
+
+__device__ __forceinline__ double block_sum(double v, double *s_red) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) s_red[w] = v;
+    __syncthreads();
+    double tot = 0.0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); i++) tot += s_red[i];
+    __syncthreads();
+    return tot;
+}
+
+// Pass 1: per valid window (output (i, j) covers input rows i..i+10, columns
+// j..j+10) and channel: SSIM s and the three adjoint maps of losses.py:86-93
+// (g_mu_x, g_wxx, g_wxy), plus the L1 and SSIM sums.  gm layout: (Hv, Wv, 9).
+__global__ void __launch_bounds__(kLT * kLT) k_loss_stats(const float *__restrict__ img, const float *__restrict__ tgt,
+                                                          int H, int W, int with_ssim, float inv_n,
+                                                          float *__restrict__ gm, double *__restrict__ sums) {
+    __shared__ float sx[3][kLR][kLR], sy[3][kLR][kLR];
+    __shared__ float hs[5][3][kLR][kLT];
+    __shared__ double s_red[kLT * kLT / 32];
+    const int tx = threadIdx.x % kLT, ty = threadIdx.x / kLT;
+    const int i0 = blockIdx.y * kLT, j0 = blockIdx.x * kLT;
+    double l1 = 0.0, ss = 0.0;
+    // L1 over the tile's own 16x16 pixels (every pixel counted once)
+    {
+        const int i = i0 + ty, j = j0 + tx;
+        if (i < H && j < W)
+            for (int c = 0; c < 3; c++) {
+                const size_t p = ((size_t)i * W + j) * 3 + c;
+                l1 += fabsf(img[p] - tgt[p]);
+            }
+    }
+    if (with_ssim) {
+        for (int q = threadIdx.x; q < kLR * kLR; q += blockDim.x) {
+            const int r = q / kLR, cc = q % kLR;
+            const int i = i0 + r, j = j0 + cc;
+            const bool in = i < H && j < W;
+            for (int c = 0; c < 3; c++) {
+                const size_t p = ((size_t)i * W + j) * 3 + c;
+                sx[c][r][cc] = in ? img[p] : 0.0f;
+                sy[c][r][cc] = in ? tgt[p] : 0.0f;
+            }
+        }
+        __syncthreads();
+        // horizontal pass: rows 0..kLR-1 of the region, output columns 0..kLT-1
+        for (int q = threadIdx.x; q < kLR * kLT; q += blockDim.x) {
+            const int r = q / kLT, cc = q % kLT;
+            for (int c = 0; c < 3; c++) {
+                float a = 0.f, b = 0.f, xx = 0.f, yy = 0.f, xy = 0.f;
+#pragma unroll
+                for (int u = 0; u < kWin; u++) {
+                    const float wgt = c_gauss[u], x = sx[c][r][cc + u], y = sy[c][r][cc + u];
+                    a = fmaf(wgt, x, a);
+                    b = fmaf(wgt, y, b);
+                    xx = fmaf(wgt, x * x, xx);
+                    yy = fmaf(wgt, y * y, yy);
+                    xy = fmaf(wgt, x * y, xy);
+                }
+                hs[0][c][r][cc] = a;
+                hs[1][c][r][cc] = b;
+                hs[2][c][r][cc] = xx;
+                hs[3][c][r][cc] = yy;
+                hs[4][c][r][cc] = xy;
+            }
+        }
+        __syncthreads();
+        const int Hv = H - kHalo, Wv = W - kHalo;
+        const int i = i0 + ty, j = j0 + tx;
+        if (i < Hv && j < Wv) {
+            for (int c = 0; c < 3; c++) {
+                float st[5];
+#pragma unroll
+                for (int k = 0; k < 5; k++) {
+                    float acc = 0.f;
+#pragma unroll
+                    for (int u = 0; u < kWin; u++) acc = fmaf(c_gauss[u], hs[k][c][ty + u][tx], acc);
+                    st[k] = acc;
+                }
+                const float mx = st[0], my = st[1];
+                const float vx = st[2] - mx * mx, vy = st[3] - my * my, cov = st[4] - mx * my;
+                const float a1 = 2.f * mx * my + kC1, a2 = 2.f * cov + kC2;
+                const float b1 = mx * mx + my * my + kC1, b2 = vx + vy + kC2;
+                const float s = (a1 * a2) / (b1 * b2);
+                ss += s;
+                // losses.py:86-93, divided by n = Hv * Wv * 3
+                const float g_a1 = a2 / (b1 * b2) * inv_n, g_a2 = a1 / (b1 * b2) * inv_n;
+                const float g_b1 = -s / b1 * inv_n, g_b2 = -s / b2 * inv_n;
+                const float g_mu = 2.f * my * g_a1 + 2.f * mx * g_b1 - 2.f * mx * g_b2 - my * 2.f * g_a2;
+                float *o = gm + ((size_t)i * Wv + j) * 9 + 3 * c;
+                o[0] = g_mu;
+                o[1] = g_b2;
+                o[2] = 2.f * g_a2;
+            }
+        }
+    }
+    const double t1 = block_sum(l1, s_red);
+    const double t2 = block_sum(ss, s_red);
+    if (threadIdx.x == 0) {
+        atomicAdd(&sums[0], t1);
+        if (with_ssim) atomicAdd(&sums[1], t2);
+    }
+}
+
+// Pass 2: dL/dpixel = (1 - l) sign(x - y) / size - l * dSSIM/dx, with
+// dSSIM/dx = full(g_mu) + 2 x full(g_wxx) + y full(g_wxy) (losses.py:94-96,
+// 112).  Full convolution: output (i, j) gathers windows i-10..i, j-10..j.
+__global__ void __launch_bounds__(kLT * kLT) k_loss_grad(const float *__restrict__ img, const float *__restrict__ tgt,
+                                                         const float *__restrict__ gm, int H, int W, int with_ssim,
+                                                         float w_l1, float w_ssim, float *__restrict__ dL) {
+    __shared__ float sg[9][kLR][kLR];
+    __shared__ float hs[9][kLR][kLT];
+    const int tx = threadIdx.x % kLT, ty = threadIdx.x / kLT;
+    const int i0 = blockIdx.y * kLT, j0 = blockIdx.x * kLT;
+    const int Hv = H - kHalo, Wv = W - kHalo;
+    if (with_ssim) {
+        // region rows i0-10 .. i0+15, columns j0-10 .. j0+15 of the gm maps
+        for (int q = threadIdx.x; q < kLR * kLR; q += blockDim.x) {
+            const int r = q / kLR, cc = q % kLR;
+            const int i = i0 - kHalo + r, j = j0 - kHalo + cc;
+            const bool in = i >= 0 && j >= 0 && i < Hv && j < Wv;
+            const float *src = gm + ((size_t)(in ? i : 0) * Wv + (in ? j : 0)) * 9;
+#pragma unroll
+            for (int k = 0; k < 9; k++) sg[k][r][cc] = in ? src[k] : 0.0f;
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < kLR * kLT; q += blockDim.x) {
+            const int r = q / kLT, cc = q % kLT;
+#pragma unroll
+            for (int k = 0; k < 9; k++) {
+                float acc = 0.f;
+#pragma unroll
+                for (int u = 0; u < kWin; u++) acc = fmaf(c_gauss[u], sg[k][r][cc + u], acc);
+                hs[k][r][cc] = acc;
+            }
+        }
+        __syncthreads();
+    }
+    const int i = i0 + ty, j = j0 + tx;
+    if (i >= H || j >= W) return;
+    for (int c = 0; c < 3; c++) {
+        const size_t p = ((size_t)i * W + j) * 3 + c;
+        const float x = img[p], y = tgt[p], d = x - y;
+        float g = w_l1 * (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f));
+        if (with_ssim) {
+            float f[3];
+#pragma unroll
+            for (int k = 0; k < 3; k++) {
+                float acc = 0.f;
+#pragma unroll
+                for (int u = 0; u < kWin; u++) acc = fmaf(c_gauss[u], hs[3 * c + k][ty + u][tx], acc);
+                f[k] = acc;
+            }
+            g -= w_ssim * (f[0] + 2.f * x * f[1] + y * f[2]);
+        }
+        dL[p] = g;
+    }
+}
+
+// losses.py:116-136 on the device: d_beta = d_eta + 2 lb beta (the rendered
+// part of d_beta equals d_eta, projection.py:365-366), d_logits += the
+// opacity-gap term; sums[2] += lb sum beta^2 + lo sum |gap|.
+__global__ void k_regularize(int64_t n, const float *__restrict__ beta, const float *__restrict__ logits,
+                             const float *__restrict__ d_eta, float lb, float lo, float *__restrict__ d_beta,
+                             float *__restrict__ d_logits, double *__restrict__ sums) {
+    __shared__ double s_red[8];
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double val = 0.0;
+    if (i < n) {
+        for (int j = 0; j < 3; j++) {
+            const float b = beta[3 * i + j];
+            d_beta[3 * i + j] = d_eta[3 * i + j] + (lb > 0.f ? 2.f * lb * b : 0.f);
+            if (lb > 0.f) val += (double)lb * (double)b * (double)b;
+        }
+        if (lo > 0.f) {
+            // kernel_math.py:158-165 branch-stable sigmoid, in fp64 like the reference
+            double sg[2];
+            for (int j = 0; j < 2; j++) {
+                const double l = logits[2 * i + j];
+                sg[j] = l >= 0 ? 1.0 / (1.0 + exp(-l)) : exp(l) / (1.0 + exp(l));
+            }
+            const double gap = sg[0] - sg[1];
+            val += (double)lo * fabs(gap);
+            const double sgn = gap > 0 ? 1.0 : (gap < 0 ? -1.0 : 0.0);
+            d_logits[2 * i] += (float)(lo * sgn * sg[0] * (1.0 - sg[0]));
+            d_logits[2 * i + 1] += (float)(-lo * sgn * sg[1] * (1.0 - sg[1]));
+        }
+    }
+    const double t = block_sum(val, s_red);
+    if (threadIdx.x == 0 && t != 0.0) atomicAdd(&sums[2], t);
+}
+
+// trainer.py:49-53: uv_sum += g_uv; z_max = max(z_max, g_z); mu_sum += d_mu
+__global__ void k_stats_add(int64_t n, const float *__restrict__ g_uv, const float *__restrict__ g_z,
+                            const float *__restrict__ d_mu, double *__restrict__ uv_sum, float *__restrict__ z_max,
+                            double *__restrict__ mu_sum) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uv_sum[i] += (double)g_uv[i];
+    z_max[i] = fmaxf(z_max[i], g_z[i]);
+    for (int j = 0; j < 3; j++) mu_sum[3 * i + j] += (double)d_mu[3 * i + j];
+}
+
+}  // namespace ssg
+
+extern "C" int64_t ssg_loss_scratch_floats(int32_t width, int32_t height) {
+    if (width < ssg::kWin || height < ssg::kWin) return 9;
+    return 9 * (int64_t)(width - ssg::kHalo) * (height - ssg::kHalo);
+}
+
+extern "C" int ssg_image_loss(const float *rendered, const float *target, int32_t width, int32_t height,
+                              float lambda_ssim, float *scratch, float *dL_dpixels, double *sums, void *stream) {
+    using namespace ssg;
+    if (!rendered || !target || !dL_dpixels || !sums || width < 1 || height < 1 || lambda_ssim < 0.f)
+        return SSG_ERR_INVALID_ARGUMENT;
+    const int with_ssim = lambda_ssim != 0.0f;
+    if (with_ssim && (width < kWin || height < kWin)) return SSG_ERR_INVALID_ARGUMENT;  // losses.py:58-59
+    if (with_ssim && !scratch) return SSG_ERR_INVALID_ARGUMENT;
+    static bool gauss_set = false;
+    if (!gauss_set) {  // losses.py:28-32, normalised in fp64
+        double g[kWin], sum = 0.0;
+        for (int u = 0; u < kWin; u++) {
+            const double x = u - (kWin - 1) / 2.0;
+            g[u] = exp(-x * x / (2.0 * 1.5 * 1.5));
+            sum += g[u];
+        }
+        float gf[kWin];
+        for (int u = 0; u < kWin; u++) gf[u] = (float)(g[u] / sum);
+        cudaError_t e = cudaMemcpyToSymbol(c_gauss, gf, sizeof(gf));
+        if (e != cudaSuccess) { set_error("gauss constant", e); return SSG_ERR_CUDA; }
+        gauss_set = true;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(sums, 0, 2 * sizeof(double), st);
+    if (e != cudaSuccess) { set_error("memset sums", e); return SSG_ERR_CUDA; }
+    const dim3 grid((width + kLT - 1) / kLT, (height + kLT - 1) / kLT);
+    const float inv_n = with_ssim ? 1.0f / (3.0f * (float)(width - kHalo) * (float)(height - kHalo)) : 0.0f;
+    k_loss_stats<<<grid, kLT * kLT, 0, st>>>(rendered, target, height, width, with_ssim, inv_n, scratch, sums);
+    const float w_l1 = (1.0f - lambda_ssim) / (3.0f * (float)width * (float)height);
+    k_loss_grad<<<grid, kLT * kLT, 0, st>>>(rendered, target, scratch, height, width, with_ssim, w_l1, lambda_ssim,
+                                            dL_dpixels);
+    return check_launch("ssg_image_loss");
+}
+
+extern "C" int ssg_regularize(int64_t n, const float *beta, const float *opacity_logits, const float *d_eta,
+                              float lambda_beta, float lambda_opacity, float *d_beta, float *d_logits,
+                              double *sums, void *stream) {
+    using namespace ssg;
+    if (n < 0 || (n > 0 && (!beta || !opacity_logits || !d_eta || !d_beta || !d_logits)) || !sums)
+        return SSG_ERR_INVALID_ARGUMENT;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(sums + 2, 0, sizeof(double), st);
+    if (e != cudaSuccess) { set_error("memset reg", e); return SSG_ERR_CUDA; }
+    if (n == 0) return SSG_OK;
+    k_regularize<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, beta, opacity_logits, d_eta, lambda_beta,
+                                                               lambda_opacity, d_beta, d_logits, sums);
+    return check_launch("ssg_regularize");
+}
+
+extern "C" int ssg_interval_stats_add(int64_t n, const float *g_uv, const float *g_z, const float *d_mu,
+                                      double *uv_sum, float *z_max, double *mu_sum, void *stream) {
+    using namespace ssg;
+    if (n < 0 || (n > 0 && (!g_uv || !g_z || !d_mu || !uv_sum || !z_max || !mu_sum))) return SSG_ERR_INVALID_ARGUMENT;
+    if (n == 0) return SSG_OK;
+    k_stats_add<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, g_uv, g_z, d_mu, uv_sum, z_max,
+                                                                               mu_sum);
+    return check_launch("ssg_interval_stats_add");
+}

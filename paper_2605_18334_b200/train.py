@@ -1,23 +1,33 @@
 """View-parallel training step (config 5) on top of the rasterizer.
 
-One process per GPU.  Every rank holds the full scene and optimizer state
-(replicated); per step each rank renders its own training view(s) forward +
-backward, the packed per-Gaussian gradient buffer is SUM all-reduced and
-g_z is MAX all-reduced over NCCL, and every rank applies
-the identical Adam step (optimize/adam.py:71-97, ssg_adam_step), so the
-replicas stay bit-identical.  The reference trains one view per step
-(trainer.py:127-129); with R ranks a step here consumes R views, so it is
-checked at gradient level: the reduced gradients equal the sum of per-view
-gradients.
+Mirrors the reference's training glue on the device:
+  TrainConfig            optimize/config.py:9-61 (fields, defaults, validate,
+                         position_lr_at)
+  image_loss             optimize/losses.py:103-113 ((1-l) L1 + l (1 - SSIM),
+                         analytic pixel gradient; ssg_image_loss)
+  regularizers           optimize/losses.py:116-136 (ssg_regularize)
+  DeviceAdam             optimize/adam.py:53-97 (ssg_adam_step: skip non-finite
+                         rows, bias-corrected moments, per-field rates, quaternion
+                         renormalisation; beta and dir keep separate moments)
+  IntervalStats          trainer.py:40-58 (ssg_interval_stats_add)
+  training_step          fit2d.py:62-78 (render, loss, stop on a non-finite loss,
+                         backward, stats before the regularizers, Adam)
 
-The photometric loss is L1 (the L1 part of losses.py:139-149; SSIM and the
-regularizers are outside the hot-path scope).
+One process per GPU.  Every rank holds the full scene and optimizer state
+(replicated); per step each rank renders its own training view forward +
+backward, the packed per-Gaussian gradient buffer is SUM all-reduced and g_z
+is MAX all-reduced over NCCL, and every rank applies the
+identical regularizers and Adam step, so the replicas stay bit-identical.
+The reference trains one view per step (trainer.py:127-129); with R ranks a
+step consumes R views, so it is checked at gradient level: the reduced
+gradients equal the sum of per-view gradients.
 """
 
 from __future__ import annotations
 
 import ctypes
 import dataclasses
+import math
 
 import torch
 import torch.distributed as dist
@@ -29,14 +39,54 @@ SUM_FIELDS = ("d_mu", "d_log_scale", "d_rot", "d_sh", "d_opacity_logits", "d_eta
 
 
 @dataclasses.dataclass
-class LearningRates:
-    """optimize/config.py:19-25 defaults; lr_beta drives beta and dir."""
-    mu: float = 1e-3
-    log_scale: float = 5e-3
-    rot: float = 2e-3
-    sh: float = 2.5e-3
-    opacity: float = 2.5e-2
-    beta: float = 1e-4
+class TrainConfig:
+    """optimize/config.py:9-38 (same fields and defaults)."""
+    lr_position: float = 1e-3
+    lr_position_final: float | None = None
+    lr_scale: float = 5e-3
+    lr_rot: float = 2e-3
+    lr_opacity: float = 2.5e-2
+    lr_sh: float = 2.5e-3
+    lr_beta: float = 1e-4
+    tau_uv: float = 1e-3
+    tau_z: float = math.nan
+    densify_interval: int = 100
+    densify_start: int = 500
+    densify_end: int = 15000
+    prune_alpha: float = 5e-3
+    split_scale_threshold: float = 0.05
+    max_screen_radius: float | None = None
+    lambda_ssim: float = 0.2
+    lambda_beta_reg: float = 1e-4
+    lambda_opacity_reg: float = 1e-3
+    iterations: int = 3000
+    seed: int = 0
+
+    def validate(self):
+        """config.py:40-55."""
+        for name in ("lr_position", "lr_scale", "lr_rot", "lr_opacity", "lr_sh"):
+            if getattr(self, name) <= 0:
+                raise ValueError(f"{name} must be > 0")
+        for name in ("lr_beta", "tau_uv", "prune_alpha", "split_scale_threshold",
+                     "lambda_ssim", "lambda_beta_reg", "lambda_opacity_reg"):
+            if getattr(self, name) < 0:
+                raise ValueError(f"{name} must be >= 0")
+        if not (math.isnan(self.tau_z) or self.tau_z >= 0):
+            raise ValueError("tau_z must be >= 0, nan (auto), or inf")
+        if self.iterations < 1:
+            raise ValueError("iterations must be >= 1")
+        return self
+
+    def position_lr_at(self, iteration: int) -> float:
+        """config.py:57-61: optional exponential decay of the position rate."""
+        if self.lr_position_final is None:
+            return self.lr_position
+        t = min(max(iteration / max(self.iterations, 1), 0.0), 1.0)
+        return self.lr_position * (self.lr_position_final / self.lr_position) ** t
+
+
+def _stream(dev) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
 
 
 def allreduce_gradients(grads: DeviceGrads, group=None) -> None:
@@ -47,30 +97,92 @@ def allreduce_gradients(grads: DeviceGrads, group=None) -> None:
     dist.all_reduce(grads.g_z, op=dist.ReduceOp.MAX, group=group)
 
 
-def l1_loss_grad(color: torch.Tensor, target: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
-    """mean |c - t| and its pixel gradient sign(c - t) / (3P)."""
-    diff = color - target
-    return diff.abs().mean(), torch.sign(diff) / diff.numel()
+class ImageLoss:
+    """Device image loss + pixel gradient (losses.py:103-113) for one image
+    size; the value is read lazily (value() synchronises)."""
+
+    def __init__(self, width: int, height: int, lambda_ssim: float, device):
+        if lambda_ssim < 0:
+            raise ValueError("lambda_ssim must be >= 0")
+        if lambda_ssim > 0 and (width < 11 or height < 11):
+            raise ValueError("images must be at least 11x11 for SSIM")  # losses.py:58-59
+        self.W, self.H, self.lam = width, height, float(lambda_ssim)
+        self.scratch = torch.empty(int(N.lib().ssg_loss_scratch_floats(width, height)), dtype=torch.float32,
+                                   device=device)
+        self.dL = torch.empty((height, width, 3), dtype=torch.float32, device=device)
+        self.sums = torch.zeros(3, dtype=torch.float64, device=device)  # l1 sum, ssim sum, reg value
+
+    def __call__(self, rendered: torch.Tensor, target: torch.Tensor) -> torch.Tensor:
+        for t in (rendered, target):
+            if tuple(t.shape) != (self.H, self.W, 3) or t.dtype != torch.float32 or not t.is_contiguous():
+                raise ValueError("image dimensions differ")
+        N.check(N.lib().ssg_image_loss(rendered.data_ptr(), target.data_ptr(), self.W, self.H, self.lam,
+                                       self.scratch.data_ptr(), self.dL.data_ptr(), self.sums.data_ptr(),
+                                       _stream(rendered.device)), "ssg_image_loss")
+        return self.dL
+
+    def value_tensor(self) -> torch.Tensor:
+        """(1-l) L1 + l (1 - SSIM) + regularizer value, on the device."""
+        l1 = self.sums[0] / (3.0 * self.W * self.H)
+        if self.lam == 0.0:
+            img = l1
+        else:
+            n = 3.0 * (self.W - 10) * (self.H - 10)
+            img = (1.0 - self.lam) * l1 + self.lam * (1.0 - self.sums[1] / n)
+        return img + self.sums[2]
+
+
+class IntervalStats:
+    """trainer.py:40-58 on the device (fp64 sums, fp32 max)."""
+
+    def __init__(self, n: int, device):
+        self.uv_sum = torch.zeros(n, dtype=torch.float64, device=device)
+        self.z_max = torch.zeros(n, dtype=torch.float32, device=device)
+        self.mu_sum = torch.zeros((n, 3), dtype=torch.float64, device=device)
+        self.steps = 0
+
+    def add(self, grads: DeviceGrads, views: int = 1):
+        n = self.uv_sum.numel()
+        N.check(N.lib().ssg_interval_stats_add(n, grads.g_uv.data_ptr(), grads.g_z.data_ptr(),
+                                               grads.d_mu.data_ptr(), self.uv_sum.data_ptr(),
+                                               self.z_max.data_ptr(), self.mu_sum.data_ptr(),
+                                               _stream(self.uv_sum.device)), "ssg_interval_stats_add")
+        self.steps += views
+
+    def bundle(self):
+        d = max(self.steps, 1)
+        return dataclasses.make_dataclass("Stats", ["g_uv", "g_z", "d_mu"])(
+            self.uv_sum / d, self.z_max, self.mu_sum / d)
 
 
 class DeviceAdam:
-    """Adam state on the device (fp32 moments) bound to a DeviceScene."""
+    """Adam state on the device (fp32 moments, one pair per scene field,
+    adam.py:60-61) bound to a DeviceScene."""
 
-    def __init__(self, ds: DeviceScene, lr: LearningRates | None = None):
+    FIELDS = ("mu", "log_scale", "rot", "sh", "logits", "beta", "dir")
+
+    def __init__(self, ds: DeviceScene, cfg: TrainConfig | None = None):
         self.ds = ds
-        self.lr = lr or LearningRates()
+        self.cfg = cfg or TrainConfig()
         self.t = 0
-        dev = ds.mu.device
-        z = lambda *shape: torch.zeros(shape, dtype=torch.float32, device=dev)  # noqa: E731
-        n, K = ds.n, ds.K
-        self.m = {"mu": z(n, 3), "log_scale": z(n, 3), "rot": z(n, 4), "sh": z(n, K, 3), "logits": z(n, 2),
-                  "eta": z(n, 3)}
-        self.v = {k: torch.zeros_like(v) for k, v in self.m.items()}
-        self.row_ok = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
-        self.n_skipped_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._alloc(ds.n)
 
-    def step(self, grads: DeviceGrads) -> None:
-        ds = self.ds
+    def _alloc(self, n: int):
+        dev = self.ds.mu.device
+        K = self.ds.K
+        shapes = {"mu": (n, 3), "log_scale": (n, 3), "rot": (n, 4), "sh": (n, K, 3), "logits": (n, 2),
+                  "beta": (n, 3), "dir": (n, 3)}
+        self.m = {k: torch.zeros(s, dtype=torch.float32, device=dev) for k, s in shapes.items()}
+        self.v = {k: torch.zeros_like(t) for k, t in self.m.items()}
+        self.row_ok = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+        self.n_skipped_dev = torch.zeros(1, dtype=torch.int32, device=dev)  # accumulated, adam.py:79
+
+    def step(self, grads, iteration: int = 0, d_beta: torch.Tensor | None = None) -> None:
+        """adam.py:71-97; `d_beta` (d_eta + regularizer) drives beta, d_eta
+        drives dir."""
+        ds, cfg = self.ds, self.cfg
+        if ds.n == 0:
+            return
         self.t += 1
         p = N.SsgParams()
         p.n, p.sh_degree, p.sh_coeffs = ds.n, ds.sh_degree, ds.K
@@ -81,30 +193,78 @@ class DeviceAdam:
         g.d_mu, g.d_log_scale, g.d_rot = grads.d_mu.data_ptr(), grads.d_log_scale.data_ptr(), grads.d_rot.data_ptr()
         g.d_sh, g.d_opacity_logits = grads.d_sh.data_ptr(), grads.d_opacity_logits.data_ptr()
         g.d_eta = grads.d_eta.data_ptr()
+        g.d_beta = d_beta.data_ptr() if d_beta is not None else None
         s = N.SsgAdamState()
-        for f, key in (("mu", "mu"), ("log_scale", "log_scale"), ("rot", "rot"), ("sh", "sh"),
-                       ("logits", "logits"), ("eta", "eta")):
-            setattr(s, "m_" + f, self.m[key].data_ptr())
-            setattr(s, "v_" + f, self.v[key].data_ptr())
+        for f in self.FIELDS:
+            setattr(s, "m_" + f, self.m[f].data_ptr())
+            setattr(s, "v_" + f, self.v[f].data_ptr())
         s.row_ok, s.n_skipped = self.row_ok.data_ptr(), self.n_skipped_dev.data_ptr()
         hp = N.SsgAdamHparams()
         hp.t = self.t
-        hp.lr_mu, hp.lr_scale, hp.lr_rot = self.lr.mu, self.lr.log_scale, self.lr.rot
-        hp.lr_sh, hp.lr_opacity, hp.lr_beta = self.lr.sh, self.lr.opacity, self.lr.beta
+        hp.lr_mu, hp.lr_scale, hp.lr_rot = cfg.position_lr_at(iteration), cfg.lr_scale, cfg.lr_rot
+        hp.lr_sh, hp.lr_opacity, hp.lr_beta = cfg.lr_sh, cfg.lr_opacity, cfg.lr_beta
         N.check(N.lib().ssg_adam_step(ctypes.byref(p), ctypes.byref(g), ctypes.byref(s), ctypes.byref(hp),
-                                      torch.cuda.current_stream(ds.mu.device).cuda_stream), "ssg_adam_step")
+                                      _stream(ds.mu.device)), "ssg_adam_step")
 
+    @property
     def n_skipped(self) -> int:
+        """Primitive-steps skipped so far for a non-finite gradient (adam.py:79)."""
         return int(self.n_skipped_dev.item())
 
 
+class Trainer:
+    """Per-image-size scratch (loss, regularizer buffers) for training_step."""
+
+    def __init__(self, eng: Engine, ds: DeviceScene, adam: DeviceAdam, cfg: TrainConfig | None = None):
+        self.eng, self.ds, self.adam = eng, ds, adam
+        self.cfg = cfg or adam.cfg
+        self._loss = {}
+        self.d_beta = None
+
+    def loss_for(self, W: int, H: int) -> ImageLoss:
+        key = (W, H)
+        if key not in self._loss:
+            self._loss[key] = ImageLoss(W, H, self.cfg.lambda_ssim, self.eng.device)
+        return self._loss[key]
+
+    def step(self, view, target: torch.Tensor, iteration: int, stats: IntervalStats | None = None,
+             s: float = 0.3, group=None, check_finite: bool = True):
+        """fit2d.py:62-78.  Returns (loss tensor of this rank, frame)."""
+        eng, ds, cfg = self.eng, self.ds, self.cfg
+        f = eng.forward(ds, view, s)
+        lossfn = self.loss_for(f.width, f.height)
+        dL = lossfn(f.color, target)
+        n = ds.n
+        if self.d_beta is None or self.d_beta.shape[0] < n:
+            self.d_beta = torch.empty((max(n, 1), 3), dtype=torch.float32, device=eng.device)
+        # the regularizer value is part of the loss (losses.py:146-149); its
+        # gradients are folded in after the backward and the statistics
+        lossfn.sums[2].zero_()
+        if check_finite:
+            v = lossfn.value_tensor()
+            if not math.isfinite(float(v)):  # fit2d.py:70-71: no backward, no update
+                return v, f
+        grads = eng.backward(ds, view, s, f.final_T, f.last_idx, dL, rebin=False)
+        allreduce_gradients(grads, group)
+        if stats is not None:
+            world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+            stats.add(grads, views=world)
+        N.check(N.lib().ssg_regularize(n, ds.beta.data_ptr(), ds.opacity_logits.data_ptr(), grads.d_eta.data_ptr(),
+                                       cfg.lambda_beta_reg, cfg.lambda_opacity_reg, self.d_beta.data_ptr(),
+                                       grads.d_opacity_logits.data_ptr(), lossfn.sums.data_ptr(),
+                                       _stream(eng.device)), "ssg_regularize")
+        self.adam.step(grads, iteration, d_beta=self.d_beta[:n])
+        return lossfn.value_tensor(), f
+
+
 def training_step(eng: Engine, ds: DeviceScene, adam: DeviceAdam, view, target: torch.Tensor,
-                  s: float = 0.3, group=None) -> torch.Tensor:
-    """One view-parallel step: render this rank's view, L1 loss, backward,
-    all-reduce gradients, Adam.  Returns the (device) loss of this rank."""
-    f = eng.forward(ds, view, s)
-    loss, dL = l1_loss_grad(f.color, target)
-    grads = eng.backward(ds, view, s, f.final_T, f.last_idx, dL.contiguous(), rebin=False)
-    allreduce_gradients(grads, group)
-    adam.step(grads)
+                  iteration: int = 0, stats: IntervalStats | None = None, s: float = 0.3,
+                  group=None) -> torch.Tensor:
+    """One view-parallel step (fit2d.py:62-78 + the gradient all-reduce).
+    Returns the (device) loss of this rank."""
+    tr = getattr(adam, "_trainer", None)
+    if tr is None or tr.eng is not eng or tr.ds is not ds:
+        tr = Trainer(eng, ds, adam)
+        adam._trainer = tr
+    loss, _ = tr.step(view, target, iteration, stats=stats, s=s, group=group)
     return loss
