@@ -237,6 +237,40 @@ int ssg_interval_stats_add(int64_t n, const float *g_uv, const float *g_z, const
 int ssg_adam_step(const ssg_params *params, const ssg_grad_buffers *grads,
                   const ssg_adam_state *state, const ssg_adam_hparams *hp, void *stream);
 
+/* ---- adaptive density control --------------------- */
+/* optimize/densify.py:24-116 inputs: the interval statistics bundle */
+typedef struct ssg_densify_stats {
+    const double *g_uv;         /* (n) mean screen-space positional gradient */
+    const float *g_z;           /* (n) max depth gradient */
+    const double *d_mu;         /* (n,3) mean position gradient */
+} ssg_densify_stats;
+
+typedef struct ssg_densify_cfg {
+    double tau_uv;
+    double tau_z;               /* NaN: calibrate to the 90th percentile of g_z */
+    double split_scale_threshold;
+    double prune_alpha;
+    double max_screen_radius;   /* < 0: no radius cap */
+    double clone_lr;            /* position_lr_at(densify_start), densify.py:49 */
+    const double *max_radii;    /* optional (n) screen radii, NULL: none */
+} ssg_densify_cfg;
+
+size_t ssg_densify_temp_bytes(int64_t n);
+/* flags (n bytes: 1 keep, 2 clone, 4 split, 8 prune) and, on the host,
+ * counts[4] = {n_keep, n_clone, n_split, n_pruned} and the tau_z used; the new
+ * primitive count is n_keep + n_clone + 2 n_split.  Synchronises the stream. */
+int ssg_densify_plan(const ssg_scene *scene, const ssg_densify_stats *stats, const ssg_densify_cfg *cfg,
+                     uint8_t *flags, void *temp, size_t temp_bytes, int64_t *counts, double *tau_z,
+                     void *stream);
+/* writes the new scene into `out` (capacity for the new count; same SH
+ * degree) in the reference's row order and, when given, the remapped Adam
+ * moments (adam.py:99-110); *bad = 1 when an output is non-finite
+ * (densify.py:112-114).  `temp` and `flags` as left by ssg_densify_plan. */
+int ssg_densify_apply(const ssg_scene *scene, const ssg_params *out, const ssg_adam_state *adam_in,
+                      const ssg_adam_state *adam_out, const ssg_densify_stats *stats,
+                      const ssg_densify_cfg *cfg, const uint8_t *flags, void *temp, int32_t *bad,
+                      void *stream);
+
 /* ---- test hooks (used by tests/ only) ----------------------------------- */
 /* the depth sort of ssg_bin_prepare in isolation: stable sort of u64 keys
  * (not modified), vals <- the ids 0..n-1 in sorted order; key_bytes must be 8,

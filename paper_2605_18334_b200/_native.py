@@ -24,7 +24,8 @@ EXPORTS = ("ssg_abi_version", "ssg_last_error", "ssg_grid_dims", "ssg_bin_temp_b
            "ssg_blend_backward", "ssg_preprocess_backward", "ssg_blend_backward_slots",
            "ssg_test_sort_temp_bytes",
            "ssg_test_sort", "ssg_test_blend_forward_vanilla", "ssg_adam_step", "ssg_blend_mask_words",
-           "ssg_loss_scratch_floats", "ssg_image_loss", "ssg_regularize", "ssg_interval_stats_add")
+           "ssg_loss_scratch_floats", "ssg_image_loss", "ssg_regularize", "ssg_interval_stats_add",
+           "ssg_densify_temp_bytes", "ssg_densify_plan", "ssg_densify_apply")
 
 _vp = ctypes.c_void_p
 
@@ -76,6 +77,15 @@ class SsgAdamState(ctypes.Structure):
     _fields_ = [(f, _vp) for f in ("m_mu", "v_mu", "m_log_scale", "v_log_scale", "m_rot", "v_rot", "m_sh",
                                    "v_sh", "m_logits", "v_logits", "m_beta", "v_beta", "m_dir", "v_dir",
                                    "row_ok", "n_skipped")]
+
+
+class SsgDensifyStats(ctypes.Structure):
+    _fields_ = [("g_uv", _vp), ("g_z", _vp), ("d_mu", _vp)]
+
+
+class SsgDensifyCfg(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_double) for f in ("tau_uv", "tau_z", "split_scale_threshold", "prune_alpha",
+                                               "max_screen_radius", "clone_lr")] + [("max_radii", _vp)]
 
 
 class SsgAdamHparams(ctypes.Structure):
@@ -131,6 +141,12 @@ def lib():
     L.ssg_test_sort_temp_bytes.restype = ctypes.c_size_t
     L.ssg_test_sort_temp_bytes.argtypes = [ctypes.c_int64, ctypes.c_int]
     L.ssg_test_sort.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int, _vp, _vp]
+    L.ssg_densify_temp_bytes.restype = ctypes.c_size_t
+    L.ssg_densify_temp_bytes.argtypes = [ctypes.c_int64]
+    L.ssg_densify_plan.argtypes = [P(SsgScene), P(SsgDensifyStats), P(SsgDensifyCfg), _vp, _vp, ctypes.c_size_t,
+                                   P(ctypes.c_int64), P(ctypes.c_double), _vp]
+    L.ssg_densify_apply.argtypes = [P(SsgScene), P(SsgParams), _vp, _vp, P(SsgDensifyStats), P(SsgDensifyCfg), _vp,
+                                    _vp, _vp, _vp]
     L.ssg_loss_scratch_floats.restype = ctypes.c_int64
     L.ssg_loss_scratch_floats.argtypes = [ctypes.c_int32, ctypes.c_int32]
     L.ssg_image_loss.argtypes = [_vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_float, _vp, _vp, _vp, _vp]

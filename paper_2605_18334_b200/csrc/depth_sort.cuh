@@ -117,7 +117,7 @@ __device__ __forceinline__ void scan256(const uint32_t *in, uint32_t *out, uint3
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_depth_sort(Args a) {
+static __global__ void __launch_bounds__(kThreads, 1) k_depth_sort(Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem &s = *reinterpret_cast<Smem *>(smem_raw);
     cg::grid_group grid = cg::this_grid();
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_depth_sort(Args a) {
 
 // Host side: sort (and, with count != nullptr, scan the counts in depth
 // order).  keys are not modified.
-inline cudaError_t sort_and_scan(const uint64_t *keys, uint32_t *order, const uint32_t *count, uint64_t *rank_offset,
+static inline cudaError_t sort_and_scan(const uint64_t *keys, uint32_t *order, const uint32_t *count, uint64_t *rank_offset,
                                  int64_t *n_instances, int64_t n, void *temp, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     char *tp = (char *)temp;
