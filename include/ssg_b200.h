@@ -271,6 +271,25 @@ int ssg_densify_apply(const ssg_scene *scene, const ssg_params *out, const ssg_a
                       const ssg_densify_cfg *cfg, const uint8_t *flags, void *temp, int32_t *bad,
                       void *stream);
 
+/* ---- frame serving --------------------------------- */
+/* dataset.py:33-38 quantize_u8 on the device: dst[i] = rint(clip(src[i], 0, 1)
+ * * 255) evaluated in fp64 (round half to even); src is f32 (a rendered
+ * frame) or, with src_is_f64, f64 */
+int ssg_quantize_u8(const void *src, int32_t src_is_f64, int64_t n_values, uint8_t *dst, void *stream);
+
+/* ---- scene PLY -> device SoA ----------------------- */
+/* PLY property types (scene.py:210-216) */
+enum { SSG_PLY_ABSENT = -1, SSG_PLY_F32 = 0, SSG_PLY_F64 = 1, SSG_PLY_I8 = 2, SSG_PLY_U8 = 3,
+       SSG_PLY_I16 = 4, SSG_PLY_U16 = 5, SSG_PLY_I32 = 6, SSG_PLY_U32 = 7 };
+/* Unpack n binary little-endian vertex records (`stride` bytes each, device
+ * memory) into `out` (capacity n).  offsets/types (host arrays of 18 + 3K
+ * entries) give each destination component's byte offset and type in the
+ * record, in the order mu 0-2, log_scale 3-5, rot 6-9, opacity_logits 10-11,
+ * beta 12-14, dir 15-17, sh (K,3); type SSG_PLY_ABSENT stores 0 (load_ply,
+ * scene.py:222-313: the host resolves names, defaults and errors). */
+int ssg_ply_unpack(const uint8_t *payload, int64_t n, int32_t stride, const int32_t *offsets,
+                   const int32_t *types, int32_t sh_coeffs, const ssg_params *out, void *stream);
+
 /* ---- test hooks (used by tests/ only) ----------------------------------- */
 /* the depth sort of ssg_bin_prepare in isolation: stable sort of u64 keys
  * (not modified), vals <- the ids 0..n-1 in sorted order; key_bytes must be 8,

@@ -7,7 +7,9 @@ include/ssg_b200.h).  No CPU fallback exists.
 """
 
 from .camera import OPENCV, OPENGL, CameraView, intrinsics, look_at, to_opencv, world_to_cam
+from .ply import PlyError, PlyFormatError, PlyMissingFieldError, PlyTruncatedError, load_ply
 from .scene import Scene, SkewGaussian
 
 __all__ = ["CameraView", "Scene", "SkewGaussian", "look_at", "to_opencv", "intrinsics",
-           "world_to_cam", "OPENCV", "OPENGL"]
+           "world_to_cam", "OPENCV", "OPENGL", "load_ply", "PlyError", "PlyFormatError",
+           "PlyMissingFieldError", "PlyTruncatedError"]

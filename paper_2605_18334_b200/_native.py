@@ -25,7 +25,8 @@ EXPORTS = ("ssg_abi_version", "ssg_last_error", "ssg_grid_dims", "ssg_bin_temp_b
            "ssg_test_sort_temp_bytes",
            "ssg_test_sort", "ssg_test_blend_forward_vanilla", "ssg_adam_step", "ssg_blend_mask_words",
            "ssg_loss_scratch_floats", "ssg_image_loss", "ssg_regularize", "ssg_interval_stats_add",
-           "ssg_densify_temp_bytes", "ssg_densify_plan", "ssg_densify_apply")
+           "ssg_densify_temp_bytes", "ssg_densify_plan", "ssg_densify_apply", "ssg_ply_unpack",
+           "ssg_quantize_u8")
 
 _vp = ctypes.c_void_p
 
@@ -141,6 +142,8 @@ def lib():
     L.ssg_test_sort_temp_bytes.restype = ctypes.c_size_t
     L.ssg_test_sort_temp_bytes.argtypes = [ctypes.c_int64, ctypes.c_int]
     L.ssg_test_sort.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int, _vp, _vp]
+    L.ssg_ply_unpack.argtypes = [_vp, ctypes.c_int64, ctypes.c_int32, _vp, _vp, ctypes.c_int32, P(SsgParams), _vp]
+    L.ssg_quantize_u8.argtypes = [_vp, ctypes.c_int32, ctypes.c_int64, _vp, _vp]
     L.ssg_densify_temp_bytes.restype = ctypes.c_size_t
     L.ssg_densify_temp_bytes.argtypes = [ctypes.c_int64]
     L.ssg_densify_plan.argtypes = [P(SsgScene), P(SsgDensifyStats), P(SsgDensifyCfg), _vp, _vp, ctypes.c_size_t,

@@ -5,7 +5,8 @@ names, shapes and fp64 host dtype (pkg/src/skewsplat/scene.py:42-164):
 mu (N,3), log_scale (N,3), rot (N,4, w x y z), sh (N,K,3), opacity_logits
 (N,2), beta (N,3), dir (N,3), background (3,), sh_degree 0..3.  Any object
 with these attributes (including the reference's own Scene) is accepted by
-the rasterizer.  PLY serialization is outside the hot-path scope.
+the rasterizer.  PLY serialization: ply.py (save_ply / load_ply, and
+load_ply_device straight into the device layout).
 """
 
 from __future__ import annotations
@@ -74,6 +75,11 @@ class Scene:
 
     def __len__(self) -> int:
         return self.mu.shape[0]
+
+    def save_ply(self, path):
+        """scene.py:177-207 (ply.save_ply)."""
+        from .ply import save_ply
+        save_ply(self, path)
 
     def primitive(self, i: int) -> SkewGaussian:
         return SkewGaussian(*(getattr(self, f)[i] for f in self.ARRAY_FIELDS))
