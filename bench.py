@@ -134,14 +134,15 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []          # (host time, fields)
         self.proc = None
+        self.window = None      # (t0, t1) of the timed region, host clock
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "20"],
+                 "--format=csv,noheader,nounits", "-lms", "10"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -150,7 +151,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
+
+    def mark(self, t0: float, t1: float):
+        self.window = (t0, t1)
 
     def stop(self):
         if self.proc is None:
@@ -161,14 +165,21 @@ class ClockSampler:
         except subprocess.TimeoutExpired:
             self.proc.kill()
         self.t.join(timeout=2)
-        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        rows = [(t, r) for t, r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        inside = rows
+        if self.window is not None:
+            # samples that arrived during the timed region (+ the reporting lag)
+            t0, t1 = self.window
+            inside = [(t, r) for t, r in rows if t0 <= t <= t1 + 0.05]
+            if not inside and rows:  # region shorter than the sampling period: nearest sample
+                inside = [min(rows, key=lambda x: abs(x[0] - 0.5 * (t0 + t1)))]
+        sm = [float(r[0]) for _, r in inside]
+        mx = [float(r[1]) for _, r in inside if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[j] for r in self.rows if len(r) >= 7
-                          for j in range(4) if r[3 + j].lower() == "active"})
+        reasons = sorted({names[j] for _, r in inside for j in range(4) if r[3 + j].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(sm)}
+                "samples": len(sm), "window_s": None if self.window is None else self.window[1] - self.window[0]}
 
 
 # ------------------------------------------------------------------ main
@@ -192,7 +203,7 @@ def tile_pairs(frame, ranges, width, height):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -274,22 +285,24 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    clocks = ClockSampler(local)
+    clocks.start()  # sampling runs from the warm-up on; the timed window is marked
     for _ in range(max(args.warmup, 3)):
         f = step()
     barrier()
     m = f.n_instances
     pairs = tile_pairs(f, eng.ranges, WIDTH, HEIGHT)
 
-    clocks = ClockSampler(local)
-    clocks.start()
     eng.stage_events = {}
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_start = time.perf_counter()
     e0.record()
     for _ in range(args.steps):
         step()
     e1.record()
     barrier()
+    clocks.mark(t_start, time.perf_counter())
     clk = clocks.stop()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     stage_ms = {k: statistics.mean(a.elapsed_time(b) for a, b in v) for k, v in eng.stage_events.items()}

@@ -89,11 +89,13 @@ def config4(args, rank, world, local):
     eng.stage_events = {}
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_start = time.perf_counter()
     e0.record()
     for _ in range(args.steps):
         render_views(ds, mine, engine=eng, out=out)
     e1.record()
     barrier()
+    clocks.mark(t_start, time.perf_counter())
     clk = clocks.stop()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     stage_ms = {k: statistics.mean(a.elapsed_time(b) for a, b in v) for k, v in eng.stage_events.items()}
@@ -166,6 +168,34 @@ def _cpu_forward_sample(scene, view, k):
     return "port", (lambda: O.render_forward(sub, sv, 0.3)), desc
 
 
+def _cpu_train_sample(scene, view, target, k):
+    """The reference's fit2d.training_step (Cython rasterizer on all cores,
+    SSIM loss, Adam) on a homothetic 1/k sample of one config-5 view."""
+    from paper_2605_18334_b200.synthetic import homothetic_sample
+    sub, sv = homothetic_sample(scene, view, k)
+    ys = (np.arange(sv.height) * view.height) // sv.height
+    xs = (np.arange(sv.width) * view.width) // sv.width
+    tgt = target[ys][:, xs].astype(np.float64)
+    desc = (f"homothetic 1/{k} sample of training view 0: {len(sub)} primitives, {sv.width}x{sv.height}, "
+            f"target subsampled; per-step time = {k} x sample time")
+    ref = B._load_reference()
+    if ref is None:
+        return None
+    from skewsplat.fit2d import training_step as ref_step
+    from skewsplat.optimize.adam import Adam
+    from skewsplat.optimize.config import TrainConfig
+    import skewsplat.scene as S
+    rs = S.Scene(*(getattr(sub, f).copy() for f in sub.ARRAY_FIELDS), background=sub.background.copy(),
+                 sh_degree=sub.sh_degree)
+    cfg = TrainConfig()
+    adam = Adam(rs, cfg)
+    ref_step(rs, sv, tgt, cfg, adam, 0)
+    t0 = time.perf_counter()
+    ref_step(rs, sv, tgt, cfg, adam, 1)
+    t = (time.perf_counter() - t0) * k
+    return {"value": 1.0 / t, "unit": "views/s", "cores": B.cpu_cores(), "kind": "reference", "sample": desc}
+
+
 def config5(args, rank, world, local):
     torch, dist = _setup(local, world)
     barrier, max_over_ranks = _helpers(torch, dist, world)
@@ -192,18 +222,20 @@ def config5(args, rank, world, local):
         step_no[0] += 1
         return training_step(eng, ds, adam, views[i], targets[i] if target is None else target)
 
+    clocks = B.ClockSampler(local)
+    clocks.start()
     for _ in range(max(args.warmup, 3)):
         step()
     barrier()
-    clocks = B.ClockSampler(local)
-    clocks.start()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_start = time.perf_counter()
     e0.record()
     for _ in range(args.steps):
         step()
     e1.record()
     barrier()
+    clocks.mark(t_start, time.perf_counter())
     clk = clocks.stop()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     # e2e: the step's input image from pinned host memory, loss read back
@@ -224,18 +256,20 @@ def config5(args, rank, world, local):
         "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 (blend, grads, moments) / f64 (preprocess)", "data": "synthetic",
         "config": {"workload": "config 5: G5 (ball scene, 2M), targets rendered from it, start perturbed "
-                               "(mu + N(0, 0.01)); per step per rank: fwd, L1, bwd, all-reduce, Adam",
+                               "(mu + N(0, 0.01)); per step per rank (fit2d.training_step): fwd, "
+                               "0.8 L1 + 0.2 (1 - SSIM) loss + pixel gradient, finite check, bwd, all-reduce, "
+                               "interval stats, regularizers, Adam (TrainConfig defaults)",
                    "parallelism": f"view-parallel x{world}, NCCL all-reduce SUM of {N5 * 65 * 4 / 1e6:.0f} MB "
                                   "packed gradients + MAX of g_z"},
         "clocks": clk,
         "e2e": {"value": world / e2e_s, "unit": "views/s", "h2d_bytes_per_step": H4 * W4 * 12,
                 "d2h_bytes_per_step": 4, "path": "training_step with the target image copied from pinned "
                                                  "host memory and the loss read back each step"},
-        "gpu_launches": (B.LAUNCHES_PER_FRAME + 8) * args.steps,
-        "cpu_baseline": None,
-        "cpu_baseline_note": "not measured for config 5 (the reference training step includes the "
-                             "SSIM loss and densification, outside this path); see config 2",
+        # per step: the frame's 14, image loss 2, regularizer 1, Adam 9 (rowcheck, 7 fields, renorm)
+        "gpu_launches": (B.LAUNCHES_PER_FRAME + 12) * args.steps,
     }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        result["cpu_baseline"] = _cpu_train_sample(start, views[0], targets[0].cpu().numpy(), 64)
     if rank == 0:
         print(json.dumps(result))
     if world > 1:
