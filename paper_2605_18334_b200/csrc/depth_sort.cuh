@@ -11,22 +11,24 @@
 //   phase 0   min / max of the valid keys; keys are rebased, k' = k - min
 //             (no-instance keys map to ~0), nbits = significant bits of the
 //             largest k'
-//   passes    LSD over the top 32 significant bits only (4 byte digits):
+//   passes    LSD over the top kWindow (24) significant bits only (3 byte
+//             digits):
 //             A: per-tile digit counts -> tile_counts[digit][tile]
 //             B: exclusive scan of each digit row over the tiles (row totals
 //                -> bucket bases)
 //             C: stable in-tile ranking (warp-striped, match_any per step),
 //                tile reordered by digit in shared memory, written out in
 //                digit runs (coalesced)
-//   fix-up    runs of keys equal in those 32 bits but out of order in the low
-//             bits (~1e-9 relative apart: rare, short) are insertion-sorted by
-//             the full key, stably; runs without an inversion (exact ties,
+//   fix-up    runs of keys equal in those 24 bits but out of order in the low
+//             bits (1 part in 2^24 of the depth range: rare, short) are
+//             insertion-sorted by the full key, stably; runs without an inversion (exact ties,
 //             no-instance keys) are already right; an inverted run longer
 //             than 32 triggers the exact fallback, a full LSD over every
 //             significant byte
 //   final     counts in depth order, exclusive scan over ranks -> rank_offset,
 //             n_instances
-// Tiles are 8192 keys; a CTA loops over several tiles when N > tiles x SMs.
+// Tiles are 8192 keys (1024 threads x 8), one CTA per SM; a CTA loops over
+// several tiles when N > tiles x CTAs.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -39,8 +41,15 @@ namespace dsort {
 
 namespace cg = cooperative_groups;
 
-constexpr int kThreads = 1024;
+#ifndef SSG_DS_THREADS
+#define SSG_DS_THREADS 1024
+#endif
+#ifndef SSG_DS_WINDOW
+#define SSG_DS_WINDOW 24
+#endif
+constexpr int kThreads = SSG_DS_THREADS;      // one CTA per SM
 constexpr int kWarps = kThreads / 32;
+constexpr int kWindow = SSG_DS_WINDOW;        // significant key bits sorted by the passes
 constexpr int kIPT = 8;                       // keys per lane per tile
 constexpr int kTile = kThreads * kIPT;        // 8192 keys
 constexpr uint64_t kInvalid = ~0ull;          // primitives without instances
@@ -117,7 +126,7 @@ __device__ __forceinline__ void scan256(const uint32_t *in, uint32_t *out, uint3
     __syncthreads();
 }
 
-static __global__ void __launch_bounds__(kThreads, 1) k_depth_sort(Args a) {
+static __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_depth_sort(Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem &s = *reinterpret_cast<Smem *>(smem_raw);
     cg::grid_group grid = cg::this_grid();
@@ -158,7 +167,7 @@ static __global__ void __launch_bounds__(kThreads, 1) k_depth_sort(Args a) {
     const uint64_t kmin = *((volatile unsigned long long *)&a.ctl->kmin);
     const uint64_t kmax = *((volatile unsigned long long *)&a.ctl->kmax);
     const int nbits = kmax >= kmin && kmax != kmin ? 64 - __clzll((long long)(kmax - kmin)) : 0;
-    const int sh = nbits > 32 ? nbits - 32 : 0;            // window [sh, nbits)
+    const int sh = nbits > kWindow ? nbits - kWindow : 0;  // window [sh, nbits)
     const int npw = (nbits - sh + 7) / 8;                    // window passes
 
     // ---------------------------------------------------------- passes

@@ -8,6 +8,6 @@ out=gpurun_out/${tag}_ab.txt; : > $out
 for v in "$@"; do
   lib=paper_2605_18334_b200/libssg_b200_${v}.so; [ "$v" = main ] && lib=paper_2605_18334_b200/libssg_b200.so
   echo "== $v" >> $out
-  SSG_B200_LIB=$lib timeout 300 python tools/stage_times.py --reps 6 2>&1 | tail -3 >> $out
+  SSG_B200_LIB=$lib timeout 300 python tools/stage_times.py --reps 6 ${STAGE_ARGS:-} 2>&1 | tail -3 >> $out
 done
 cat $out

@@ -24,10 +24,17 @@ def main():
     ap.add_argument("--h", type=int, default=1080)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--plain", type=float, default=0.0)
+    ap.add_argument("--ball", action="store_true", help="config-4 scene (3M ball, orbit view 0, 1297x840)")
     a = ap.parse_args()
     t0 = time.time()
-    scene = frustum_scene(a.n, width=a.w, height=a.h, plain_fraction=a.plain)
-    view = frustum_view(a.w, a.h)
+    if a.ball:
+        from paper_2605_18334_b200.synthetic import ball_scene, orbit_views
+        scene = ball_scene(3_000_000, seed=0)
+        view = orbit_views(64, radius=4.0, elevation=1.2, width=1297, height=840, fov_x=0.9)[0]
+        a.w, a.h = 1297, 840
+    else:
+        scene = frustum_scene(a.n, width=a.w, height=a.h, plain_fraction=a.plain)
+        view = frustum_view(a.w, a.h)
     print(f"scene gen {time.time()-t0:.1f}s", flush=True)
     eng = Engine()
     ds = DeviceScene.from_host(scene)
