@@ -268,8 +268,10 @@ def main():
     ds = DeviceScene.from_host(scene)
     dL = torch.from_numpy(dL_host).cuda().float()
 
-    def step():
-        f = eng.forward(ds, view, 0.3)
+    def step(sync=False):
+        # no host round trip inside the frame (the instance buffers are sized
+        # by the first, synchronised frame; eng.instances() checks after the run)
+        f = eng.forward(ds, view, 0.3, sync=sync)
         eng.backward(ds, view, 0.3, f.final_T, f.last_idx, dL, rebin=False)
         return f
 
@@ -287,10 +289,10 @@ def main():
 
     clocks = ClockSampler(local)
     clocks.start()  # sampling runs from the warm-up on; the timed window is marked
-    for _ in range(max(args.warmup, 3)):
-        f = step()
+    for i in range(max(args.warmup, 3)):
+        f = step(sync=(i == 0))
     barrier()
-    m = f.n_instances
+    m = eng.instances()
     pairs = tile_pairs(f, eng.ranges, WIDTH, HEIGHT)
 
     eng.stage_events = {}
@@ -304,6 +306,7 @@ def main():
     barrier()
     clocks.mark(t_start, time.perf_counter())
     clk = clocks.stop()
+    assert eng.instances() == m  # no sync-free frame overflowed its buffers
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     stage_ms = {k: statistics.mean(a.elapsed_time(b) for a, b in v) for k, v in eng.stage_events.items()}
     eng.stage_events = None

@@ -103,7 +103,9 @@ typedef struct ssg_prim_buffers {
 typedef struct ssg_bin_buffers {
     uint32_t *depth_order;      /* (n) primitive ids sorted by (depth, id) */
     uint64_t *rank_offset;      /* (n+1) exclusive scan of counts in depth order */
-    int64_t *n_instances;       /* (1) device copy of M */
+    int64_t *n_instances;       /* (2) device: [0] M of the last ssg_bin_prepare, [1] running
+                                   max of M (never reset by the library; lets a caller that
+                                   skips the read-back check a batch of frames at once) */
     int64_t capacity;           /* allocated instances */
     uint32_t *inst_prim;        /* (capacity) sorted primitive id per instance */
     uint16_t *inst_tile;        /* (capacity) sorted tile id per instance */
@@ -187,7 +189,9 @@ int ssg_bin_prepare(int64_t n, const ssg_prim_buffers *prim, const ssg_bin_buffe
 int ssg_bin_rects(int64_t n, const double *mean2d, const double *radius, const double *depth,
                   const uint8_t *valid, int32_t width, int32_t height,
                   const ssg_prim_buffers *out, void *stream);
-/* duplicate, stable sort by tile, ranges; m = value of *bins->n_instances */
+/* two-level counting scatter, ranges; m = bins->n_instances[0] read back, or m < 0 to
+ * skip the read-back (writes stay inside `capacity`; M > capacity means the frame is
+ * invalid and must be redone with larger buffers) */
 int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t height,
                    const ssg_prim_buffers *prim, const ssg_bin_buffers *bins, void *stream);
 /* words of the optional frame blend mask for m instances over n_tiles tiles */

@@ -310,8 +310,11 @@ __global__ void __launch_bounds__(256) k_cs1_rowscan(uint32_t *__restrict__ cnt1
 
 // one CTA: row starts (exclusive scan of row totals) and level-2 chunk bases
 // (exclusive scan of ceil(total / C2)); ctl[0] = number of level-2 chunks
+// A sync-free frame (ssg_bin_finish with m < 0) may find more instances than
+// the buffers hold: chunk bases are clamped to max_ch2 so no table is
+// overrun (the caller detects the overflow as n_instances > capacity).
 __global__ void __launch_bounds__(1024) k_cs1_rowstart(const uint32_t *__restrict__ row_total, int32_t nty,
-                                                       uint32_t *__restrict__ row_start,
+                                                       uint32_t max_ch2, uint32_t *__restrict__ row_start,
                                                        uint32_t *__restrict__ chunk_base, uint32_t *__restrict__ ctl) {
     __shared__ uint32_t s_warp[32];
     for (int y = threadIdx.x; y < nty; y += blockDim.x) chunk_base[y] = (row_total[y] + kCsC2 - 1) / kCsC2;
@@ -319,10 +322,12 @@ __global__ void __launch_bounds__(1024) k_cs1_rowstart(const uint32_t *__restric
     const uint32_t rt = cta_scan_runs(row_total, row_start, nty, s_warp);
     __syncthreads();
     const uint32_t ct = cta_scan_runs(chunk_base, chunk_base, nty, s_warp);
+    __syncthreads();
+    for (int y = threadIdx.x; y < nty; y += blockDim.x) chunk_base[y] = min(chunk_base[y], max_ch2);
     if (threadIdx.x == 0) {
         row_start[nty] = rt;
-        chunk_base[nty] = ct;
-        ctl[0] = ct;
+        chunk_base[nty] = min(ct, max_ch2);
+        ctl[0] = min(ct, max_ch2);
     }
 }
 
@@ -334,7 +339,7 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs1_scatter(const uint32_t *_
                                                                const uint32_t *__restrict__ cnt1,
                                                                const uint32_t *__restrict__ row_total,
                                                                const uint32_t *__restrict__ row_start,
-                                                               uint64_t *__restrict__ rowlist) {
+                                                               uint64_t *__restrict__ rowlist, uint32_t cap) {
     extern __shared__ __align__(16) unsigned char s_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     unsigned char *base = s_raw + (size_t)w * cs_warp_smem<uint64_t>(nty);
@@ -365,13 +370,16 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs1_scatter(const uint32_t *_
             if (staged) {
                 st_pay[pos] = pay;
                 st_b[pos] = (uint16_t)y;
-            } else {
+            } else if (pos < cap) {
                 rowlist[pos] = pay;
             }
         });
     if (staged) {  // bucket-major local order: runs of one row are contiguous in rowlist
         __syncwarp();
-        for (uint32_t i = lane; i < total; i += 32) rowlist[delta[st_b[i]] + i] = st_pay[i];
+        for (uint32_t i = lane; i < total; i += 32) {
+            const uint32_t pos = delta[st_b[i]] + i;
+            if (pos < cap) rowlist[pos] = st_pay[i];
+        }
     }
 }
 
@@ -391,7 +399,7 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs2_count(const uint64_t *__r
                                                              const uint32_t *__restrict__ row_start,
                                                              const uint32_t *__restrict__ chunk_base,
                                                              const uint32_t *__restrict__ ctl, int32_t ntx,
-                                                             int32_t nty, uint32_t *__restrict__ cnt2) {
+                                                             int32_t nty, uint32_t *__restrict__ cnt2, uint32_t cap) {
     extern __shared__ uint32_t s_cs[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     uint32_t *h = s_cs + (size_t)w * (ntx + 1);
@@ -401,7 +409,7 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs2_count(const uint64_t *__r
         const uint32_t k = c - chunk_base[y], nk = chunk_base[y + 1] - chunk_base[y];
         for (int x = lane; x <= ntx; x += 32) h[x] = 0;
         __syncwarp();
-        const uint32_t i0 = row_start[y] + k * kCsC2, i1 = min(row_start[y + 1], i0 + kCsC2);
+        const uint32_t i0 = row_start[y] + k * kCsC2, i1 = min(min(row_start[y + 1], i0 + kCsC2), cap);
         for (uint32_t i = i0 + lane; i < i1; i += 32) {
             const uint64_t seg = rowlist[i];
             atomicAdd(&h[(int)((seg >> 32) & 0xffff)], 1u);
@@ -455,15 +463,16 @@ __global__ void __launch_bounds__(256) k_cs2_tilescan(uint32_t *__restrict__ cnt
 // [start, start + total): empty tiles sit at the insertion point, exactly
 // np.searchsorted left/right (tiles.py:76-78)
 __global__ void __launch_bounds__(1024) k_cs2_tilestart(const uint32_t *__restrict__ tile_total, int32_t n_tiles,
-                                                        uint32_t *__restrict__ tile_start,
+                                                        uint32_t cap, uint32_t *__restrict__ tile_start,
                                                         int32_t *__restrict__ ranges) {
     __shared__ uint32_t s_warp[32];
     cta_scan_runs(tile_total, tile_start, n_tiles, s_warp);
     __syncthreads();
     for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
         const uint32_t st = tile_start[t];
-        ranges[2 * t] = (int32_t)st;
-        ranges[2 * t + 1] = (int32_t)(st + tile_total[t]);
+        // clamped to the capacity: an overflowing sync-free frame never reads past it
+        ranges[2 * t] = (int32_t)min(st, cap);
+        ranges[2 * t + 1] = (int32_t)min(st + tile_total[t], cap);
     }
 }
 
@@ -477,7 +486,7 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs2_scatter(const uint64_t *_
                                                                const uint32_t *__restrict__ tile_start,
                                                                int32_t ntx, int32_t nty,
                                                                uint32_t *__restrict__ inst_prim,
-                                                               uint16_t *__restrict__ inst_tile) {
+                                                               uint16_t *__restrict__ inst_tile, uint32_t cap) {
     extern __shared__ __align__(16) unsigned char s_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     unsigned char *base = s_raw + (size_t)w * cs_warp_smem<uint32_t>(ntx);
@@ -498,7 +507,7 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs2_scatter(const uint64_t *_
             },
             [&](int x) { return tile_start[trow + x] + blk[(size_t)x * nk + k]; });
         const bool staged = total <= (uint32_t)kCsStage;
-        const uint32_t i0 = row_start[y] + k * kCsC2, i1 = min(row_start[y + 1], i0 + kCsC2);
+        const uint32_t i0 = row_start[y] + k * kCsC2, i1 = min(min(row_start[y + 1], i0 + kCsC2), cap);
         cs_walk<uint32_t>(
             i0, i1, lane, scur,
             [&](int64_t i, int &b0, int &b1, uint32_t &pay) {
@@ -511,7 +520,7 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs2_scatter(const uint64_t *_
                 if (staged) {
                     st_pay[pos] = p;
                     st_b[pos] = (uint16_t)x;
-                } else {
+                } else if (pos < cap) {
                     inst_prim[pos] = p;
                     if (inst_tile) inst_tile[pos] = (uint16_t)(trow + x);
                 }
@@ -521,6 +530,7 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs2_scatter(const uint64_t *_
             for (uint32_t i = lane; i < total; i += 32) {
                 const int x = st_b[i];
                 const uint32_t pos = delta[x] + i;
+                if (pos >= cap) continue;
                 inst_prim[pos] = st_pay[i];
                 if (inst_tile) inst_tile[pos] = (uint16_t)(trow + x);
             }
@@ -575,7 +585,7 @@ extern "C" int ssg_bin_prepare(int64_t n, const ssg_prim_buffers *prim, const ss
     if (!prim || !bins || n < 0 || n >= (int64_t)UINT32_MAX) return SSG_ERR_INVALID_ARGUMENT;
     cudaStream_t st = (cudaStream_t)stream;
     if (n == 0) {
-        cudaError_t e = cudaMemsetAsync(bins->n_instances, 0, sizeof(int64_t), st);
+        cudaError_t e = cudaMemsetAsync(bins->n_instances, 0, sizeof(int64_t), st);  // [1] (max) unchanged
         if (e == cudaSuccess) e = cudaMemsetAsync(bins->rank_offset, 0, sizeof(uint64_t), st);
         if (e != cudaSuccess) { set_error("memset", e); return SSG_ERR_CUDA; }
         return SSG_OK;
@@ -593,8 +603,11 @@ extern "C" int ssg_bin_prepare(int64_t n, const ssg_prim_buffers *prim, const ss
 extern "C" int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t height,
                               const ssg_prim_buffers *prim, const ssg_bin_buffers *bins, void *stream) {
     using namespace ssg;
-    if (!prim || !bins || n < 0 || m < 0 || width < 1 || height < 1) return SSG_ERR_INVALID_ARGUMENT;
-    if (m > bins->capacity || m >= (int64_t)INT32_MAX) return SSG_ERR_CAPACITY;
+    if (!prim || !bins || n < 0 || width < 1 || height < 1) return SSG_ERR_INVALID_ARGUMENT;
+    // m < 0: sync-free frame, M not read back; the kernels stay inside the
+    // capacity and the caller checks n_instances <= capacity afterwards
+    if (m > bins->capacity || m >= (int64_t)INT32_MAX || bins->capacity >= (int64_t)UINT32_MAX)
+        return SSG_ERR_CAPACITY;
     if (width > SSG_MAX_IMAGE_DIM || height > SSG_MAX_IMAGE_DIM) return SSG_ERR_DIM_OVERFLOW;
     const int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
     const int32_t n_tiles = ntx * nty;
@@ -629,17 +642,18 @@ extern "C" int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t heigh
     k_cs1_count<<<g1, 32 * kCsWarps, smc1, st>>>(bins->depth_order, prim->tile_count, prim->tile_rect, n, L.nch1,
                                                  nty, cnt1);
     k_cs1_rowscan<<<nty, 256, 0, st>>>(cnt1, L.nch1, row_total);
-    k_cs1_rowstart<<<1, 1024, 0, st>>>(row_total, nty, row_start, chunk_base, ctl);
+    const uint32_t cap = (uint32_t)(bins->capacity > 0 ? bins->capacity : 0);
+    k_cs1_rowstart<<<1, 1024, 0, st>>>(row_total, nty, (uint32_t)L.max_ch2, row_start, chunk_base, ctl);
     if (n > 0)
         k_cs1_scatter<<<g1, 32 * kCsWarps, sm1, st>>>(bins->depth_order, prim->tile_count, prim->tile_rect, n,
-                                                      L.nch1, nty, cnt1, row_total, row_start, rowlist);
+                                                      L.nch1, nty, cnt1, row_total, row_start, rowlist, cap);
     // level 2: per-tile lists of each row
-    k_cs2_count<<<g2, 32 * kCsWarps, smc2, st>>>(rowlist, row_start, chunk_base, ctl, ntx, nty, cnt2);
+    k_cs2_count<<<g2, 32 * kCsWarps, smc2, st>>>(rowlist, row_start, chunk_base, ctl, ntx, nty, cnt2, cap);
     k_cs2_tilescan<<<(unsigned)(((int64_t)n_tiles * 32 + 255) / 256), 256, 0, st>>>(cnt2, chunk_base, ntx, nty,
                                                                                     tile_total);
-    k_cs2_tilestart<<<1, 1024, 0, st>>>(tile_total, n_tiles, tile_start, bins->ranges);
+    k_cs2_tilestart<<<1, 1024, 0, st>>>(tile_total, n_tiles, cap, tile_start, bins->ranges);
     k_cs2_scatter<<<g2, 32 * kCsWarps, sm2, st>>>(rowlist, row_start, chunk_base, ctl, cnt2, tile_total, tile_start,
-                                                  ntx, nty, bins->inst_prim, bins->inst_tile);
+                                                  ntx, nty, bins->inst_prim, bins->inst_tile, cap);
     return check_launch("ssg_bin_finish");
 }
 

@@ -78,7 +78,7 @@ struct Args {
     uint32_t *order_out;          // (n) depth order (final permutation)
     const uint32_t *count;        // (n) instances per primitive (nullptr: sort only)
     uint64_t *rank_offset;        // (n+1)
-    int64_t *n_instances;         // (1)
+    int64_t *n_instances;         // (2): [0] M, [1] running max of M (caller-reset)
     int64_t n;
     Ctl *ctl;
     uint32_t *tile_counts;        // [256][ntiles]
@@ -409,7 +409,10 @@ static __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_depth_sort
             if (r < n) a.rank_offset[r + 1] = run;
         }
         if (tile == 0 && t == 0) a.rank_offset[0] = 0;
-        if (tile == ntiles - 1 && t == kThreads - 1) *a.n_instances = (int64_t)run;
+        if (tile == ntiles - 1 && t == kThreads - 1) {
+            a.n_instances[0] = (int64_t)run;
+            atomicMax(reinterpret_cast<unsigned long long *>(a.n_instances + 1), (unsigned long long)run);
+        }
         __syncthreads();
     }
 }

@@ -108,7 +108,7 @@ class DeviceFrame:
     width: int
     height: int
     n_primitives: int
-    n_instances: int
+    n_instances: int          # -1 for a sync-free frame (Engine.instances() reads it)
     s: float
 
 
@@ -176,7 +176,7 @@ class Engine:
         self.n_fallback = self._empty((1,), torch.int32)
         self.depth_order = self._empty((nn,), torch.int32)
         self.rank_offset = self._empty((nn + 1,), torch.int64)
-        self.n_inst_dev = self._empty((1,), torch.int64)
+        self.n_inst_dev = torch.zeros((2,), dtype=torch.int64, device=self.device)  # M, running max
         self._prim_n = nn
         self._bins_key = None
 
@@ -273,17 +273,23 @@ class Engine:
         return torch.cuda.current_stream(self.device).cuda_stream
 
     # ------------------------------------------------------------- stages
-    def _bin(self, n: int, W: int, H: int) -> int:
-        """bin_prepare -> M (one 8-byte D2H) -> bin_finish."""
+    def _bin(self, n: int, W: int, H: int, sync: bool = True) -> int:
+        """bin_prepare -> M (one 8-byte D2H) -> bin_finish.  sync=False skips
+        the read-back when buffers already exist for this size: the kernels
+        stay inside the capacity and instances() detects an overflow later
+        (returns -1 for M)."""
         ntx, nty = grid_dims(W, H)
         st = self._stream()
+        sync = sync or self.capacity == 0 or self._bins_key is None or self._bins_key[2:] != (W, H) \
+            or self._prim_n < n
         self._ensure_bins(n, self.capacity, W, H)
         prim = self._prim_struct()
         with self._mark("bin_prepare"):
             N.check(self.lib.ssg_bin_prepare(n, ctypes.byref(prim), ctypes.byref(self._bins_struct()), st),
                     "ssg_bin_prepare")
-        m = int(self.n_inst_dev.item())
-        self._ensure_bins(n, m, W, H)
+        m = int(self.n_inst_dev[0].item()) if sync else -1
+        if sync:
+            self._ensure_bins(n, m, W, H)
         with self._mark("bin_finish"):
             N.check(self.lib.ssg_bin_finish(n, m, W, H, ctypes.byref(prim), ctypes.byref(self._bins_struct()), st),
                     "ssg_bin_finish")
@@ -291,7 +297,20 @@ class Engine:
         self._bin_gen += 1
         return m
 
-    def project_and_bin(self, ds: DeviceScene, cam: N.SsgCamera) -> int:
+    def instances(self) -> int:
+        """M of the last binning (synchronises); raises if any frame since the
+        last call overflowed the instance capacity (those results are
+        invalid; the next synchronised binning grows the buffers)."""
+        m, worst = (int(x) for x in self.n_inst_dev.tolist())
+        self.n_inst_dev[1] = 0
+        if worst > self.capacity:
+            self._bins_key = None
+            raise N.NativeError(f"sync-free frame needed {worst} instances, capacity {self.capacity}; "
+                                "re-run synchronised")
+        self.last_m = m
+        return m
+
+    def project_and_bin(self, ds: DeviceScene, cam: N.SsgCamera, sync: bool = True) -> int:
         W, H = int(cam.width), int(cam.height)
         if W > 65535 or H > 65535:
             raise ValueError("image dimension overflow")
@@ -301,7 +320,7 @@ class Engine:
             N.check(self.lib.ssg_preprocess_forward(ctypes.byref(sc), ctypes.byref(cam),
                                                     ctypes.byref(self._prim_struct()), self._stream()),
                     "ssg_preprocess_forward")
-        return self._bin(ds.n, W, H)
+        return self._bin(ds.n, W, H, sync)
 
     def bin_arrays(self, mean2d, radius, depth, valid, W: int, H: int) -> int:
         """Binning of caller-provided screen arrays (device tensors, fp64/uint8)."""
@@ -313,13 +332,15 @@ class Engine:
         return self._bin(n, W, H)
 
     def forward(self, ds: DeviceScene, view: CameraView, s: float = 0.3,
-                color_out: torch.Tensor | None = None) -> DeviceFrame:
+                color_out: torch.Tensor | None = None, sync: bool = True) -> DeviceFrame:
         """Project, bin and blend one view.  `color_out` (contiguous f32
         (H,W,3) on this device) receives the image instead of the engine's
-        own colour buffer (view batches write straight into their slice)."""
+        own colour buffer (view batches write straight into their slice).
+        sync=False: no host round trip inside the frame (see _bin); the
+        caller checks instances() before trusting the result."""
         cam = camera_struct(view, s)
         W, H = int(cam.width), int(cam.height)
-        m = self.project_and_bin(ds, cam)
+        m = self.project_and_bin(ds, cam, sync)
         self._ensure_frame(W, H)
         if color_out is not None and (tuple(color_out.shape) != (H, W, 3) or color_out.dtype != torch.float32
                                       or not color_out.is_contiguous() or color_out.device != self.device):
@@ -373,7 +394,7 @@ class Engine:
     # ------------------------------------------------------ introspection
     def grid(self, n_tiles: int):
         """Sorted instance lists and ranges of the last binning (device)."""
-        m = self.last_m
+        m = self.last_m if self.last_m >= 0 else self.instances()
         return (self.inst_prim[:m], self.inst_tile[:m], self.ranges[:n_tiles])
 
     def n_skew_fallback(self) -> int:

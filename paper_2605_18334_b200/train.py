@@ -231,7 +231,7 @@ class Trainer:
              s: float = 0.3, group=None, check_finite: bool = True):
         """fit2d.py:62-78.  Returns (loss tensor of this rank, frame)."""
         eng, ds, cfg = self.eng, self.ds, self.cfg
-        f = eng.forward(ds, view, s)
+        f = eng.forward(ds, view, s, sync=False)  # M is checked with the loss below
         lossfn = self.loss_for(f.width, f.height)
         dL = lossfn(f.color, target)
         n = ds.n
@@ -240,6 +240,12 @@ class Trainer:
         # the regularizer value is part of the loss (losses.py:146-149); its
         # gradients are folded in after the backward and the statistics
         lossfn.sums[2].zero_()
+        try:
+            eng.instances()
+        except N.NativeError:  # the scene outgrew the instance buffers: redo synchronised
+            f = eng.forward(ds, view, s, sync=True)
+            dL = lossfn(f.color, target)
+            lossfn.sums[2].zero_()
         if check_finite:
             v = lossfn.value_tensor()
             if not math.isfinite(float(v)):  # fit2d.py:70-71: no backward, no update

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import torch
 
+from . import _native as N
 from .engine import DeviceScene, Engine, default_engine
 
 
@@ -34,6 +35,14 @@ def render_views(ds: DeviceScene, views, s: float = 0.3, engine: Engine | None =
         raise ValueError("render_views needs views of one image size")
     if out is None:
         out = torch.empty((len(views), H, W, 3), dtype=torch.float32, device=eng.device)
+    # every frame after the first skips the instance-count read-back, so the
+    # batch runs without host round trips; one check at the end (an
+    # overflowing frame makes the batch re-render synchronised)
     for i, v in enumerate(views):
-        eng.forward(ds, v, s, color_out=out[i])
+        eng.forward(ds, v, s, color_out=out[i], sync=(i == 0))
+    try:
+        eng.instances()
+    except N.NativeError:  # capacity overflow somewhere in the batch: redo with read-backs
+        for i, v in enumerate(views):
+            eng.forward(ds, v, s, color_out=out[i], sync=True)
     return out
