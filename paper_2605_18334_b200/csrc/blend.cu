@@ -56,8 +56,9 @@ struct SmemBatch {
     float D[kBatch];
 };
 
+template <typename S>
 __device__ __forceinline__ void stage_splat(const ssg_splat *splat, uint32_t p, double ox, double oy,
-                                            SmemBatch &s, int slot) {
+                                            S &s, int slot) {
     const double2 m = __ldg(reinterpret_cast<const double2 *>(splat + p));
     const float4 q1 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 1);
     const float4 q2 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 2);
