@@ -265,6 +265,7 @@ def main():
 
     scene, view, dL_host = workload()
     eng = Engine(torch.device("cuda", local))
+    eng.keep_inst_tile = False  # introspection-only output
     ds = DeviceScene.from_host(scene)
     dL = torch.from_numpy(dL_host).cuda().float()
 

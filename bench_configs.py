@@ -75,6 +75,7 @@ def config4(args, rank, world, local):
     views = orbit_views(V4, radius=4.0, elevation=1.2, width=W4, height=H4, fov_x=0.9)
     mine = [views[i] for i in shard_views(V4, rank, world)]
     eng = Engine(torch.device("cuda", local))
+    eng.keep_inst_tile = False  # introspection-only output
     ds = DeviceScene.from_host(scene)
     out = torch.empty((len(mine), H4, W4, 3), dtype=torch.float32, device="cuda")
     pairs = 0
@@ -206,6 +207,7 @@ def config5(args, rank, world, local):
     target_scene = ball_scene(N5, seed=0)
     views = orbit_views(V4, radius=4.0, elevation=1.2, width=W4, height=H4, fov_x=0.9)
     eng = Engine(torch.device("cuda", local))
+    eng.keep_inst_tile = False  # introspection-only output
     tgt_ds = DeviceScene.from_host(target_scene)
     targets = torch.empty((V4, H4, W4, 3), dtype=torch.float32, device="cuda")
     for i, v in enumerate(views):

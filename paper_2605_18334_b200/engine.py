@@ -139,6 +139,9 @@ class Engine:
         self._bin_gen = 0          # bumped by every binning
         self._mask_state = None    # (bin_gen, final_T ptr, last_idx ptr) the blend mask belongs to
         self.blend_mask = None
+        # the sorted tile id per instance is output only for introspection
+        # (grid(), bin_arrays); throughput loops switch it off
+        self.keep_inst_tile = True
         self.stage_events = None  # name -> [(start, end)] CUDA events when enabled
 
     def _mark(self, name: str):
@@ -215,7 +218,8 @@ class Engine:
         b.depth_order, b.rank_offset, b.n_instances = _ptr(self.depth_order), _ptr(self.rank_offset), _ptr(self.n_inst_dev)
         b.capacity = self.capacity
         if self.capacity > 0:
-            b.inst_prim, b.inst_tile = _ptr(self.inst_prim), _ptr(self.inst_tile)
+            b.inst_prim = _ptr(self.inst_prim)
+            b.inst_tile = _ptr(self.inst_tile) if self.keep_inst_tile else None
         if self._bins_key is not None:
             b.ranges, b.temp, b.temp_bytes = _ptr(self.ranges), _ptr(self.temp), self.temp.numel()
         return b
@@ -395,6 +399,8 @@ class Engine:
     def grid(self, n_tiles: int):
         """Sorted instance lists and ranges of the last binning (device)."""
         m = self.last_m if self.last_m >= 0 else self.instances()
+        if not self.keep_inst_tile:
+            raise RuntimeError("this engine does not keep inst_tile (keep_inst_tile = False)")
         return (self.inst_prim[:m], self.inst_tile[:m], self.ranges[:n_tiles])
 
     def n_skew_fallback(self) -> int:

@@ -37,6 +37,7 @@ def main():
         view = frustum_view(a.w, a.h)
     print(f"scene gen {time.time()-t0:.1f}s", flush=True)
     eng = Engine()
+    eng.keep_inst_tile = os.environ.get("KEEP_TILE", "0") == "1"
     ds = DeviceScene.from_host(scene)
     dL = torch.from_numpy(np.random.default_rng(1).normal(size=(a.h, a.w, 3))).cuda().float()
     for rep in range(a.reps):
