@@ -251,11 +251,12 @@ class Engine:
         nn = max(n, 1)
         self.g_screen = self._empty((nn, 12), torch.float32)
         widths = (3, 3, 4, 3 * K, 2, 3, 1)
-        self.g_flat = self._empty((nn * sum(widths),), torch.float32)
+        pad = lambda x: (x + 3) // 4 * 4  # noqa: E731 -- every field 16-byte aligned (float4 access)
+        self.g_flat = self._empty((sum(pad(nn * w) for w in widths),), torch.float32)
         views, off = [], 0
         for w in widths:
             views.append(self.g_flat[off:off + nn * w])
-            off += nn * w
+            off += pad(nn * w)
         self.g_mu = views[0].view(nn, 3)
         self.g_log_scale = views[1].view(nn, 3)
         self.g_rot = views[2].view(nn, 4)
