@@ -358,9 +358,16 @@ def main():
     dom = max(("blend_fwd", "blend_bwd"), key=lambda k: stage_ms.get(k, 0.0))
     t_dom = stage_ms[dom] * 1e-3
     achieved = FP32_PER_PAIR[dom] * pairs / t_dom
-    roofline = {"bound": "fp32", "kernel": f"k_{dom.replace('blend_', 'blend_')}",
+    kname = {"blend_fwd": "k_blend_forward", "blend_bwd": "k_blend_backward"}[dom]
+    try:  # DRAM bytes of the kernel from the committed ncu --set full capture
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(kname)
+    except (OSError, ValueError):
+        traffic = None
+    roofline = {"bound": "fp32", "kernel": kname,
                 "achieved": achieved / 1e12, "peak": r_fp32 / 1e12, "unit": "Tinstr/s (FP32 lane)",
-                "frac": achieved / r_fp32, "traffic": None,
+                "frac": achieved / r_fp32, "traffic": traffic,
+                "traffic_note": "DRAM bytes per launch (profiles/ncu_traffic.json); the blend kernels are "
+                                "issue-bound, DRAM ~1 % busy",
                 "algorithmic": f"{FP32_PER_PAIR[dom]} FP32 instr/pair x {pairs} tile-synchronous "
                                f"pixel-instance pairs per launch (SURVEY.md §8(d))",
                 "mufu_frac": MUFU_PER_PAIR[dom] * pairs / t_dom / r_mufu,
@@ -379,6 +386,13 @@ def main():
             gbs = b / (stage_ms[k_] * 1e-3) / 1e9
             stage_roofline[k_] = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
                                   "frac": gbs / hbm, "bytes": b}
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        stage_roofline.get("preprocess_fwd", {})["traffic"] = tr.get("k_preprocess_forward")
+        if "preprocess_bwd" in stage_roofline:
+            stage_roofline["preprocess_bwd"]["traffic"] = tr.get("k_preprocess_backward", 0) + tr.get("k_sh_backward", 0)
+    except (OSError, ValueError):
+        pass
     t_floor = (FP32_PER_PAIR["blend_fwd"] + FP32_PER_PAIR["blend_bwd"]) * pairs / r_fp32 + \
         sum(stage_bytes.values()) / (hbm * 1e9) + m * 32 / (hbm * 1e9)
 
