@@ -274,7 +274,7 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                  const int32_t *__restrict__ last_idx, const uint32_t *__restrict__ blend_mask,
                  const float *__restrict__ dL, float *__restrict__ grad_screen, float *__restrict__ slots) {
     __shared__ SmemBatch s;
-    __shared__ uint32_t sP[kBatch];
+    __shared__ float4 *sRow[kBatch];  // destination gradient row of each staged instance
     __shared__ int sMax[kThreads / 32];
     const int tile = blockIdx.x;
     const int tyi = tile / ntx, txi = tile - tyi * ntx;
@@ -328,7 +328,10 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
         if ((int)threadIdx.x < cnt) {
             const uint32_t p = inst_prim[lo + threadIdx.x];
             stage_splat(splat, p, ox, oy, s, threadIdx.x);
-            sP[threadIdx.x] = p;
+            // per-primitive accumulator, or (plugin slot mode) the per-instance
+            // (M,12) slot row of _core.pyx:309-312 (raster/backward.py:70-73)
+            sRow[threadIdx.x] = reinterpret_cast<float4 *>(slots ? slots + (size_t)(lo + threadIdx.x) * 12
+                                                                 : grad_screen + (size_t)p * 12);
         }
         __syncthreads();
 
@@ -425,9 +428,7 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                     if ((lane & 7) == 0 && lane < 24) {
                         // per-primitive accumulator, or (plugin slot mode) the
                         // per-instance (M,12) slot row of _core.pyx:309-312
-                        float *row = slots ? slots + (size_t)k * 12 : grad_screen + (size_t)sP[j] * 12;
-                        float4 *dst = reinterpret_cast<float4 *>(row) + (lane >> 3);
-                        atomicAdd(dst, make_float4(v0, v1, v2, v3));
+                        atomicAdd(sRow[j] + (lane >> 3), make_float4(v0, v1, v2, v3));
                     }
                 }
             }
