@@ -355,56 +355,55 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                 mask &= ~(1u << bit);
                 const int j = c0 + bit;
                 const int k = lo + j;
-                float g[12];
-#pragma unroll
-                for (int q = 0; q < 12; q++) g[q] = 0.0f;
-                bool contrib = false;
-                if (k <= li) {  // :263-264
-                    const float4 A = lds128(aA + 16 * j);
-                    const float4 B = lds128(aB + 16 * j);
-                    const float dx = fx - A.x, dy = fy - A.y;
-                    const float power = -0.5f * (A.z * dx * dx + B.x * dy * dy) - A.w * dx * dy;
-                    if (power >= B.y && power <= 0.0f) {
-                        const float4 C = lds128(aC + 16 * j);
-                        const bool skewed = (B.z != 0.0f || B.w != 0.0f);
-                        float E = 1.0f, z = 0.0f, o = C.x;
-                        if (skewed) {
-                            z = (B.z * dx + B.w * dy) * SSG_SQRT1_2;
-                            E = skew_E(z);
-                            o = fmaf(C.y, E - 1.0f, C.x);
-                        }
-                        const float G = fast_exp2(power * SSG_LOG2E);
-                        const float Aval = o * G * E;
-                        const float alpha = fminf(Aval, SSG_ALPHA_MAX);
-                        if (alpha >= SSG_ALPHA_SKIP) {
-                            contrib = true;
-                            const float cb = lds32(aD + 4 * j);
-                            T = T * fast_rcp(1.0f - alpha);                                   // :280
-                            const float d_alpha = T * ((C.z - R0) * d0 + (C.w - R1) * d1 + (cb - R2) * d2);
-                            const float aT = alpha * T;
-                            g[9] = aT * d0;
-                            g[10] = aT * d1;
-                            g[11] = aT * d2;
-                            const float DA = Aval <= SSG_ALPHA_MAX ? d_alpha : 0.0f;          // :290
-                            const float d_power = DA * Aval;
-                            const float Gez2 = skewed ? fast_exp2((power - z * z) * SSG_LOG2E) : G;
-                            const float dzs = DA * SSG_TWO_OVER_SQRT_PI * SSG_SQRT1_2 * Gez2 * fmaf(C.y, E, o);
-                            g[0] = d_power * (A.z * dx + A.w * dy) - dzs * B.z;               // -d_dx
-                            g[1] = d_power * (B.x * dy + A.w * dx) - dzs * B.w;               // -d_dy
-                            g[2] = d_power * (-0.5f * dx * dx);
-                            g[3] = d_power * (-dx * dy);
-                            g[4] = d_power * (-0.5f * dy * dy);
-                            g[5] = dzs * dx;
-                            g[6] = dzs * dy;
-                            const float hGE = 0.5f * DA * G * E;
-                            g[7] = hGE * E;
-                            g[8] = hGE * (2.0f - E);
-                            R0 = alpha * C.z + (1.0f - alpha) * R0;                           // :306-308
-                            R1 = alpha * C.w + (1.0f - alpha) * R1;
-                            R2 = alpha * cb + (1.0f - alpha) * R2;
-                        }
-                    }
+                // Branch-free per lane (every visited instance has a
+                // contributing pixel, so no warp-wide skip is lost): lanes that
+                // do not contribute compute with a zero weight and keep T, R;
+                // contributing lanes run exactly the reference's operations.
+                const float4 A = lds128(aA + 16 * j);
+                const float4 B = lds128(aB + 16 * j);
+                const float4 C = lds128(aC + 16 * j);
+                const float cb = lds32(aD + 4 * j);
+                const float dx = fx - A.x, dy = fy - A.y;
+                const float power = -0.5f * (A.z * dx * dx + B.x * dy * dy) - A.w * dx * dy;
+                const bool live = k <= li && power >= B.y && power <= 0.0f;                // :263-264, :265-269
+                const float pw = fminf(power, 0.0f);   // == power on live lanes; finite exps elsewhere
+                const bool skewed = (B.z != 0.0f || B.w != 0.0f);                          // warp-uniform
+                float E = 1.0f, z = 0.0f, o = C.x;
+                if (skewed) {
+                    z = (B.z * dx + B.w * dy) * SSG_SQRT1_2;
+                    E = skew_E(z);
+                    o = fmaf(C.y, E - 1.0f, C.x);
                 }
+                const float G = fast_exp2(pw * SSG_LOG2E);
+                const float Aval = o * G * E;
+                const float alpha = fminf(Aval, SSG_ALPHA_MAX);
+                const bool contrib = live && alpha >= SSG_ALPHA_SKIP;
+                const float Tn = T * fast_rcp(1.0f - alpha);                                   // :280
+                T = contrib ? Tn : T;
+                const float d_alpha = T * ((C.z - R0) * d0 + (C.w - R1) * d1 + (cb - R2) * d2);
+                const float aT = contrib ? alpha * T : 0.0f;
+                float g[12];
+                g[9] = aT * d0;
+                g[10] = aT * d1;
+                g[11] = aT * d2;
+                const float DA = contrib && Aval <= SSG_ALPHA_MAX ? d_alpha : 0.0f;            // :290
+                const float d_power = DA * Aval;
+                const float Gez2 = skewed ? fast_exp2((pw - z * z) * SSG_LOG2E) : G;
+                const float dzs = DA * SSG_TWO_OVER_SQRT_PI * SSG_SQRT1_2 * Gez2 * fmaf(C.y, E, o);
+                g[0] = d_power * (A.z * dx + A.w * dy) - dzs * B.z;                           // -d_dx
+                g[1] = d_power * (B.x * dy + A.w * dx) - dzs * B.w;                           // -d_dy
+                g[2] = d_power * (-0.5f * dx * dx);
+                g[3] = d_power * (-dx * dy);
+                g[4] = d_power * (-0.5f * dy * dy);
+                g[5] = dzs * dx;
+                g[6] = dzs * dy;
+                const float hGE = 0.5f * DA * G * E;
+                g[7] = hGE * E;
+                g[8] = hGE * (2.0f - E);
+                const float ae = contrib ? alpha : 0.0f;                                       // :306-308
+                R0 = ae * C.z + (1.0f - ae) * R0;
+                R1 = ae * C.w + (1.0f - ae) * R1;
+                R2 = ae * cb + (1.0f - ae) * R2;
 #ifdef SSG_BLEND_STATS
                 {
                     const unsigned cbal = __ballot_sync(0xffffffffu, contrib);
