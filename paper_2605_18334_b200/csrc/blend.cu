@@ -366,6 +366,7 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                 const float dx = fx - A.x, dy = fy - A.y;
                 const float power = -0.5f * (A.z * dx * dx + B.x * dy * dy) - A.w * dx * dy;
                 const bool live = k <= li && power >= B.y && power <= 0.0f;                // :263-264, :265-269
+                if (!blend_mask && !__any_sync(0xffffffffu, live)) continue;  // test-driven walk: empty hit
                 const float pw = fminf(power, 0.0f);   // == power on live lanes; finite exps elsewhere
                 const bool skewed = (B.z != 0.0f || B.w != 0.0f);                          // warp-uniform
                 float E = 1.0f, z = 0.0f, o = C.x;
