@@ -174,40 +174,40 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
                 const int bit = __ffs(mask) - 1;
                 mask &= mask - 1;
                 const int j = c0 + bit;
-                if (!done) {
-                    const float4 A = lds128(aA + 16 * j);
-                    const float4 B = lds128(aB + 16 * j);
-                    const float dx = fx - A.x, dy = fy - A.y;
-                    // _core.pyx:133-135
-                    const float power = -0.5f * (A.z * dx * dx + B.x * dy * dy) - A.w * dx * dy;
-                    if (power >= B.y && power <= 0.0f) {
-                        const float4 C = lds128(aC + 16 * j);
-                        float E = 1.0f, o = C.x;
-                        if (!kVanilla && (B.z != 0.0f || B.w != 0.0f)) {     // warp-uniform
-                            const float z = (B.z * dx + B.w * dy) * SSG_SQRT1_2;   // :136
-                            E = skew_E(z);                                          // :137
-                            o = fmaf(C.y, E - 1.0f, C.x);                           // :138
-                        }
-                        const float Aval = kVanilla ? o * fast_exp2(power * SSG_LOG2E)
-                                                    : o * fast_exp2(power * SSG_LOG2E) * E;   // :139
-                        const float alpha = fminf(Aval, SSG_ALPHA_MAX);             // :140
-                        if (alpha >= SSG_ALPHA_SKIP) {                              // :141-142
-                            const float test_T = T * (1.0f - alpha);                // :143
-                            if (test_T < SSG_T_STOP) {                              // :144-147
-                                done = 1;
-                            } else {                                                // :148-154
-                                const float w = alpha * T;
-                                C0 = fmaf(w, C.z, C0);
-                                C1 = fmaf(w, C.w, C1);
-                                C2 = fmaf(w, lds32(aD + 4 * j), C2);
-                                T = test_T;
-                                nc++;
-                                li = base + j;
-                                lbits |= 1u << bit;
-                            }
-                        }
-                    }
+                // branch-free per lane (the warp skips an instance no live
+                // pixel can blend); blending lanes run exactly the
+                // reference's operations, the others carry zero weight
+                const float4 A = lds128(aA + 16 * j);
+                const float4 B = lds128(aB + 16 * j);
+                const float dx = fx - A.x, dy = fy - A.y;
+                const float power = -0.5f * (A.z * dx * dx + B.x * dy * dy) - A.w * dx * dy;   // :133-135
+                const bool live = !done && power >= B.y && power <= 0.0f;
+                if (!__any_sync(0xffffffffu, live)) continue;
+                const float4 C = lds128(aC + 16 * j);
+                const float cb = lds32(aD + 4 * j);
+                float E = 1.0f, o = C.x;
+                if (!kVanilla && (B.z != 0.0f || B.w != 0.0f)) {     // warp-uniform
+                    const float z = (B.z * dx + B.w * dy) * SSG_SQRT1_2;   // :136
+                    E = skew_E(z);                                          // :137
+                    o = fmaf(C.y, E - 1.0f, C.x);                           // :138
                 }
+                const float pw = fminf(power, 0.0f);
+                const float Aval = kVanilla ? o * fast_exp2(pw * SSG_LOG2E)
+                                            : o * fast_exp2(pw * SSG_LOG2E) * E;      // :139
+                const float alpha = fminf(Aval, SSG_ALPHA_MAX);                         // :140
+                const bool pass = live && alpha >= SSG_ALPHA_SKIP;                     // :141-142
+                const float test_T = T * (1.0f - alpha);                                // :143
+                const bool stop = pass && test_T < SSG_T_STOP;                          // :144-147
+                const bool blend = pass && !stop;                                       // :148-154
+                done |= stop;
+                const float w = blend ? alpha * T : 0.0f;
+                C0 = fmaf(w, C.z, C0);
+                C1 = fmaf(w, C.w, C1);
+                C2 = fmaf(w, cb, C2);
+                T = blend ? test_T : T;
+                nc += blend;
+                li = blend ? base + j : li;
+                lbits |= (uint32_t)blend << bit;
             }
             if (blend_mask) {
                 const uint32_t bmask = __reduce_or_sync(0xffffffffu, lbits);
