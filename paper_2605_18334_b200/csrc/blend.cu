@@ -125,7 +125,7 @@ __device__ __forceinline__ size_t mask_word(int start, int tile, int chunk, int 
 #define SSG_FWD_MINB 5
 #endif
 #ifndef SSG_BWD_MINB
-#define SSG_BWD_MINB 4
+#define SSG_BWD_MINB 5
 #endif
 
 template <bool kVanilla>
