@@ -41,11 +41,11 @@ METRIC = "fwd+bwd raster ms/frame, 1M skew Gaussians @1080p; views/s at 1/2/4/8 
 # kernels): preprocess_fwd 1; depth sort + count scan 1 (cooperative);
 # two-level counting scatter 8 (rows: count, rowscan, rowstart, scatter;
 # tiles: count, tilescan, tilestart, scatter); blend_fwd 1; blend_bwd 1;
-# preprocess_bwd + sh_backward 2.
-LAUNCHES_PER_FRAME = 14
+# preprocess_bwd 1 (geometry + SH chain fused).
+LAUNCHES_PER_FRAME = 13
 LAUNCHES_NOTE = ("per frame: k_preprocess_forward 1, k_depth_sort 1, k_cs1_{count,rowscan,rowstart,scatter} 4, "
                  "k_cs2_{count,tilescan,tilestart,scatter} 4, k_blend_forward 1, k_blend_backward 1, "
-                 "k_preprocess_backward + k_sh_backward 2; no library kernels (cudaMemsetAsync excluded)")
+                 "k_preprocess_backward 1; no library kernels (cudaMemsetAsync excluded)")
 UNIT = "views/s"
 N_PRIM, WIDTH, HEIGHT = 1_000_000, 1920, 1080
 # per-pair algorithmic instruction counts (fixed, not tuned)

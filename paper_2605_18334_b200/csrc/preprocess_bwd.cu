@@ -67,11 +67,10 @@ __device__ __forceinline__ void sh_dot_grad_f(int deg, float x, float y, float z
 #define SSG_PB_MINB 4
 #endif
 
-// Geometry part: everything but the SH chain (run first; writes d_mu).
-__global__ void __launch_bounds__(128, SSG_PB_MINB)
-k_preprocess_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= sc.n) return;
+// Geometry part of one primitive: every output but d_sh; the geometric
+// d_mu is returned (the SH chain adds its view-direction term).
+__device__ __forceinline__ void prep_geom(const ssg_scene &sc, const ssg_camera &cam, const ssg_grad_buffers &gr,
+                                          int64_t i, float *dmu_out) {
     const float4 *sg4 = reinterpret_cast<const float4 *>(gr.screen + 12 * i);
     const float4 s0 = sg4[0], s1 = sg4[1], s2 = sg4[2];
     const bool zero = s0.x == 0.0f && s0.y == 0.0f && s0.z == 0.0f && s0.w == 0.0f && s1.x == 0.0f &&
@@ -79,7 +78,7 @@ k_preprocess_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
                       s2.z == 0.0f && s2.w == 0.0f;
     if (zero) {  // no instance touched a pixel with dL != 0: every output is 0
 #pragma unroll
-        for (int j = 0; j < 3; j++) gr.d_mu[3 * i + j] = gr.d_log_scale[3 * i + j] = gr.d_eta[3 * i + j] = 0.0f;
+        for (int j = 0; j < 3; j++) dmu_out[j] = gr.d_log_scale[3 * i + j] = gr.d_eta[3 * i + j] = 0.0f;
 #pragma unroll
         for (int j = 0; j < 4; j++) gr.d_rot[4 * i + j] = 0.0f;
         gr.d_opacity_logits[2 * i] = gr.d_opacity_logits[2 * i + 1] = 0.0f;
@@ -104,7 +103,7 @@ k_preprocess_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
 
     if (!P.valid) {  // zero_invalid, projection.py:368-379; g_z -> 0 (:349)
 #pragma unroll
-        for (int j = 0; j < 3; j++) gr.d_mu[3 * i + j] = gr.d_log_scale[3 * i + j] = gr.d_eta[3 * i + j] = 0.0f;
+        for (int j = 0; j < 3; j++) dmu_out[j] = gr.d_log_scale[3 * i + j] = gr.d_eta[3 * i + j] = 0.0f;
 #pragma unroll
         for (int j = 0; j < 4; j++) gr.d_rot[4 * i + j] = 0.0f;
         gr.d_opacity_logits[2 * i] = gr.d_opacity_logits[2 * i + 1] = 0.0f;
@@ -261,21 +260,24 @@ k_preprocess_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
 
 #pragma unroll
     for (int j = 0; j < 3; j++) {
-        gr.d_mu[3 * i + j] = (float)dmu[j];
+        dmu_out[j] = (float)dmu[j];
         gr.d_eta[3 * i + j] = (float)geta[j];                               // :365-366
     }
 }
 
 
-// SH part (projection.py:355-363, sh.py:25-109): d_sh = basis (x) dcolor on
-// the unclamped channels, plus the view-direction term added into d_mu.  A
-// warp stages its 32 primitives' coefficient rows (3K floats each) through
-// shared memory so global loads and stores are fully coalesced float4s.  An
+// One kernel for the whole projection backward.  A warp owns 32 consecutive
+// primitives: it stages their SH coefficient rows (3K floats each) through
+// shared memory with coalesced float4 loads, every lane runs the fp64
+// geometry chain of its primitive (prep_geom) while the rows are in flight,
+// then the SH part (projection.py:355-363, sh.py:25-109): d_sh = basis (x)
+// dcolor on the unclamped channels, written back through the same staging,
+// and the view-direction term folded into d_mu before its single store.  An
 // invalid primitive has no tile instances, so its screen gradients are zero
 // and so are its outputs (zero_invalid, projection.py:368-379).
 template <int DEG>
-__global__ void __launch_bounds__(128)
-k_sh_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
+__global__ void __launch_bounds__(128, SSG_PB_MINB)
+k_preprocess_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
     constexpr int K = (DEG + 1) * (DEG + 1);
     constexpr int ROW = 3 * K;                 // floats per primitive
     __shared__ __align__(16) float tile[4][32 * ROW];
@@ -293,6 +295,8 @@ k_sh_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
     }
     __syncwarp();
     const int64_t i = first + lane;
+    float dmu[3] = {0.0f, 0.0f, 0.0f};
+    if (lane < nw) prep_geom(sc, cam, gr, i, dmu);  // fp64 geometry while the rows sit in smem
     if (lane < nw) {
         const float *sh = t + lane * ROW;
         const float *sg = gr.screen + 12 * i;
@@ -328,10 +332,12 @@ k_sh_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
         if (DEG > 0) {
             const float inner = x * dd[0] + y * dd[1] + z * dd[2];
             const float rdn = (float)(1.0 / dns);
-            gr.d_mu[3 * i] += (dd[0] - x * inner) * rdn;
-            gr.d_mu[3 * i + 1] += (dd[1] - y * inner) * rdn;
-            gr.d_mu[3 * i + 2] += (dd[2] - z * inner) * rdn;
+            dmu[0] += (dd[0] - x * inner) * rdn;
+            dmu[1] += (dd[1] - y * inner) * rdn;
+            dmu[2] += (dd[2] - z * inner) * rdn;
         }
+#pragma unroll
+        for (int j = 0; j < 3; j++) gr.d_mu[3 * i + j] = dmu[j];
     }
     __syncwarp();
     float *dst = gr.d_sh + first * ROW;
@@ -353,14 +359,11 @@ extern "C" int ssg_preprocess_backward(const ssg_scene *scene, const ssg_camera 
     if (scene->n == 0) return SSG_OK;
     cudaStream_t st = (cudaStream_t)stream;
     unsigned blocks = (unsigned)((scene->n + 127) / 128);
-    k_preprocess_backward<<<blocks, 128, 0, st>>>(*scene, *cam, *grads);
-    int rc = check_launch("k_preprocess_backward");
-    if (rc != SSG_OK) return rc;
     switch (scene->sh_degree) {
-        case 0: k_sh_backward<0><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
-        case 1: k_sh_backward<1><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
-        case 2: k_sh_backward<2><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
-        default: k_sh_backward<3><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
+        case 0: k_preprocess_backward<0><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
+        case 1: k_preprocess_backward<1><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
+        case 2: k_preprocess_backward<2><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
+        default: k_preprocess_backward<3><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
     }
-    return check_launch("k_sh_backward");
+    return check_launch("k_preprocess_backward");
 }
