@@ -89,6 +89,19 @@ def _stream(dev) -> int:
     return torch.cuda.current_stream(dev).cuda_stream
 
 
+def _world(group=None) -> int:
+    return dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+
+
+def any_rank(flag: bool, group=None, device=None) -> bool:
+    """True on every rank when `flag` is true on any rank (MAX all-reduce)."""
+    if _world(group) == 1:
+        return bool(flag)
+    t = torch.tensor([1.0 if flag else 0.0], device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return bool(t.item() > 0)
+
+
 def allreduce_gradients(grads: DeviceGrads, group=None) -> None:
     """SUM of the packed gradient buffer, MAX of g_z (one call each)."""
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
@@ -248,13 +261,15 @@ class Trainer:
             lossfn.sums[2].zero_()
         if check_finite:
             v = lossfn.value_tensor()
-            if not math.isfinite(float(v)):  # fit2d.py:70-71: no backward, no update
+            # every rank must take the same branch (the all-reduce below is
+            # collective): the step is skipped when any rank's view diverged
+            bad = any_rank(not math.isfinite(float(v)), group, eng.device)
+            if bad:  # fit2d.py:70-71: no backward, no update
                 return v, f
         grads = eng.backward(ds, view, s, f.final_T, f.last_idx, dL, rebin=False)
         allreduce_gradients(grads, group)
         if stats is not None:
-            world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
-            stats.add(grads, views=world)
+            stats.add(grads, views=_world(group))
         N.check(N.lib().ssg_regularize(n, ds.beta.data_ptr(), ds.opacity_logits.data_ptr(), grads.d_eta.data_ptr(),
                                        cfg.lambda_beta_reg, cfg.lambda_opacity_reg, self.d_beta.data_ptr(),
                                        grads.d_opacity_logits.data_ptr(), lossfn.sums.data_ptr(),

@@ -11,7 +11,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2605_18334_b200.engine import DeviceGrads
-from paper_2605_18334_b200.train import allreduce_gradients
+from paper_2605_18334_b200.train import allreduce_gradients, any_rank
 from paper_2605_18334_b200.views import shard_views
 
 
@@ -83,3 +83,27 @@ def test_shard_views_partitions(n, world):
     assert flat == list(range(n))
     sizes = [len(p) for p in parts]
     assert max(sizes) - min(sizes) <= 1
+
+
+def _worker_any(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # the training step's finite-loss decision is collective: one diverged
+    # view makes every rank skip the step (no rank waits in the all-reduce)
+    q.put((rank, any_rank(rank == 1), any_rank(False)))
+    dist.destroy_process_group()
+
+
+def test_any_rank_decision_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_any, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r[0] for r in res) == [0, 1]
+    assert all(r[1] is True and r[2] is False for r in res)
