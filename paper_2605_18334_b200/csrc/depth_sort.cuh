@@ -12,13 +12,18 @@
 //             (no-instance keys map to ~0), nbits = significant bits of the
 //             largest k'
 //   passes    LSD over the top kWindow (24) significant bits only (3 byte
-//             digits):
-//             A: per-tile digit counts -> tile_counts[digit][tile]
-//             B: exclusive scan of each digit row over the tiles (row totals
-//                -> bucket bases)
-//             C: stable in-tile ranking (warp-striped, match_any per step),
-//                tile reordered by digit in shared memory, written out in
-//                digit runs (coalesced)
+//             digits), one grid barrier per pass:
+//             counts  per-(tile, digit) counts of the pass, tile_counts
+//                     [pass][tile][digit]: pass 0 from a shared-memory
+//                     histogram of each tile; pass k+1 accumulated by pass k's
+//                     scatter (one global reduction per key, into the tile the
+//                     key lands in)
+//             prefix  every CTA sums the count table itself: digit totals
+//                     (-> bucket bases) and the counts of the tiles before
+//                     its own (-> the tile's run starts); no scan phase
+//             scatter stable in-tile ranking (warp-striped, match_any per
+//                     step), tile reordered by digit in shared memory,
+//                     written out in digit runs (coalesced)
 //   fix-up    runs of keys equal in those 24 bits but out of order in the low
 //             bits (1 part in 2^24 of the depth range: rare, short) are
 //             insertion-sorted by the full key, stably; runs without an inversion (exact ties,
@@ -58,17 +63,20 @@ struct Ctl {
     unsigned long long kmin, kmax;            // range of the valid keys
     uint32_t long_run;                        // fix-up found a run > kFixMax
     uint32_t pad;
-    uint32_t rowtot[256];                     // keys with each digit (current pass)
 };
 
 constexpr int kFixMax = 32;
+constexpr unsigned long long kReady = 1ull << 63;  // tile_sums flag (final phase)
+constexpr int kMaxPasses = 8;                 // 64-bit keys, byte digits
+constexpr int kSub = kThreads / 256;          // threads per digit in the prefix sums
+static_assert(kThreads % 256 == 0, "prefix sums map 256 digits x kSub threads");
 
 __host__ __device__ inline int64_t num_tiles(int64_t n) { return (n + kTile - 1) / kTile; }
 
-// temp = [Ctl | tile_counts 256 x tiles | tile_sums tiles | keys x2 | vals x1]
+// temp = [Ctl | tile_counts passes x tiles x 256 | tile_sums tiles | keys x2 | vals x1]
 inline size_t temp_bytes(int64_t n) {
     const int64_t nt = num_tiles(n > 0 ? n : 1);
-    return radix::align256(sizeof(Ctl)) + radix::align256(sizeof(uint32_t) * 256 * nt) +
+    return radix::align256(sizeof(Ctl)) + radix::align256(sizeof(uint32_t) * kMaxPasses * 256 * nt) +
            radix::align256(sizeof(uint64_t) * nt) + 2 * radix::align256(sizeof(uint64_t) * n) +
            radix::align256(sizeof(uint32_t) * n);
 }
@@ -81,7 +89,7 @@ struct Args {
     int64_t *n_instances;         // (2): [0] M, [1] running max of M (caller-reset)
     int64_t n;
     Ctl *ctl;
-    uint32_t *tile_counts;        // [256][ntiles]
+    uint32_t *tile_counts;        // [kMaxPasses][ntiles][256]
     uint64_t *tile_sums;          // [ntiles]
     uint64_t *keys_a, *keys_b;    // ping-pong keys
     uint32_t *vals_a;             // ping-pong values (the other buffer is order_out)
@@ -94,6 +102,7 @@ struct Smem {
     uint32_t base[256];           // bucket base of the current pass
     uint32_t tstart[256];         // tile-local start of each digit run
     uint32_t excl[256];           // global start of this tile's digit run
+    uint32_t red[2][kSub][256];   // prefix sums: partial (before tile, total) per sub-thread
     uint32_t swarp[kWarps];
     uint64_t sum64[kWarps];
     unsigned long long kmin, kmax;
@@ -163,6 +172,16 @@ static __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_depth_sort
         atomicMin(&a.ctl->kmin, s.kmin);
         atomicMax(&a.ctl->kmax, s.kmax);
     }
+    const size_t slot = (size_t)ntiles * 256;       // one pass's count table
+    // zero the count tables of passes 1.. (pass 0's is stored, not accumulated)
+    auto zero_counts = [&]() {
+        for (size_t q = (size_t)blockIdx.x * kThreads + t + slot; q < kMaxPasses * slot;
+             q += (size_t)gridDim.x * kThreads)
+            a.tile_counts[q] = 0u;
+    };
+    zero_counts();
+    for (int64_t q = (int64_t)blockIdx.x * kThreads + t; q < ntiles; q += (int64_t)gridDim.x * kThreads)
+        a.tile_sums[q] = 0ull;
     grid.sync();
     const uint64_t kmin = *((volatile unsigned long long *)&a.ctl->kmin);
     const uint64_t kmax = *((volatile unsigned long long *)&a.ctl->kmax);
@@ -172,6 +191,27 @@ static __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_depth_sort
 
     // ---------------------------------------------------------- passes
     auto run_passes = [&](int np, int shift0) {
+        // pass 0 counts: shared-memory histogram per tile
+        if (np > 0) {
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                if (t < 256) s.base[t] = 0u;
+                __syncthreads();
+                const int64_t base = tile * kTile;
+#pragma unroll
+                for (int i = 0; i < kIPT; i++) {
+                    const int64_t idx = base + (int64_t)i * kThreads + t;
+                    if (idx < n) {
+                        const uint64_t kk = a.keys_in[idx];
+                        const uint64_t kr = kk == kInvalid ? ~0ull : kk - kmin;
+                        atomicAdd(&s.base[(uint32_t)(kr >> shift0) & 255u], 1u);
+                    }
+                }
+                __syncthreads();
+                if (t < 256) a.tile_counts[(size_t)tile * 256 + t] = s.base[t];
+                __syncthreads();
+            }
+            grid.sync();
+        }
         for (int k = 0; k < np; k++) {
             const int shift = shift0 + 8 * k;
             const uint64_t *kin = (k & 1) ? a.keys_a : a.keys_b;  // k == 0 reads keys_in (rebased)
@@ -180,57 +220,44 @@ static __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_depth_sort
             // (np - 1 - k) is even; pass 0 generates the ids
             uint32_t *vout = ((np - 1 - k) & 1) ? a.vals_a : a.order_out;
             const uint32_t *vin = k == 0 ? nullptr : (((np - k) & 1) ? a.vals_a : a.order_out);
+            const uint32_t *cnt = a.tile_counts + (size_t)k * slot;
+            uint32_t *cnext = k + 1 < np ? a.tile_counts + (size_t)(k + 1) * slot : nullptr;
             auto load_key = [&](int64_t idx) -> uint64_t {
                 if (k > 0) return kin[idx];
                 const uint64_t kk = a.keys_in[idx];
                 return kk == kInvalid ? ~0ull : kk - kmin;
             };
 
-            // A: per-tile digit counts
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int q = t; q < kWarps * 256; q += kThreads) (&s.wcnt[0][0])[q] = 0;
-                __syncthreads();
-                const int64_t base = tile * kTile;
+                // prefix sums over the count table: digit totals (first tile
+                // only; -> bucket bases) and counts of the tiles before this one
+                {
+                    const int d = t & 255, j = t >> 8;
+                    const bool first = tile == blockIdx.x;
+                    const int64_t qend = first ? ntiles : tile;
+                    uint32_t pre = 0, tot = 0;
+#pragma unroll 4
+                    for (int64_t q = j; q < qend; q += kSub) {
+                        const uint32_t c = __ldcg(cnt + (size_t)q * 256 + d);
+                        tot += c;
+                        pre += q < tile ? c : 0u;
+                    }
+                    s.red[0][j][d] = pre;
+                    s.red[1][j][d] = tot;
+                    __syncthreads();
+                    if (t < 256) {
+                        uint32_t p = 0, tt = 0;
 #pragma unroll
-                for (int i = 0; i < kIPT; i++) {
-                    const int64_t idx = base + w * (32 * kIPT) + i * 32 + lane;
-                    const uint32_t d = idx < n ? ((uint32_t)(load_key(idx) >> shift) & 255u) : 256u;
-                    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-                    if (d < 256u && (peers & lt) == 0) s.wcnt[w][d] += __popc(peers);
-                    __syncwarp();
+                        for (int q = 0; q < kSub; q++) {
+                            p += s.red[0][q][t];
+                            tt += s.red[1][q][t];
+                        }
+                        s.excl[t] = p;
+                        if (first) s.wcnt[0][t] = tt;
+                    }
+                    __syncthreads();
+                    if (first) scan256(s.wcnt[0], s.base, s.swarp);  // bucket bases of this pass
                 }
-                __syncthreads();
-                if (t < 256) {
-                    uint32_t c = 0;
-#pragma unroll 8
-                    for (int ww = 0; ww < kWarps; ww++) c += s.wcnt[ww][t];
-                    a.tile_counts[(size_t)t * ntiles + tile] = c;
-                }
-                __syncthreads();
-            }
-            grid.sync();
-
-            // B: exclusive scan of each digit row over the tiles (a warp per row)
-            for (int d = blockIdx.x * kWarps + w; d < 256; d += gridDim.x * kWarps) {
-                uint32_t *row = a.tile_counts + (size_t)d * ntiles;
-                uint32_t carry = 0;
-                for (int64_t c0 = 0; c0 < ntiles; c0 += 32) {
-                    const int64_t i = c0 + lane;
-                    const uint32_t v = i < ntiles ? row[i] : 0u;
-                    const uint32_t x = warp_incl_scan(v, lane);
-                    if (i < ntiles) row[i] = carry + x - v;
-                    carry += __shfl_sync(0xffffffffu, x, 31);
-                }
-                if (lane == 0) a.ctl->rowtot[d] = carry;
-            }
-            grid.sync();
-            // bucket bases of this pass (every CTA)
-            if (t < 256) s.wcnt[0][t] = *((volatile uint32_t *)&a.ctl->rowtot[t]);
-            __syncthreads();
-            scan256(s.wcnt[0], s.base, s.swarp);
-
-            // C: stable scatter
-            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int q = t; q < kWarps * 256; q += kThreads) (&s.wcnt[0][0])[q] = 0;
                 __syncthreads();
                 const int64_t base = tile * kTile;
@@ -264,7 +291,7 @@ static __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_depth_sort
                         s.wcnt[ww][t] = run;
                         run += c;
                     }
-                    s.excl[t] = s.base[t] + a.tile_counts[(size_t)t * ntiles + tile];
+                    s.excl[t] += s.base[t];
                     s.tstart[t] = run;  // tile count, scanned below
                 }
                 __syncthreads();
@@ -284,6 +311,8 @@ static __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_depth_sort
                     const uint32_t dest = s.excl[d] + (uint32_t)p - s.tstart[d];
                     kout[dest] = kk;
                     vout[dest] = s.vals[p];
+                    // next pass's count of (destination tile, next digit)
+                    if (cnext) atomicAdd(cnext + (size_t)(dest / kTile) * 256 + ((uint32_t)(kk >> (shift + 8)) & 255u), 1u);
                 }
                 __syncthreads();
             }
@@ -341,48 +370,20 @@ static __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_depth_sort
         grid.sync();
         if (*((volatile uint32_t *)&a.ctl->long_run)) {
             // exact fallback: full LSD over every significant byte
+            zero_counts();
+            grid.sync();
             run_passes((nbits + 7) / 8, 0);
         }
     }
     if (!a.count) return;
 
     // ---------------------------------------------------------- final
-    // counts in depth order; rank_offset[r+1] = sum of counts of ranks <= r
+    // counts in depth order; rank_offset[r+1] = sum of counts of ranks <= r.
+    // One pass: each tile publishes its sum with a ready flag (bit 63) and
+    // adds the sums of the tiles before it as they appear.  Every CTA is
+    // resident and walks its tiles in increasing order, so the lowest
+    // unfinished tile never waits.
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t base = tile * kTile;
-        uint64_t sum = 0;
-#pragma unroll
-        for (int i = 0; i < kIPT; i++) {
-            const int64_t r = base + (int64_t)t * kIPT + i;
-            if (r < n) sum += a.count[a.order_out[r]];
-        }
-        uint64_t x = sum;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const uint64_t y = __shfl_up_sync(0xffffffffu, x, off);
-            if (lane >= off) x += y;
-        }
-        if (lane == 31) s.sum64[w] = x;
-        __syncthreads();
-        if (t == 0) {
-            uint64_t tot = 0;
-            for (int ww = 0; ww < kWarps; ww++) tot += s.sum64[ww];
-            a.tile_sums[tile] = tot;
-        }
-        __syncthreads();
-    }
-    grid.sync();
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        // prefix of the earlier tiles (ntiles is small: a strided block sum)
-        uint64_t pre = 0;
-        for (int64_t q = t; q < tile; q += kThreads) pre += a.tile_sums[q];
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, off);
-        if (lane == 0) s.sum64[w] = pre;
-        __syncthreads();
-        uint64_t tile_pre = 0;
-        for (int ww = 0; ww < kWarps; ww++) tile_pre += s.sum64[ww];
-        __syncthreads();
         const int64_t base = tile * kTile;
         uint64_t v[kIPT], sum = 0;
 #pragma unroll
@@ -399,8 +400,32 @@ static __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_depth_sort
         }
         if (lane == 31) s.sum64[w] = x;
         __syncthreads();
-        uint64_t wpre = 0;
-        for (int ww = 0; ww < w; ww++) wpre += s.sum64[ww];
+        uint64_t wpre = 0, tot = 0;
+        for (int ww = 0; ww < kWarps; ww++) {
+            const uint64_t c = s.sum64[ww];
+            wpre += ww < w ? c : 0u;
+            tot += c;
+        }
+        if (t == 0) {
+            __threadfence();
+            *((volatile unsigned long long *)&a.tile_sums[tile]) = (unsigned long long)(tot | kReady);
+        }
+        // prefix of the earlier tiles
+        uint64_t pre = 0;
+        for (int64_t q = t; q < tile; q += kThreads) {
+            unsigned long long f;
+            do {
+                f = *((volatile unsigned long long *)&a.tile_sums[q]);
+            } while (!(f & kReady));
+            pre += f & ~kReady;
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, off);
+        __syncthreads();  // sum64 reads done
+        if (lane == 0) s.sum64[w] = pre;
+        __syncthreads();
+        uint64_t tile_pre = 0;
+        for (int ww = 0; ww < kWarps; ww++) tile_pre += s.sum64[ww];
         uint64_t run = tile_pre + wpre + x - sum;
 #pragma unroll
         for (int i = 0; i < kIPT; i++) {
@@ -434,7 +459,7 @@ static inline cudaError_t sort_and_scan(const uint64_t *keys, uint32_t *order, c
     a.ctl = (Ctl *)tp;
     tp += radix::align256(sizeof(Ctl));
     a.tile_counts = (uint32_t *)tp;
-    tp += radix::align256(sizeof(uint32_t) * 256 * nt);
+    tp += radix::align256(sizeof(uint32_t) * kMaxPasses * 256 * nt);
     a.tile_sums = (uint64_t *)tp;
     tp += radix::align256(sizeof(uint64_t) * nt);
     a.keys_a = (uint64_t *)tp;
