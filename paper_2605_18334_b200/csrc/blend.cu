@@ -284,6 +284,9 @@ __device__ __forceinline__ int comp_lane(int c) {
     return 8 * g + 2 * (c - 3 * g);
 }
 
+// d_z * SQRT1_2 of _core.pyx:293-302 (d_z = DA G (2/sqrt(pi)) e^-z^2 (o + (o1-o2)E/2))
+constexpr float kDzScale = SSG_TWO_OVER_SQRT_PI * SSG_SQRT1_2;
+
 __global__ void __launch_bounds__(kThreads, SSG_BWD_MINB)
 k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float bg2,
                  const ssg_splat *__restrict__ splat, const uint32_t *__restrict__ inst_prim,
@@ -400,7 +403,8 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                 const bool contrib = live && alpha >= SSG_ALPHA_SKIP;
                 const float Tn = T * fast_rcp(1.0f - alpha);                                   // :280
                 T = contrib ? Tn : T;
-                const float d_alpha = T * ((C.z - R0) * d0 + (C.w - R1) * d1 + (cb - R2) * d2);
+                const float e0 = C.z - R0, e1 = C.w - R1, e2 = cb - R2;
+                const float d_alpha = T * (e0 * d0 + e1 * d1 + e2 * d2);
                 const float aT = contrib ? alpha * T : 0.0f;
                 float g[12];
                 g[9] = aT * d0;
@@ -409,21 +413,22 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                 const float DA = contrib && Aval <= SSG_ALPHA_MAX ? d_alpha : 0.0f;            // :290
                 const float d_power = DA * Aval;
                 const float Gez2 = skewed ? fast_exp2((pw - z * z) * SSG_LOG2E) : G;
-                const float dzs = DA * SSG_TWO_OVER_SQRT_PI * SSG_SQRT1_2 * Gez2 * fmaf(C.y, E, o);
-                g[0] = d_power * (A.z * dx + A.w * dy) - dzs * B.z;                           // -d_dx
-                g[1] = d_power * (B.x * dy + A.w * dx) - dzs * B.w;                           // -d_dy
-                g[2] = d_power * (-0.5f * dx * dx);
-                g[3] = d_power * (-dx * dy);
-                g[4] = d_power * (-0.5f * dy * dy);
+                const float dzs = (DA * kDzScale) * Gez2 * fmaf(C.y, E, o);
+                const float px_ = d_power * dx, py_ = d_power * dy;
+                g[0] = fmaf(A.z, px_, fmaf(A.w, py_, -dzs * B.z));                           // -d_dx
+                g[1] = fmaf(B.x, py_, fmaf(A.w, px_, -dzs * B.w));                           // -d_dy
+                g[2] = -0.5f * px_ * dx;
+                g[3] = -px_ * dy;
+                g[4] = -0.5f * py_ * dy;
                 g[5] = dzs * dx;
                 g[6] = dzs * dy;
                 const float hGE = 0.5f * DA * G * E;
                 g[7] = hGE * E;
                 g[8] = hGE * (2.0f - E);
                 const float ae = contrib ? alpha : 0.0f;                                       // :306-308
-                R0 = ae * C.z + (1.0f - ae) * R0;
-                R1 = ae * C.w + (1.0f - ae) * R1;
-                R2 = ae * cb + (1.0f - ae) * R2;
+                R0 = fmaf(ae, e0, R0);
+                R1 = fmaf(ae, e1, R1);
+                R2 = fmaf(ae, e2, R2);
 #ifdef SSG_BLEND_STATS
                 {
                     const unsigned cbal = __ballot_sync(0xffffffffu, contrib);
