@@ -18,9 +18,11 @@
 // are exactly those of the unculled loop; it removes the pixel-instance pairs
 // that cannot contribute before any arithmetic is spent on them.
 // Backward: the 12 per-instance sums of a warp are reduced with a transposed
-// butterfly (16 shuffles instead of 60) and added to the primitive's
-// gradient row with three float4 global reductions (sm_90+ vector REDs; the
-// shared-memory fp32 atomic on sm_100 is a CAS loop, so no smem staging).
+// butterfly (13 shuffles instead of 60) and added to the primitive's
+// gradient row by the 12 lanes holding them, one scalar global reduction
+// each (one RED instruction; measured 2.4 % faster than gathering them into
+// three float4 vector REDs; the shared-memory fp32 atomic on sm_100 is a CAS
+// loop, so no smem staging).
 #include "ssg_common.cuh"
 
 #ifdef SSG_BLEND_STATS
@@ -278,12 +280,6 @@ __device__ __forceinline__ float warp_reduce_transposed12(float (&v)[12], int la
     return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
-// lane holding component c after warp_reduce_transposed12
-__device__ __forceinline__ int comp_lane(int c) {
-    const int g = (c * 11) >> 5;  // c / 3 for c < 16
-    return 8 * g + 2 * (c - 3 * g);
-}
-
 // d_z * SQRT1_2 of _core.pyx:293-302 (d_z = DA G (2/sqrt(pi)) e^-z^2 (o + (o1-o2)E/2))
 constexpr float kDzScale = SSG_TWO_OVER_SQRT_PI * SSG_SQRT1_2;
 
@@ -294,7 +290,7 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                  const int32_t *__restrict__ last_idx, const uint32_t *__restrict__ blend_mask,
                  const float *__restrict__ dL, float *__restrict__ grad_screen, float *__restrict__ slots) {
     __shared__ SmemBatch s;
-    __shared__ float4 *sRow[kBatch];  // destination gradient row of each staged instance
+    __shared__ float *sRow[kBatch];  // destination gradient row of each staged instance
     __shared__ int sMax[kThreads / 32];
     const int tile = blockIdx.x;
     const int tyi = tile / ntx, txi = tile - tyi * ntx;
@@ -331,10 +327,9 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
     const int hi = min(maxli + 1, end);
     const uint32_t aA = smem_addr(s.A), aB = smem_addr(s.B), aC = smem_addr(s.C);
     const uint32_t aX = smem_addr(s.X), aD = smem_addr(s.D);
-    // the three writer lanes (0, 8, 16) gather components 4w..4w+3
-    const int wsel = min(lane >> 3, 2);
-    const int src0 = comp_lane(4 * wsel), src1 = comp_lane(4 * wsel + 1);
-    const int src2 = comp_lane(4 * wsel + 2), src3 = comp_lane(4 * wsel + 3);
+    // lane 8g + 2c (c < 3) holds component 3g + c after the reduction
+    const bool holder = (lane & 1) == 0 && ((lane >> 1) & 3) < 3;
+    const int my_comp = 3 * (lane >> 3) + ((lane >> 1) & 3);
 
     // batches aligned to the forward's chunk grid (start + 256 b), top down
     for (int b = (hi - start - 1) / kBatch; b >= 0; b--) {
@@ -350,8 +345,7 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
             stage_splat(splat, p, ox, oy, s, threadIdx.x);
             // per-primitive accumulator, or (plugin slot mode) the per-instance
             // (M,12) slot row of _core.pyx:309-312 (raster/backward.py:70-73)
-            sRow[threadIdx.x] = reinterpret_cast<float4 *>(slots ? slots + (size_t)(lo + threadIdx.x) * 12
-                                                                 : grad_screen + (size_t)p * 12);
+            sRow[threadIdx.x] = slots ? slots + (size_t)(lo + threadIdx.x) * 12 : grad_screen + (size_t)p * 12;
         }
         __syncthreads();
 
@@ -441,19 +435,12 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                 // with the forward's mask every visited instance has a
                 // contributing pixel; without it, skip empty hits
                 if (blend_mask || __any_sync(0xffffffffu, contrib)) {
-                    // lanes 0 / 8 / 16 gather four consecutive components and
-                    // issue one float4 reduction each straight into the
-                    // primitive's accumulator (raster/backward.py:70-73)
+                    // the 12 holder lanes add their component straight into the
+                    // primitive's accumulator row, or (plugin slot mode) the
+                    // per-instance (M,12) slot row of _core.pyx:309-312
+                    // (raster/backward.py:70-73)
                     const float v = warp_reduce_transposed12(g, lane);
-                    const float v0 = __shfl_sync(0xffffffffu, v, src0);
-                    const float v1 = __shfl_sync(0xffffffffu, v, src1);
-                    const float v2 = __shfl_sync(0xffffffffu, v, src2);
-                    const float v3 = __shfl_sync(0xffffffffu, v, src3);
-                    if ((lane & 7) == 0 && lane < 24) {
-                        // per-primitive accumulator, or (plugin slot mode) the
-                        // per-instance (M,12) slot row of _core.pyx:309-312
-                        atomicAdd(sRow[j] + (lane >> 3), make_float4(v0, v1, v2, v3));
-                    }
+                    if (holder) atomicAdd(sRow[j] + my_comp, v);
                 }
             }
         }
