@@ -266,86 +266,156 @@ __device__ __forceinline__ void prep_geom(const ssg_scene &sc, const ssg_camera 
 }
 
 
-// One kernel for the whole projection backward.  A warp owns 32 consecutive
-// primitives: it stages their SH coefficient rows (3K floats each) through
-// shared memory with coalesced float4 loads, every lane runs the fp64
-// geometry chain of its primitive (prep_geom) while the rows are in flight,
-// then the SH part (projection.py:355-363, sh.py:25-109): d_sh = basis (x)
-// dcolor on the unclamped channels, written back through the same staging,
-// and the view-direction term folded into d_mu before its single store.  An
-// invalid primitive has no tile instances, so its screen gradients are zero
-// and so are its outputs (zero_invalid, projection.py:368-379).
+// Outputs of a primitive whose 12 screen gradients are all zero: every
+// gradient is 0 (no instance touched a pixel with dL != 0, or the primitive
+// is invalid: zero_invalid, projection.py:368-379).
+template <int ROW>
+__device__ __forceinline__ void zero_outputs(const ssg_grad_buffers &gr, int64_t i) {
+#pragma unroll
+    for (int j = 0; j < 3; j++) gr.d_mu[3 * i + j] = gr.d_log_scale[3 * i + j] = gr.d_eta[3 * i + j] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 4; j++) gr.d_rot[4 * i + j] = 0.0f;
+    gr.d_opacity_logits[2 * i] = gr.d_opacity_logits[2 * i + 1] = 0.0f;
+    gr.g_uv[i] = 0.0f;
+    gr.g_z[i] = 0.0f;
+    float *row = gr.d_sh + (size_t)i * ROW;
+    if (ROW % 4 == 0 && (((uintptr_t)row) & 15) == 0) {
+#pragma unroll
+        for (int q = 0; q < ROW / 4; q++) reinterpret_cast<float4 *>(row)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+#pragma unroll
+        for (int q = 0; q < ROW; q++) row[q] = 0.0f;
+    }
+}
+
+// One kernel for the whole projection backward.  Only primitives with a
+// non-zero screen gradient need the chain (off-screen and occluded ones are
+// zero-filled), and they are scattered through the index range, so a warp
+// owns kPbSpan consecutive primitives and compacts its active ones:
+//   scan    the screen gradients of the whole span, all loads in flight at
+//           once; inactive primitives are zero-filled, the active ones'
+//           offsets listed in shared memory in index order
+//   batches of 32 listed primitives, every lane busy:
+//     stage   their SH coefficient rows (3K floats each) into shared memory
+//             with asynchronous copies (no register round trip)
+//     lanes   the fp64 geometry chain of the lane's primitive (prep_geom),
+//             then the SH part (projection.py:355-363, sh.py:25-109): d_sh =
+//             basis (x) dcolor on the unclamped channels, written back
+//             through the same staging, and the view-direction term folded
+//             into d_mu before its single store
+//     store   the d_sh rows, one row per step (coalesced)
+#ifndef SSG_PB_SPAN
+#define SSG_PB_SPAN 128
+#endif
+constexpr int kPbSpan = SSG_PB_SPAN;
+constexpr int kPbIt = kPbSpan / 32;
+
+__device__ __forceinline__ void cp_async4(float *dst_smem, const float *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst_smem)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 template <int DEG>
 __global__ void __launch_bounds__(128, SSG_PB_MINB)
 k_preprocess_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
     constexpr int K = (DEG + 1) * (DEG + 1);
     constexpr int ROW = 3 * K;                 // floats per primitive
     __shared__ __align__(16) float tile[4][32 * ROW];
+    __shared__ int32_t list[4][kPbSpan];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t first = ((int64_t)blockIdx.x * 4 + warp) * 32;
-    if (first >= sc.n) return;
-    const int nw = (int)(sc.n - first < 32 ? sc.n - first : 32);
+    const uint32_t lt = (1u << lane) - 1u;
+    const int64_t p0 = ((int64_t)blockIdx.x * 4 + warp) * kPbSpan;
+    if (p0 >= sc.n) return;
+    const int span = sc.n - p0 < kPbSpan ? (int)(sc.n - p0) : kPbSpan;
     float *t = tile[warp];
-    const float *src = sc.sh + first * ROW;
-    if ((ROW * nw) % 4 == 0 && (((uintptr_t)src) & 15) == 0) {
-        const float4 *s4 = reinterpret_cast<const float4 *>(src);
-        for (int q = lane; q < ROW * nw / 4; q += 32) reinterpret_cast<float4 *>(t)[q] = __ldg(s4 + q);
-    } else {
-        for (int q = lane; q < ROW * nw; q += 32) t[q] = __ldg(src + q);
-    }
-    __syncwarp();
-    const int64_t i = first + lane;
-    float dmu[3] = {0.0f, 0.0f, 0.0f};
-    if (lane < nw) prep_geom(sc, cam, gr, i, dmu);  // fp64 geometry while the rows sit in smem
-    if (lane < nw) {
-        const float *sh = t + lane * ROW;
-        const float *sg = gr.screen + 12 * i;
-        const float dcol[3] = {sg[9], sg[10], sg[11]};
-        // the forward's fp32 colour (preprocess_fwd.cu), recomputed bit for bit
-        // so the clamp mask of projection.py:221-223 / :356 is the forward's
-        const double dv0 = sc.mu[3 * i] - cam.campos[0], dv1 = sc.mu[3 * i + 1] - cam.campos[1],
-                     dv2 = sc.mu[3 * i + 2] - cam.campos[2];
-        const double dn = sqrt(dv0 * dv0 + dv1 * dv1 + dv2 * dv2);
-        const double dns = dn > 1e-12 ? dn : 1.0;
-        const float x = (float)(dv0 / dns), y = (float)(dv1 / dns), z = (float)(dv2 / dns);
-        float basis[16];
-        sh_basis_f(DEG, x, y, z, basis);
-        float col[3] = {0.0f, 0.0f, 0.0f};
+    int32_t *q = list[warp];
+
+    // scan: activity of the span's primitives
+    int nact = 0;
+    {
+        float4 g[kPbIt][3];
 #pragma unroll
-        for (int k = 0; k < K; k++)
-#pragma unroll
-            for (int c = 0; c < 3; c++) col[c] = fmaf(basis[k], sh[3 * k + c], col[c]);
-        float dcc[3];
-#pragma unroll
-        for (int c = 0; c < 3; c++) dcc[c] = (col[c] + 0.5f > 0.0f) ? dcol[c] : 0.0f;
-        float w[16];
-#pragma unroll
-        for (int k = 0; k < K; k++) w[k] = sh[3 * k] * dcc[0] + sh[3 * k + 1] * dcc[1] + sh[3 * k + 2] * dcc[2];
-        float dd[3] = {0.0f, 0.0f, 0.0f};
-        if (DEG > 0) sh_dot_grad_f(DEG, x, y, z, w, dd);
-        __syncwarp(__activemask());
-        float *out = t + lane * ROW;  // this lane's own row: safe to overwrite now
-#pragma unroll
-        for (int k = 0; k < K; k++)
-#pragma unroll
-            for (int c = 0; c < 3; c++) out[3 * k + c] = basis[k] * dcc[c];
-        if (DEG > 0) {
-            const float inner = x * dd[0] + y * dd[1] + z * dd[2];
-            const float rdn = (float)(1.0 / dns);
-            dmu[0] += (dd[0] - x * inner) * rdn;
-            dmu[1] += (dd[1] - y * inner) * rdn;
-            dmu[2] += (dd[2] - z * inner) * rdn;
+        for (int k = 0; k < kPbIt; k++) {
+            const int o = 32 * k + lane;
+            const float4 *sg4 = reinterpret_cast<const float4 *>(gr.screen + 12 * (p0 + (o < span ? o : 0)));
+            g[k][0] = sg4[0];
+            g[k][1] = sg4[1];
+            g[k][2] = sg4[2];
         }
 #pragma unroll
-        for (int j = 0; j < 3; j++) gr.d_mu[3 * i + j] = dmu[j];
+        for (int k = 0; k < kPbIt; k++) {
+            const int o = 32 * k + lane;
+            const float4 a = g[k][0], b = g[k][1], c = g[k][2];
+            const bool act = o < span && (a.x != 0.0f || a.y != 0.0f || a.z != 0.0f || a.w != 0.0f || b.x != 0.0f ||
+                                          b.y != 0.0f || b.z != 0.0f || b.w != 0.0f || c.x != 0.0f ||
+                                          c.y != 0.0f || c.z != 0.0f || c.w != 0.0f);
+            const uint32_t m = __ballot_sync(0xffffffffu, act);
+            if (act) q[nact + __popc(m & lt)] = o;
+            if (o < span && !act) zero_outputs<ROW>(gr, p0 + o);
+            nact += __popc(m);
+        }
     }
     __syncwarp();
-    float *dst = gr.d_sh + first * ROW;
-    if ((ROW * nw) % 4 == 0 && (((uintptr_t)dst) & 15) == 0) {
-        float4 *d4 = reinterpret_cast<float4 *>(dst);
-        for (int q = lane; q < ROW * nw / 4; q += 32) d4[q] = reinterpret_cast<const float4 *>(t)[q];
-    } else {
-        for (int q = lane; q < ROW * nw; q += 32) dst[q] = t[q];
+
+    for (int b0 = 0; b0 < nact; b0 += 32) {
+        const int nb = nact - b0 < 32 ? nact - b0 : 32;
+        // stage the batch's SH rows (asynchronous copies, one wait)
+        for (int r = 0; r < nb; r++) {
+            const float *src = sc.sh + (size_t)(p0 + q[b0 + r]) * ROW;
+            for (int c = lane; c < ROW; c += 32) cp_async4(t + r * ROW + c, src + c);
+        }
+        cp_async_wait_all();
+        __syncwarp();
+        if (lane < nb) {
+            const int64_t i = p0 + q[b0 + lane];
+            float dmu[3] = {0.0f, 0.0f, 0.0f};
+            prep_geom(sc, cam, gr, i, dmu);  // fp64 geometry
+            const float *sh = t + lane * ROW;
+            const float *sg = gr.screen + 12 * i;
+            const float dcol[3] = {sg[9], sg[10], sg[11]};
+            // the forward's fp32 colour (preprocess_fwd.cu), recomputed bit for
+            // bit so the clamp mask of projection.py:221-223 / :356 is the forward's
+            const double dv0 = sc.mu[3 * i] - cam.campos[0], dv1 = sc.mu[3 * i + 1] - cam.campos[1],
+                         dv2 = sc.mu[3 * i + 2] - cam.campos[2];
+            const double dn = sqrt(dv0 * dv0 + dv1 * dv1 + dv2 * dv2);
+            const double dns = dn > 1e-12 ? dn : 1.0;
+            const float x = (float)(dv0 / dns), y = (float)(dv1 / dns), z = (float)(dv2 / dns);
+            float basis[16];
+            sh_basis_f(DEG, x, y, z, basis);
+            float col[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+            for (int k = 0; k < K; k++)
+#pragma unroll
+                for (int c = 0; c < 3; c++) col[c] = fmaf(basis[k], sh[3 * k + c], col[c]);
+            float dcc[3];
+#pragma unroll
+            for (int c = 0; c < 3; c++) dcc[c] = (col[c] + 0.5f > 0.0f) ? dcol[c] : 0.0f;
+            float w[16];
+#pragma unroll
+            for (int k = 0; k < K; k++) w[k] = sh[3 * k] * dcc[0] + sh[3 * k + 1] * dcc[1] + sh[3 * k + 2] * dcc[2];
+            float dd[3] = {0.0f, 0.0f, 0.0f};
+            if (DEG > 0) sh_dot_grad_f(DEG, x, y, z, w, dd);
+            float *out = t + lane * ROW;  // this lane's own row: safe to overwrite now
+#pragma unroll
+            for (int k = 0; k < K; k++)
+#pragma unroll
+                for (int c = 0; c < 3; c++) out[3 * k + c] = basis[k] * dcc[c];
+            if (DEG > 0) {
+                const float inner = x * dd[0] + y * dd[1] + z * dd[2];
+                const float rdn = (float)(1.0 / dns);
+                dmu[0] += (dd[0] - x * inner) * rdn;
+                dmu[1] += (dd[1] - y * inner) * rdn;
+                dmu[2] += (dd[2] - z * inner) * rdn;
+            }
+#pragma unroll
+            for (int j = 0; j < 3; j++) gr.d_mu[3 * i + j] = dmu[j];
+        }
+        __syncwarp();
+        for (int r = 0; r < nb; r++) {
+            float *dst = gr.d_sh + (size_t)(p0 + q[b0 + r]) * ROW;
+            for (int c = lane; c < ROW; c += 32) dst[c] = t[r * ROW + c];
+        }
+        __syncwarp();
     }
 }
 
@@ -358,7 +428,8 @@ extern "C" int ssg_preprocess_backward(const ssg_scene *scene, const ssg_camera 
     if (scene->sh_degree < 0 || scene->sh_degree > 3) return SSG_ERR_INVALID_ARGUMENT;
     if (scene->n == 0) return SSG_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    unsigned blocks = (unsigned)((scene->n + 127) / 128);
+    const int64_t per_block = 4 * (int64_t)kPbSpan;  // 4 warps of kPbSpan primitives
+    unsigned blocks = (unsigned)((scene->n + per_block - 1) / per_block);
     switch (scene->sh_degree) {
         case 0: k_preprocess_backward<0><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
         case 1: k_preprocess_backward<1><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
