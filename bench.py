@@ -353,8 +353,17 @@ def main():
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
         peaks = json.load(fh)
     f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    r_fp32 = n_sm * 128 * f_max          # FP32 lane-instructions / s
-    r_mufu = n_sm * 16 * f_max
+    # FP32 / MUFU lane rates: measured per SM clock (tools/micro/peaks.sh ->
+    # profiles/measured_issue_peaks.json) scaled to sm_max, else nominal
+    per_clk, peak_src = {"ffma": 128.0, "ex2": 16.0}, "nominal"
+    try:
+        mp = json.load(open(os.path.join(ROOT, "profiles", "measured_issue_peaks.json")))
+        per_clk = {"ffma": float(mp["ffma_per_sm_clk"]), "ex2": float(mp["ex2_per_sm_clk"])}
+        peak_src = "measured (profiles/measured_issue_peaks.json)"
+    except (OSError, ValueError, KeyError):
+        pass
+    r_fp32 = n_sm * per_clk["ffma"] * f_max   # FP32 lane-instructions / s
+    r_mufu = n_sm * per_clk["ex2"] * f_max
     dom = max(("blend_fwd", "blend_bwd"), key=lambda k: stage_ms.get(k, 0.0))
     t_dom = stage_ms[dom] * 1e-3
     achieved = FP32_PER_PAIR[dom] * pairs / t_dom
@@ -375,8 +384,8 @@ def main():
                              "while the kernels cull pairs per 8x4-pixel warp block by an exact ellipse test "
                              "and the backward visits only (warp, instance) pairs the forward blended; "
                              "profiles/ has the measured issue-slot utilisation",
-                "peak_basis": f"{n_sm} SMs x 128 FP32 lanes x sm_max {f_max/1e6:.0f} MHz (nominal; "
-                              "no dense contraction on this path, tensor cores unused)"}
+                "peak_basis": f"{n_sm} SMs x {per_clk['ffma']:.1f} FFMA lanes/clk x sm_max {f_max/1e6:.0f} MHz, "
+                              f"{peak_src}; no dense contraction on this path, tensor cores unused"}
     hbm = float(peaks["hbm_gbs"])
     stage_bytes = {"preprocess_fwd": n * (304 + 64 + 29),
                    "preprocess_bwd": n * (304 + 48 + 65 * 4)}
@@ -390,7 +399,7 @@ def main():
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
         stage_roofline.get("preprocess_fwd", {})["traffic"] = tr.get("k_preprocess_forward")
         if "preprocess_bwd" in stage_roofline:
-            stage_roofline["preprocess_bwd"]["traffic"] = tr.get("k_preprocess_backward", 0) + tr.get("k_sh_backward", 0)
+            stage_roofline["preprocess_bwd"]["traffic"] = tr.get("k_preprocess_backward")
     except (OSError, ValueError):
         pass
     t_floor = (FP32_PER_PAIR["blend_fwd"] + FP32_PER_PAIR["blend_bwd"]) * pairs / r_fp32 + \
