@@ -340,8 +340,31 @@ def main():
     scene_bytes = n * (3 + 3 + 4 + 3 * K + 2 + 3 + 3) * 8
     h2d = 2 * scene_bytes + HEIGHT * WIDTH * (8 + 8 + 24)  # fwd + bwd uploads, final_T, last_idx, dL
     d2h = HEIGHT * WIDTH * (24 + 8 + 4 + 8) + n * (3 + 3 + 4 + 3 * K + 2 + 3 + 3 + 1 + 1) * 8
+    # the e2e path is host-link bound: measured pinned copy rates -> floor
+    def link_gbs(h2d_dir: bool) -> float:
+        nb = 256 << 20
+        host = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+        devb = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        best = 0.0
+        for _ in range(4):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            if h2d_dir:
+                devb.copy_(host, non_blocking=True)
+            else:
+                host.copy_(devb, non_blocking=True)
+            b.record()
+            b.synchronize()
+            best = max(best, nb / (a.elapsed_time(b) * 1e-3) / 1e9)
+        return best
+    h2d_gbs, d2h_gbs = link_gbs(True), link_gbs(False)
+    link_floor_s = h2d / (h2d_gbs * 1e9) + d2h / (d2h_gbs * 1e9)
     e2e = {"value": world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
+           "link": {"h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs, "floor_ms": link_floor_s * 1e3,
+                    "frac": link_floor_s / e2e_s,
+                    "note": "pinned 256 MiB copies, best of 4; floor = the step's H2D + D2H bytes at "
+                            "those rates, serialised (the API's calls are synchronous)"},
            "path": "paper_2605_18334_b200.raster.render_forward + render_backward, numpy fp64 "
                    "scene/dL in pinned host memory, fp64 outputs back to host; backward "
                    "recomputes projection+binning like the reference"}
