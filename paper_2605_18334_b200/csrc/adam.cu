@@ -69,9 +69,55 @@ __global__ void __launch_bounds__(256) k_adam_field(int64_t n, P *__restrict__ p
     }
 }
 
+// fp32 parameters, 4 elements per thread with 16-byte accesses (each
+// element keeps its own row check: a float4 may straddle two rows when W is
+// not a multiple of 4).  Same arithmetic as k_adam_field.
+template <int W>
+__global__ void __launch_bounds__(256) k_adam_field_v4(int64_t n, float4 *__restrict__ p,
+                                                       const float4 *__restrict__ g, float4 *__restrict__ m,
+                                                       float4 *__restrict__ v, const uint8_t *__restrict__ row_ok,
+                                                       float lr, float rc1, float rc2) {
+    const uint32_t total4 = (uint32_t)(n * W / 4);
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < total4; q += gridDim.x * blockDim.x) {
+        const float4 g4 = g[q];
+        float4 m4 = m[q], v4 = v[q], p4 = p[q];
+        float *gg = reinterpret_cast<float *>(const_cast<float4 *>(&g4)), *mm = reinterpret_cast<float *>(&m4);
+        float *vv = reinterpret_cast<float *>(&v4), *pp = reinterpret_cast<float *>(&p4);
+        bool any = false;
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            if (!row_ok[(4 * q + c) / W]) continue;
+            any = true;
+            const float mn = kBeta1 * mm[c] + (1.0f - kBeta1) * gg[c];
+            const float vn = kBeta2 * vv[c] + (1.0f - kBeta2) * gg[c] * gg[c];
+            mm[c] = mn;
+            vv[c] = vn;
+            const float upd = lr * (mn * rc1) / (sqrtf(vn * rc2) + kEps);
+            pp[c] = (float)((double)pp[c] - (double)upd);
+        }
+        if (any) {
+            m[q] = m4;
+            v[q] = v4;
+            p[q] = p4;
+        }
+    }
+}
+
 template <typename P, int W>
 static void launch_field(int64_t n, P *p, const float *g, float *m, float *v, const uint8_t *row_ok, double lr,
                          double c1, double c2, cudaStream_t st) {
+    if constexpr (sizeof(P) == 4) {
+        const auto al = [](const void *x) { return (((uintptr_t)x) & 15) == 0; };
+        if ((n * W) % 4 == 0 && al(p) && al(g) && al(m) && al(v)) {
+            const int64_t b64 = (n * W / 4 + 255) / 256;
+            const unsigned blocks = (unsigned)(b64 < 148 * 16 ? b64 : 148 * 16);
+            k_adam_field_v4<W><<<blocks, 256, 0, st>>>(n, reinterpret_cast<float4 *>(p),
+                                                       reinterpret_cast<const float4 *>(g),
+                                                       reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v),
+                                                       row_ok, (float)lr, (float)(1.0 / c1), (float)(1.0 / c2));
+            return;
+        }
+    }
     const int64_t blocks64 = (n * W + 255) / 256;
     const unsigned blocks = (unsigned)(blocks64 < 148 * 16 ? blocks64 : 148 * 16);
     k_adam_field<P, W><<<blocks, 256, 0, st>>>(n, p, g, m, v, row_ok, (float)lr, (float)(1.0 / c1),
