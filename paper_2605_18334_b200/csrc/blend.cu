@@ -224,9 +224,12 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
                 C1 = fmaf(w, C.w, C1);
                 C2 = fmaf(w, cb, C2);
                 T = blend ? test_T : T;
-                nc += blend;
-                li = blend ? base + j : li;
                 lbits |= (uint32_t)blend << bit;
+            }
+            // n_contrib and last_idx from the chunk's blend bits (ascending k)
+            if (lbits) {
+                nc += __popc(lbits);
+                li = base + c0 + 31 - __clz(lbits);
             }
             if (blend_mask) {
                 const uint32_t bmask = __reduce_or_sync(0xffffffffu, lbits);
