@@ -13,7 +13,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --c
 python tools/launch_table.py gpurun_out/${tag}_launches.csv > gpurun_out/${tag}_launch_table.txt 2>&1
 # skip the warm-up frames: 3 warm-up + 2 timed frames of the value loop come first
 for k in blend preprocess depth_sort cs; do
-  case $k in blend) rx="k_blend"; sk=6; c=2;; preprocess) rx="k_preprocess|k_sh_backward"; sk=9; c=3;;
+  case $k in blend) rx="k_blend"; sk=6; c=2;; preprocess) rx="k_preprocess"; sk=6; c=2;;
              depth_sort) rx="k_depth_sort"; sk=3; c=1;; cs) rx="k_cs"; sk=24; c=8;; esac
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$rx" -s $sk -c $c \
     -o gpurun_out/${tag}_$k -f python bench.py --steps 2 --warmup 3 --e2e-steps 1 --no-cpu > gpurun_out/${tag}_ncu_$k.log 2>&1
