@@ -64,21 +64,13 @@ def test_config3_mixed_scene_matches_oracle():
         assert np.mean(e <= 1e-3) >= 0.999 and e.max() <= 1e-2, k
 
 
-@pytest.mark.parametrize("plain", [0.0, 0.5])
-def test_full_size_properties(plain):
-    scene = frustum_scene(1_000_000, plain_fraction=plain)
-    view = frustum_view()
-    eng = Engine()
-    ds = DeviceScene.from_host(scene)
-    f = eng.forward(ds, view, 0.3)
-    m = f.n_instances
-    if plain == 0.0:
-        assert m == 9_097_352  # SURVEY.md §8(d), measured from the reference on G2
-    ntx, nty = grid_dims(1920, 1080)
+def _check_lists(eng, n, m, width, height):
+    """Instance lists sorted by (tile, depth, id); ranges = the tile histogram."""
+    ntx, nty = grid_dims(width, height)
     ip, it, rg = eng.grid(ntx * nty)
     tile = it.long() & 0xFFFF
     prim = ip.long()
-    depth = eng.depth[: len(scene)][prim]
+    depth = eng.depth[:n][prim]
     assert bool((tile[1:] >= tile[:-1]).all())
     same = tile[1:] == tile[:-1]
     dd = depth[1:] - depth[:-1]
@@ -89,6 +81,33 @@ def test_full_size_properties(plain):
     cnt = torch.bincount(tile, minlength=ntx * nty)
     assert torch.equal(r[:, 1] - r[:, 0], cnt)
     assert int(r[-1, 1]) == m and int(r[0, 0]) == 0
+    return prim
+
+
+def test_config4_full_size_lists():
+    """G4 view 0 at full size (3M primitives: several depth-sort tiles per
+    CTA, the flagged-sum scan across them): M equals the reference's count
+    and the lists keep their order."""
+    scene = ball_scene(3_000_000, seed=0)
+    view = orbit_views(64, radius=4.0, elevation=1.2, width=1297, height=840, fov_x=0.9)[0]
+    eng = Engine()
+    ds = DeviceScene.from_host(scene)
+    f = eng.forward(ds, view, 0.3)
+    assert f.n_instances == 17_916_589  # SURVEY.md §8(d), G4 view 0
+    _check_lists(eng, len(scene), f.n_instances, 1297, 840)
+
+
+@pytest.mark.parametrize("plain", [0.0, 0.5])
+def test_full_size_properties(plain):
+    scene = frustum_scene(1_000_000, plain_fraction=plain)
+    view = frustum_view()
+    eng = Engine()
+    ds = DeviceScene.from_host(scene)
+    f = eng.forward(ds, view, 0.3)
+    m = f.n_instances
+    if plain == 0.0:
+        assert m == 9_097_352  # SURVEY.md §8(d), measured from the reference on G2
+    prim = _check_lists(eng, len(scene), m, 1920, 1080)
     T = f.final_T
     assert float(T.min()) >= 1e-4 * (1 - 0.99) - 1e-7 and float(T.max()) <= 1.0
     assert bool(torch.isfinite(f.color).all())
