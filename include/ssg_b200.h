@@ -208,6 +208,19 @@ int ssg_blend_backward(int64_t n, int64_t m, int32_t width, int32_t height,
                        const float *dL_dpixels, const ssg_grad_buffers *grads, void *stream);
 int ssg_preprocess_backward(const ssg_scene *scene, const ssg_camera *cam,
                             const ssg_grad_buffers *grads, void *stream);
+/* The projection backward in two parts, so the zero-fill can overlap the
+ * blend (what the engine does: ssg_zero_prim_grads on a second stream while
+ * ssg_blend_backward runs, then ssg_preprocess_backward_ex with
+ * SSG_PREP_BWD_ACTIVE_ONLY).  ssg_zero_prim_grads zeroes grads' per-primitive
+ * fields (d_mu, d_log_scale, d_rot, d_sh with sh_coeffs, d_opacity_logits,
+ * d_eta, g_uv, g_z); with SSG_PREP_BWD_ACTIVE_ONLY the projection backward
+ * writes only the primitives with a non-zero screen gradient (the others must
+ * already be zero).  flags = 0 is ssg_preprocess_backward.  Outputs are
+ * identical either way. */
+#define SSG_PREP_BWD_ACTIVE_ONLY 1
+int ssg_zero_prim_grads(int64_t n, int32_t sh_coeffs, const ssg_grad_buffers *grads, void *stream);
+int ssg_preprocess_backward_ex(const ssg_scene *scene, const ssg_camera *cam,
+                               const ssg_grad_buffers *grads, int32_t flags, void *stream);
 /* the reference's blend-backward plugin contract (raster/_core.pyx:315-343,
  * backward_tiles): per-instance gradient slots (m,12) instead of the fused
  * per-primitive reduction; slots is zeroed by the call */

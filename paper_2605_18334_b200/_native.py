@@ -18,10 +18,12 @@ SSG_ERR_INVALID_ARGUMENT = 1
 SSG_ERR_DIM_OVERFLOW = 2
 SSG_ERR_CAPACITY = 3
 SSG_ERR_CUDA = 4
+SSG_PREP_BWD_ACTIVE_ONLY = 1
 
 EXPORTS = ("ssg_abi_version", "ssg_last_error", "ssg_grid_dims", "ssg_bin_temp_bytes",
            "ssg_preprocess_forward", "ssg_bin_rects", "ssg_bin_prepare", "ssg_bin_finish", "ssg_blend_forward",
            "ssg_blend_backward", "ssg_preprocess_backward", "ssg_blend_backward_slots",
+           "ssg_zero_prim_grads", "ssg_preprocess_backward_ex",
            "ssg_test_sort_temp_bytes",
            "ssg_test_sort", "ssg_test_blend_forward_vanilla", "ssg_adam_step", "ssg_blend_mask_words",
            "ssg_loss_scratch_floats", "ssg_image_loss", "ssg_regularize", "ssg_interval_stats_add",
@@ -95,7 +97,7 @@ class SsgAdamHparams(ctypes.Structure):
 
 
 SPLAT_BYTES = 64
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _lib = None
 
@@ -133,6 +135,8 @@ def lib():
                                      ctypes.c_int32, P(ctypes.c_float), _vp, P(SsgBinBuffers),
                                      P(SsgFrameBuffers), _vp, P(SsgGradBuffers), _vp]
     L.ssg_preprocess_backward.argtypes = [P(SsgScene), P(SsgCamera), P(SsgGradBuffers), _vp]
+    L.ssg_zero_prim_grads.argtypes = [ctypes.c_int64, ctypes.c_int32, P(SsgGradBuffers), _vp]
+    L.ssg_preprocess_backward_ex.argtypes = [P(SsgScene), P(SsgCamera), P(SsgGradBuffers), ctypes.c_int32, _vp]
     L.ssg_blend_backward_slots.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                            P(ctypes.c_float), _vp, P(SsgBinBuffers), P(SsgFrameBuffers),
                                            _vp, _vp, _vp]

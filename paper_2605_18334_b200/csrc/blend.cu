@@ -490,7 +490,7 @@ extern "C" int ssg_blend_backward(int64_t n, int64_t m, int32_t width, int32_t h
                                   const ssg_bin_buffers *bins, const ssg_frame_buffers *frame,
                                   const float *dL_dpixels, const ssg_grad_buffers *grads, void *stream) {
     using namespace ssg;
-    if (!bins || !frame || !grads || !background || !dL_dpixels || width < 1 || height < 1)
+    if (!bins || !frame || !grads || !background || !dL_dpixels || width < 1 || height < 1 || n < 0)
         return SSG_ERR_INVALID_ARGUMENT;
     (void)m;
     cudaStream_t st = (cudaStream_t)stream;

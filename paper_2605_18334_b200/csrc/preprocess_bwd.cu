@@ -317,7 +317,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 template <int DEG>
 __global__ void __launch_bounds__(128, SSG_PB_MINB)
-k_preprocess_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
+k_preprocess_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr, int zero_inactive) {
     constexpr int K = (DEG + 1) * (DEG + 1);
     constexpr int ROW = 3 * K;                 // floats per primitive
     __shared__ __align__(16) float tile[4][32 * ROW];
@@ -351,7 +351,7 @@ k_preprocess_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
                                           c.y != 0.0f || c.z != 0.0f || c.w != 0.0f);
             const uint32_t m = __ballot_sync(0xffffffffu, act);
             if (act) q[nact + __popc(m & lt)] = o;
-            if (o < span && !act) zero_outputs<ROW>(gr, p0 + o);
+            if (zero_inactive && o < span && !act) zero_outputs<ROW>(gr, p0 + o);
             nact += __popc(m);
         }
     }
@@ -421,20 +421,43 @@ k_preprocess_backward(ssg_scene sc, ssg_camera cam, ssg_grad_buffers gr) {
 
 }  // namespace ssg
 
-extern "C" int ssg_preprocess_backward(const ssg_scene *scene, const ssg_camera *cam,
-                                       const ssg_grad_buffers *grads, void *stream) {
+extern "C" int ssg_zero_prim_grads(int64_t n, int32_t sh_coeffs, const ssg_grad_buffers *grads, void *stream) {
+    using namespace ssg;
+    if (!grads || n < 0 || sh_coeffs < 1 || sh_coeffs > 16) return SSG_ERR_INVALID_ARGUMENT;
+    if (n == 0) return SSG_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    float *const f[8] = {grads->d_mu, grads->d_log_scale, grads->d_rot, grads->d_sh,
+                         grads->d_opacity_logits, grads->d_eta, grads->g_uv, grads->g_z};
+    const int w[8] = {3, 3, 4, 3 * sh_coeffs, 2, 3, 1, 1};
+    for (int k = 0; k < 8; k++) {
+        if (!f[k]) return SSG_ERR_INVALID_ARGUMENT;
+        const cudaError_t e = cudaMemsetAsync(f[k], 0, sizeof(float) * (size_t)w[k] * (size_t)n, st);
+        if (e != cudaSuccess) { set_error("memset prim grads", e); return SSG_ERR_CUDA; }
+    }
+    return SSG_OK;
+}
+
+extern "C" int ssg_preprocess_backward_ex(const ssg_scene *scene, const ssg_camera *cam,
+                                          const ssg_grad_buffers *grads, int32_t flags, void *stream) {
     using namespace ssg;
     if (!scene || !cam || !grads) return SSG_ERR_INVALID_ARGUMENT;
     if (scene->sh_degree < 0 || scene->sh_degree > 3) return SSG_ERR_INVALID_ARGUMENT;
+    if ((flags & ~SSG_PREP_BWD_ACTIVE_ONLY) != 0) return SSG_ERR_INVALID_ARGUMENT;
     if (scene->n == 0) return SSG_OK;
+    const int zero = (flags & SSG_PREP_BWD_ACTIVE_ONLY) ? 0 : 1;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t per_block = 4 * (int64_t)kPbSpan;  // 4 warps of kPbSpan primitives
     unsigned blocks = (unsigned)((scene->n + per_block - 1) / per_block);
     switch (scene->sh_degree) {
-        case 0: k_preprocess_backward<0><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
-        case 1: k_preprocess_backward<1><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
-        case 2: k_preprocess_backward<2><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
-        default: k_preprocess_backward<3><<<blocks, 128, 0, st>>>(*scene, *cam, *grads); break;
+        case 0: k_preprocess_backward<0><<<blocks, 128, 0, st>>>(*scene, *cam, *grads, zero); break;
+        case 1: k_preprocess_backward<1><<<blocks, 128, 0, st>>>(*scene, *cam, *grads, zero); break;
+        case 2: k_preprocess_backward<2><<<blocks, 128, 0, st>>>(*scene, *cam, *grads, zero); break;
+        default: k_preprocess_backward<3><<<blocks, 128, 0, st>>>(*scene, *cam, *grads, zero); break;
     }
     return check_launch("k_preprocess_backward");
+}
+
+extern "C" int ssg_preprocess_backward(const ssg_scene *scene, const ssg_camera *cam,
+                                       const ssg_grad_buffers *grads, void *stream) {
+    return ssg_preprocess_backward_ex(scene, cam, grads, 0, stream);
 }

@@ -277,6 +277,17 @@ class Engine:
     def _stream(self) -> int:
         return torch.cuda.current_stream(self.device).cuda_stream
 
+    def _side_stream(self) -> torch.cuda.Stream:
+        """Second stream for work that overlaps an issue-bound kernel (the
+        projection backward's zero-fill under the blend).  Lowest priority:
+        its blocks take the SMs the blend's last wave leaves idle instead of
+        displacing blend blocks (a high-priority memset slowed the blend by
+        about its own duration)."""
+        if getattr(self, "_side", None) is None:
+            lo, _ = torch.cuda.Stream.priority_range()
+            self._side = torch.cuda.Stream(self.device, priority=lo)
+        return self._side
+
     # ------------------------------------------------------------- stages
     def _bin(self, n: int, W: int, H: int, sync: bool = True) -> int:
         """bin_prepare -> M (one 8-byte D2H) -> bin_finish.  sync=False skips
@@ -383,15 +394,30 @@ class Engine:
         # the forward's blend mask is reusable only for the same binning and
         # the same frame buffers that forward wrote
         use_mask = self._mask_state == (self._bin_gen, _ptr(final_T), _ptr(last_idx))
+        # the projection backward's zero-fill runs on a second stream under
+        # the issue-bound blend, which leaves DRAM idle; the
+        # projection backward then visits only primitives with a non-zero
+        # screen gradient.  The side stream starts after everything queued so
+        # far (earlier readers of the gradient buffers) and the projection
+        # backward waits for it.
+        main = torch.cuda.current_stream(self.device)
+        side = self._side_stream()
+        ev_start, ev_zero = torch.cuda.Event(), torch.cuda.Event()
+        ev_start.record(main)
+        side.wait_event(ev_start)
+        N.check(self.lib.ssg_zero_prim_grads(ds.n, ds.K, ctypes.byref(gs), side.cuda_stream), "ssg_zero_prim_grads")
+        ev_zero.record(side)
         with self._mark("blend_bwd"):
             N.check(self.lib.ssg_blend_backward(ds.n, m, W, H, bg, _ptr(self.splat), ctypes.byref(self._bins_struct()),
                                                 ctypes.byref(self._frame_struct(final_T, last_idx, mask=use_mask)),
                                                 _ptr(dL), ctypes.byref(gs), st),
                     "ssg_blend_backward")
+        main.wait_event(ev_zero)
         sc = ds.struct()
         with self._mark("preprocess_bwd"):
-            N.check(self.lib.ssg_preprocess_backward(ctypes.byref(sc), ctypes.byref(cam), ctypes.byref(gs), st),
-                    "ssg_preprocess_backward")
+            N.check(self.lib.ssg_preprocess_backward_ex(ctypes.byref(sc), ctypes.byref(cam), ctypes.byref(gs),
+                                                        N.SSG_PREP_BWD_ACTIVE_ONLY, st),
+                    "ssg_preprocess_backward_ex")
         n = ds.n
         return DeviceGrads(self.g_flat, self.g_screen[:n], self.g_mu[:n], self.g_log_scale[:n], self.g_rot[:n],
                            self.g_sh[:n], self.g_logits[:n], self.g_eta[:n], self.g_uv[:n], self.g_z[:n])
