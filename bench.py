@@ -210,6 +210,9 @@ def main():
     ap.add_argument("--cpu-k", type=int, default=16, help="homothetic CPU sample factor")
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--lanes", type=int, default=1,
+                    help="config 4: engines on their own streams (views overlap); measured slower at 2-4 "
+                         "(668 vs 720 views/s): the cooperative depth sort needs every SM free")
     ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=2,
                     help="BASELINE.json config: 2 (default, the headline), 3 (50%% skew-free), "
                          "4 (3M, 64-view forward batch sharded over ranks), 5 (2M view-parallel training)")

@@ -277,6 +277,13 @@ class Engine:
     def _stream(self) -> int:
         return torch.cuda.current_stream(self.device).cuda_stream
 
+    def lane_stream(self) -> torch.cuda.Stream:
+        """This engine's own stream for multi-engine view batches
+        (views.render_views): work queued there overlaps other engines'."""
+        if getattr(self, "_lane", None) is None:
+            self._lane = torch.cuda.Stream(self.device)
+        return self._lane
+
     def _side_stream(self) -> torch.cuda.Stream:
         """Second stream for work that overlaps an issue-bound kernel (the
         projection backward's zero-fill under the blend).  Lowest priority:

@@ -23,11 +23,17 @@ def shard_views(n_views: int, rank: int, world: int) -> range:
     return range(start, start + base + (1 if rank < extra else 0))
 
 
-def render_views(ds: DeviceScene, views, s: float = 0.3, engine: Engine | None = None,
+def render_views(ds: DeviceScene, views, s: float = 0.3, engine=None,
                  out: torch.Tensor | None = None) -> torch.Tensor:
     """Forward-render every view of `views` (same width/height) into
-    out[v] (float32 (V,H,W,3) on the engine's device)."""
-    eng = engine or default_engine()
+    out[v] (float32 (V,H,W,3) on the engine's device).
+
+    `engine` may be one Engine or several: with k engines, view i renders on
+    engine i % k, each on its own CUDA stream, so one view's latency-bound
+    projection and binning overlap another view's issue-bound blend (the
+    views are independent; every engine owns its buffers)."""
+    engines = list(engine) if isinstance(engine, (list, tuple)) else [engine or default_engine()]
+    eng = engines[0]
     if not views:
         return torch.empty((0, 0, 0, 3), dtype=torch.float32, device=eng.device)
     W, H = int(views[0].width), int(views[0].height)
@@ -35,13 +41,30 @@ def render_views(ds: DeviceScene, views, s: float = 0.3, engine: Engine | None =
         raise ValueError("render_views needs views of one image size")
     if out is None:
         out = torch.empty((len(views), H, W, 3), dtype=torch.float32, device=eng.device)
-    # every frame after the first skips the instance-count read-back, so the
-    # batch runs without host round trips; one check at the end (an
-    # overflowing frame makes the batch re-render synchronised)
-    for i, v in enumerate(views):
-        eng.forward(ds, v, s, color_out=out[i], sync=(i == 0))
+    # every frame after an engine's first skips the instance-count read-back,
+    # so the batch runs without host round trips; one check per engine at the
+    # end (an overflowing frame makes the batch re-render synchronised)
+    if len(engines) == 1:
+        for i, v in enumerate(views):
+            eng.forward(ds, v, s, color_out=out[i], sync=(i == 0))
+    else:
+        main = torch.cuda.current_stream(eng.device)
+        start = torch.cuda.Event()
+        start.record(main)
+        lanes = [e.lane_stream() for e in engines]
+        for st in lanes:
+            st.wait_event(start)
+        for i, v in enumerate(views):
+            k = i % len(engines)
+            with torch.cuda.stream(lanes[k]):
+                engines[k].forward(ds, v, s, color_out=out[i], sync=(i < len(engines)))
+        for st in lanes:
+            done = torch.cuda.Event()
+            done.record(st)
+            main.wait_event(done)
     try:
-        eng.instances()
+        for e in engines:
+            e.instances()
     except N.NativeError:  # capacity overflow somewhere in the batch: redo with read-backs
         for i, v in enumerate(views):
             eng.forward(ds, v, s, color_out=out[i], sync=True)

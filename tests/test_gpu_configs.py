@@ -136,3 +136,9 @@ def test_config4_view_batch_equals_single_views():
     batch = render_views(ds, views, engine=eng)
     for a, b in zip(singles, batch):
         assert torch.equal(a, b)
+    # several engines on their own streams (views overlap): same pixels
+    lanes = [eng, Engine(), Engine()]
+    for _ in range(2):
+        multi = render_views(ds, views, engine=lanes)
+        for a, b in zip(singles, multi):
+            assert torch.equal(a, b)
