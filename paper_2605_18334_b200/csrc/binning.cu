@@ -232,37 +232,6 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs1_count(const uint32_t *__r
     }
 }
 
-// Exclusive scan, in place, of `len` u32 at a (one CTA); returns the total.
-__device__ __forceinline__ uint32_t cta_exclusive_scan(uint32_t *a, int64_t len, uint32_t *s_warp, uint32_t &s_carry) {
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
-    if (t == 0) s_carry = 0;
-    __syncthreads();
-    for (int64_t c0 = 0; c0 < len; c0 += blockDim.x) {
-        const int64_t i = c0 + t;
-        const uint32_t v = i < len ? a[i] : 0u;
-        uint32_t x = v;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
-            if (lane >= off) x += y;
-        }
-        if (lane == 31) s_warp[w] = x;
-        __syncthreads();
-        uint32_t wpre = 0, tot = 0;
-        for (int ww = 0; ww < nw; ww++) {
-            const uint32_t sw = s_warp[ww];
-            wpre += ww < w ? sw : 0u;
-            tot += sw;
-        }
-        const uint32_t carry = s_carry;
-        if (i < len) a[i] = carry + wpre + x - v;
-        __syncthreads();
-        if (t == 0) s_carry = carry + tot;
-        __syncthreads();
-    }
-    return s_carry;
-}
-
 // Exclusive scan with one CTA of 1024 threads, each owning a contiguous run
 // (read twice): src -> dst (may alias); returns the total.
 __device__ __forceinline__ uint32_t cta_scan_runs(const uint32_t *src, uint32_t *dst, int len, uint32_t *s_warp) {
@@ -299,12 +268,13 @@ __device__ __forceinline__ uint32_t cta_scan_runs(const uint32_t *src, uint32_t 
     return total;
 }
 
-// level 1, per-row scan over chunks (one CTA per row)
-__global__ void __launch_bounds__(256) k_cs1_rowscan(uint32_t *__restrict__ cnt1, int64_t nch1,
-                                                     uint32_t *__restrict__ row_total) {
-    __shared__ uint32_t s_warp[8];
-    __shared__ uint32_t s_carry;
-    const uint32_t tot = cta_exclusive_scan(cnt1 + (size_t)blockIdx.x * nch1, nch1, s_warp, s_carry);
+// level 1, per-row scan over chunks (one CTA of 1024 threads per row, each
+// thread a contiguous run: one pass, no per-256 loop of barriers)
+__global__ void __launch_bounds__(1024) k_cs1_rowscan(uint32_t *__restrict__ cnt1, int64_t nch1,
+                                                      uint32_t *__restrict__ row_total) {
+    __shared__ uint32_t s_warp[32];
+    uint32_t *row = cnt1 + (size_t)blockIdx.x * nch1;
+    const uint32_t tot = cta_scan_runs(row, row, (int)nch1, s_warp);
     if (threadIdx.x == 0) row_total[blockIdx.x] = tot;
 }
 
@@ -641,7 +611,7 @@ extern "C" int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t heigh
     // level 1: row segments in per-row lists
     k_cs1_count<<<g1, 32 * kCsWarps, smc1, st>>>(bins->depth_order, prim->tile_count, prim->tile_rect, n, L.nch1,
                                                  nty, cnt1);
-    k_cs1_rowscan<<<nty, 256, 0, st>>>(cnt1, L.nch1, row_total);
+    k_cs1_rowscan<<<nty, 1024, 0, st>>>(cnt1, L.nch1, row_total);
     const uint32_t cap = (uint32_t)(bins->capacity > 0 ? bins->capacity : 0);
     k_cs1_rowstart<<<1, 1024, 0, st>>>(row_total, nty, (uint32_t)L.max_ch2, row_start, chunk_base, ctl);
     if (n > 0)
