@@ -320,18 +320,25 @@ class Engine:
         self._bin_gen += 1
         return m
 
-    def instances(self) -> int:
+    def instances(self, extra: torch.Tensor | None = None):
         """M of the last binning (synchronises); raises if any frame since the
         last call overflowed the instance capacity (those results are
-        invalid; the next synchronised binning grows the buffers)."""
-        m, worst = (int(x) for x in self.n_inst_dev.tolist())
+        invalid; the next synchronised binning grows the buffers).  With
+        `extra` (a device tensor), its values come back in the same D2H
+        read: returns (M, list of floats)."""
+        if extra is None:
+            m, worst = (int(x) for x in self.n_inst_dev.tolist())
+            vals = None
+        else:
+            host = torch.cat([self.n_inst_dev.double(), extra.double().reshape(-1)]).tolist()
+            m, worst, vals = int(host[0]), int(host[1]), host[2:]
         self.n_inst_dev[1] = 0
         if worst > self.capacity:
             self._bins_key = None
             raise N.NativeError(f"sync-free frame needed {worst} instances, capacity {self.capacity}; "
                                 "re-run synchronised")
         self.last_m = m
-        return m
+        return m if vals is None else (m, vals)
 
     def project_and_bin(self, ds: DeviceScene, cam: N.SsgCamera, sync: bool = True) -> int:
         W, H = int(cam.width), int(cam.height)

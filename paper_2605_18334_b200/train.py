@@ -253,17 +253,19 @@ class Trainer:
         # the regularizer value is part of the loss (losses.py:146-149); its
         # gradients are folded in after the backward and the statistics
         lossfn.sums[2].zero_()
-        try:
-            eng.instances()
+        v = lossfn.value_tensor()
+        try:  # one read-back for the instance-count check and the loss value
+            _, (loss,) = eng.instances(v)
         except N.NativeError:  # the scene outgrew the instance buffers: redo synchronised
             f = eng.forward(ds, view, s, sync=True)
             dL = lossfn(f.color, target)
             lossfn.sums[2].zero_()
-        if check_finite:
             v = lossfn.value_tensor()
+            loss = float(v)
+        if check_finite:
             # every rank must take the same branch (the all-reduce below is
             # collective): the step is skipped when any rank's view diverged
-            bad = any_rank(not math.isfinite(float(v)), group, eng.device)
+            bad = any_rank(not math.isfinite(loss), group, eng.device)
             if bad:  # fit2d.py:70-71: no backward, no update
                 return v, f
         grads = eng.backward(ds, view, s, f.final_T, f.last_idx, dL, rebin=False)
