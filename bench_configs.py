@@ -208,7 +208,7 @@ def config5(args, rank, world, local):
     barrier, max_over_ranks = _helpers(torch, dist, world)
     from paper_2605_18334_b200.engine import DeviceScene, Engine
     from paper_2605_18334_b200.synthetic import ball_scene, fp32_round, orbit_views
-    from paper_2605_18334_b200.train import DeviceAdam, training_step
+    from paper_2605_18334_b200.train import DeviceAdam, Trainer
 
     target_scene = ball_scene(N5, seed=0)
     views = orbit_views(V4, radius=4.0, elevation=1.2, width=W4, height=H4, fov_x=0.9)
@@ -223,12 +223,16 @@ def config5(args, rank, world, local):
     start.mu += np.random.default_rng(5).normal(size=start.mu.shape) * 0.01
     ds = DeviceScene.from_host(fp32_round(start))
     adam = DeviceAdam(ds)
+    # pipelined steps: no host read-back inside a step (the finite-loss branch
+    # and the instance check are a device flag, resolved at the next step)
+    tr = Trainer(eng, ds, adam, pipelined=True)
     step_no = [0]
 
     def step(target=None):
         i = (step_no[0] * world + rank) % V4
         step_no[0] += 1
-        return training_step(eng, ds, adam, views[i], targets[i] if target is None else target)
+        loss, _ = tr.step(views[i], targets[i] if target is None else target, i)
+        return loss
 
     clocks = B.ClockSampler(local)
     clocks.start()
@@ -245,6 +249,8 @@ def config5(args, rank, world, local):
     barrier()
     clocks.mark(t_start, time.perf_counter())
     clk = clocks.stop()
+    tr.flush()
+    assert tr.skipped_steps == 0
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     # e2e: the step's input image from pinned host memory, loss read back
     host_t = torch.empty((H4, W4, 3), dtype=torch.float32, pin_memory=True)
@@ -266,14 +272,15 @@ def config5(args, rank, world, local):
         "config": {"workload": "config 5: G5 (ball scene, 2M), targets rendered from it, start perturbed "
                                "(mu + N(0, 0.01)); per step per rank (fit2d.training_step): fwd, "
                                "0.8 L1 + 0.2 (1 - SSIM) loss + pixel gradient, finite check, bwd, all-reduce, "
-                               "interval stats, regularizers, Adam (TrainConfig defaults)",
+                               "interval stats, regularizers, Adam (TrainConfig defaults); pipelined: the "
+                               "finite check and instance check are a device flag resolved at the next step",
                    "parallelism": f"view-parallel x{world}, NCCL all-reduce SUM of {N5 * 65 * 4 / 1e6:.0f} MB "
                                   "packed gradients + MAX of g_z"},
         "clocks": clk,
         "e2e": {"value": world / e2e_s, "unit": "views/s", "h2d_bytes_per_step": H4 * W4 * 12,
                 "d2h_bytes_per_step": 4, "path": "training_step with the target image copied from pinned "
                                                  "host memory and the loss read back each step"},
-        # per step: the frame's 14, image loss 2, regularizer 1, Adam 9 (rowcheck, 7 fields, renorm)
+        # per step: the frame's 13, image loss 2, regularizer 1, Adam 9 (rowcheck, 7 fields, renorm)
         "gpu_launches": (B.LAUNCHES_PER_FRAME + 12) * args.steps,
     }
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -169,6 +169,10 @@ typedef struct ssg_adam_state {
 typedef struct ssg_adam_hparams {
     int64_t t;                  /* step count after this step (>= 1) */
     double lr_mu, lr_scale, lr_rot, lr_sh, lr_opacity, lr_beta;
+    const int32_t *skip;        /* optional device flag: nonzero = this whole step is
+                                   skipped (no moment, parameter or quaternion update,
+                                   nothing counted), the device-side form of
+                                   fit2d.py:70-71 for pipelined training steps; NULL = run */
 } ssg_adam_hparams;
 
 /* ---- queries ---------------------------------------------------------- */
@@ -249,6 +253,10 @@ int ssg_regularize(int64_t n, const float *beta, const float *opacity_logits, co
  * mu_sum += d_mu */
 int ssg_interval_stats_add(int64_t n, const float *g_uv, const float *g_z, const float *d_mu,
                            double *uv_sum, float *z_max, double *mu_sum, void *stream);
+/* the same, skipped entirely when *skip != 0 (device flag; NULL = always add) */
+int ssg_interval_stats_add_ex(int64_t n, const float *g_uv, const float *g_z, const float *d_mu,
+                              double *uv_sum, float *z_max, double *mu_sum, const int32_t *skip,
+                              void *stream);
 /* optimize/adam.py:71-97 Adam.step on the device (skip non-finite rows,
  * bias-corrected moments, per-field learning rates, quaternion renorm) */
 int ssg_adam_step(const ssg_params *params, const ssg_grad_buffers *grads,

@@ -23,7 +23,7 @@ SSG_PREP_BWD_ACTIVE_ONLY = 1
 EXPORTS = ("ssg_abi_version", "ssg_last_error", "ssg_grid_dims", "ssg_bin_temp_bytes",
            "ssg_preprocess_forward", "ssg_bin_rects", "ssg_bin_prepare", "ssg_bin_finish", "ssg_blend_forward",
            "ssg_blend_backward", "ssg_preprocess_backward", "ssg_blend_backward_slots",
-           "ssg_zero_prim_grads", "ssg_preprocess_backward_ex",
+           "ssg_zero_prim_grads", "ssg_preprocess_backward_ex", "ssg_interval_stats_add_ex",
            "ssg_test_sort_temp_bytes",
            "ssg_test_sort", "ssg_test_blend_forward_vanilla", "ssg_adam_step", "ssg_blend_mask_words",
            "ssg_loss_scratch_floats", "ssg_image_loss", "ssg_regularize", "ssg_interval_stats_add",
@@ -93,11 +93,12 @@ class SsgDensifyCfg(ctypes.Structure):
 
 class SsgAdamHparams(ctypes.Structure):
     _fields_ = [("t", ctypes.c_int64)] + [(f, ctypes.c_double) for f in
-                                          ("lr_mu", "lr_scale", "lr_rot", "lr_sh", "lr_opacity", "lr_beta")]
+                                          ("lr_mu", "lr_scale", "lr_rot", "lr_sh", "lr_opacity", "lr_beta")] + \
+               [("skip", _vp)]
 
 
 SPLAT_BYTES = 64
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 _lib = None
 
@@ -159,6 +160,7 @@ def lib():
     L.ssg_image_loss.argtypes = [_vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_float, _vp, _vp, _vp, _vp]
     L.ssg_regularize.argtypes = [ctypes.c_int64, _vp, _vp, _vp, ctypes.c_float, ctypes.c_float, _vp, _vp, _vp, _vp]
     L.ssg_interval_stats_add.argtypes = [ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+    L.ssg_interval_stats_add_ex.argtypes = [ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
     L.ssg_blend_mask_words.restype = ctypes.c_int64
     L.ssg_blend_mask_words.argtypes = [ctypes.c_int64, ctypes.c_int32]
     if L.ssg_abi_version() != ABI_VERSION:

@@ -20,8 +20,13 @@ constexpr float kBeta1 = 0.9f, kBeta2 = 0.999f, kEps = 1e-15f;
 
 // One thread per primitive: is every gradient of the row finite
 // (adam.py:75-79)?  The (K,3) SH row is read as float4s when 16-byte aligned.
-__global__ void k_adam_rowcheck(int64_t n, int K, ssg_grad_buffers g, uint8_t *row_ok, int32_t *n_skipped) {
+__global__ void k_adam_rowcheck(int64_t n, int K, ssg_grad_buffers g, uint8_t *row_ok, int32_t *n_skipped,
+                                const int32_t *skip) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (skip && *skip) {  // the whole step is skipped (hp->skip): no row updates, nothing counted
+        if (i < n) row_ok[i] = 0;
+        return;
+    }
     bool ok = true;
     if (i < n) {
 #pragma unroll
@@ -130,9 +135,9 @@ static void launch_sh(int64_t n, float *p, const float *g, float *m, float *v, c
     launch_field<float, W>(n, p, g, m, v, row_ok, lr, c1, c2, st);
 }
 
-__global__ void k_quat_renorm(int64_t n, double *rot) {
+__global__ void k_quat_renorm(int64_t n, double *rot, const int32_t *skip) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= n || (skip && *skip)) return;
     double q[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) q[j] = rot[4 * i + j];
@@ -157,7 +162,7 @@ extern "C" int ssg_adam_step(const ssg_params *p, const ssg_grad_buffers *g, con
     const int K = p->sh_coeffs;
     if (K != 1 && K != 4 && K != 9 && K != 16) return SSG_ERR_INVALID_ARGUMENT;
     if (p->n * 3 * K >= (int64_t)UINT32_MAX) return SSG_ERR_CAPACITY;
-    k_adam_rowcheck<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, K, *g, s->row_ok, s->n_skipped);
+    k_adam_rowcheck<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, K, *g, s->row_ok, s->n_skipped, hp->skip);
     const double c1 = 1.0 - pow(0.9, (double)hp->t), c2 = 1.0 - pow(0.999, (double)hp->t);
     launch_field<double, 3>(n, p->mu, g->d_mu, s->m_mu, s->v_mu, s->row_ok, hp->lr_mu, c1, c2, st);
     launch_field<double, 3>(n, p->log_scale, g->d_log_scale, s->m_log_scale, s->v_log_scale, s->row_ok,
@@ -176,6 +181,6 @@ extern "C" int ssg_adam_step(const ssg_params *p, const ssg_grad_buffers *g, con
                                hp->lr_beta, c1, c2, st);
         launch_field<float, 3>(n, p->dir, g->d_eta, s->m_dir, s->v_dir, s->row_ok, hp->lr_beta, c1, c2, st);
     }
-    k_quat_renorm<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, p->rot);
+    k_quat_renorm<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, p->rot, hp->skip);
     return check_launch("ssg_adam_step");
 }

@@ -223,9 +223,9 @@ __global__ void k_regularize(int64_t n, const float *__restrict__ beta, const fl
 // trainer.py:49-53: uv_sum += g_uv; z_max = max(z_max, g_z); mu_sum += d_mu
 __global__ void k_stats_add(int64_t n, const float *__restrict__ g_uv, const float *__restrict__ g_z,
                             const float *__restrict__ d_mu, double *__restrict__ uv_sum, float *__restrict__ z_max,
-                            double *__restrict__ mu_sum) {
+                            double *__restrict__ mu_sum, const int32_t *__restrict__ skip) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= n || (skip && *skip)) return;
     uv_sum[i] += (double)g_uv[i];
     z_max[i] = fmaxf(z_max[i], g_z[i]);
     for (int j = 0; j < 3; j++) mu_sum[3 * i + j] += (double)d_mu[3 * i + j];
@@ -287,12 +287,18 @@ extern "C" int ssg_regularize(int64_t n, const float *beta, const float *opacity
     return check_launch("ssg_regularize");
 }
 
-extern "C" int ssg_interval_stats_add(int64_t n, const float *g_uv, const float *g_z, const float *d_mu,
-                                      double *uv_sum, float *z_max, double *mu_sum, void *stream) {
+extern "C" int ssg_interval_stats_add_ex(int64_t n, const float *g_uv, const float *g_z, const float *d_mu,
+                                         double *uv_sum, float *z_max, double *mu_sum, const int32_t *skip,
+                                         void *stream) {
     using namespace ssg;
     if (n < 0 || (n > 0 && (!g_uv || !g_z || !d_mu || !uv_sum || !z_max || !mu_sum))) return SSG_ERR_INVALID_ARGUMENT;
     if (n == 0) return SSG_OK;
     k_stats_add<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, g_uv, g_z, d_mu, uv_sum, z_max,
-                                                                               mu_sum);
+                                                                               mu_sum, skip);
     return check_launch("ssg_interval_stats_add");
+}
+
+extern "C" int ssg_interval_stats_add(int64_t n, const float *g_uv, const float *g_z, const float *d_mu,
+                                      double *uv_sum, float *z_max, double *mu_sum, void *stream) {
+    return ssg_interval_stats_add_ex(n, g_uv, g_z, d_mu, uv_sum, z_max, mu_sum, nullptr, stream);
 }

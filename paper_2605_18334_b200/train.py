@@ -154,12 +154,15 @@ class IntervalStats:
         self.mu_sum = torch.zeros((n, 3), dtype=torch.float64, device=device)
         self.steps = 0
 
-    def add(self, grads: DeviceGrads, views: int = 1):
+    def add(self, grads: DeviceGrads, views: int = 1, skip: torch.Tensor | None = None):
+        """`skip`: optional device int32 flag; nonzero = this step adds nothing
+        (the caller then takes the `views` back, see Trainer)."""
         n = self.uv_sum.numel()
-        N.check(N.lib().ssg_interval_stats_add(n, grads.g_uv.data_ptr(), grads.g_z.data_ptr(),
-                                               grads.d_mu.data_ptr(), self.uv_sum.data_ptr(),
-                                               self.z_max.data_ptr(), self.mu_sum.data_ptr(),
-                                               _stream(self.uv_sum.device)), "ssg_interval_stats_add")
+        N.check(N.lib().ssg_interval_stats_add_ex(n, grads.g_uv.data_ptr(), grads.g_z.data_ptr(),
+                                                  grads.d_mu.data_ptr(), self.uv_sum.data_ptr(),
+                                                  self.z_max.data_ptr(), self.mu_sum.data_ptr(),
+                                                  skip.data_ptr() if skip is not None else None,
+                                                  _stream(self.uv_sum.device)), "ssg_interval_stats_add_ex")
         self.steps += views
 
     def bundle(self):
@@ -190,9 +193,11 @@ class DeviceAdam:
         self.row_ok = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
         self.n_skipped_dev = torch.zeros(1, dtype=torch.int32, device=dev)  # accumulated, adam.py:79
 
-    def step(self, grads, iteration: int = 0, d_beta: torch.Tensor | None = None) -> None:
+    def step(self, grads, iteration: int = 0, d_beta: torch.Tensor | None = None,
+             skip: torch.Tensor | None = None) -> None:
         """adam.py:71-97; `d_beta` (d_eta + regularizer) drives beta, d_eta
-        drives dir."""
+        drives dir.  `skip`: optional device int32 flag, nonzero = the step is
+        skipped on the device (the caller then takes `t` back, see Trainer)."""
         ds, cfg = self.ds, self.cfg
         if ds.n == 0:
             return
@@ -216,6 +221,7 @@ class DeviceAdam:
         hp.t = self.t
         hp.lr_mu, hp.lr_scale, hp.lr_rot = cfg.position_lr_at(iteration), cfg.lr_scale, cfg.lr_rot
         hp.lr_sh, hp.lr_opacity, hp.lr_beta = cfg.lr_sh, cfg.lr_opacity, cfg.lr_beta
+        hp.skip = skip.data_ptr() if skip is not None else None
         N.check(N.lib().ssg_adam_step(ctypes.byref(p), ctypes.byref(g), ctypes.byref(s), ctypes.byref(hp),
                                       _stream(ds.mu.device)), "ssg_adam_step")
 
@@ -226,13 +232,32 @@ class DeviceAdam:
 
 
 class Trainer:
-    """Per-image-size scratch (loss, regularizer buffers) for training_step."""
+    """Per-image-size scratch (loss, regularizer buffers) for training_step.
 
-    def __init__(self, eng: Engine, ds: DeviceScene, adam: DeviceAdam, cfg: TrainConfig | None = None):
+    pipelined=True runs each step without a host read-back: the finite-loss
+    branch of fit2d.py:70-71 and the instance-capacity check become a device
+    flag (0 run, 1 non-finite loss, 2 instance overflow; MAX over ranks) that
+    Adam and the interval statistics consume, so the update is skipped on the
+    device exactly when the synchronous step would skip it.  The flag is read
+    back asynchronously and checked when the next step starts (or at
+    flush()): a skipped step takes back the host's Adam step count and the
+    statistics' view count, and an overflowed step (its lists were truncated,
+    so its update was skipped) is re-run synchronously with grown buffers
+    before anything else is queued -- the same parameters as the synchronous
+    loop.  Call flush() before reading parameters (or the loss tensor of the
+    last step) between steps."""
+
+    def __init__(self, eng: Engine, ds: DeviceScene, adam: DeviceAdam, cfg: TrainConfig | None = None,
+                 pipelined: bool = False):
         self.eng, self.ds, self.adam = eng, ds, adam
         self.cfg = cfg or adam.cfg
         self._loss = {}
         self.d_beta = None
+        self.pipelined = pipelined
+        self._pending = None
+        self._skip_dev = torch.zeros(1, dtype=torch.int32, device=eng.device)
+        self._skip_host = torch.zeros(1, dtype=torch.int32, pin_memory=True) if pipelined else None
+        self.skipped_steps = 0  # pipelined steps skipped on the device (non-finite loss)
 
     def loss_for(self, W: int, H: int) -> ImageLoss:
         key = (W, H)
@@ -240,9 +265,71 @@ class Trainer:
             self._loss[key] = ImageLoss(W, H, self.cfg.lambda_ssim, self.eng.device)
         return self._loss[key]
 
+    def flush(self) -> None:
+        """Resolve the last pipelined step (see the class docstring)."""
+        if self._pending is None:
+            return
+        ev, args, loss = self._pending
+        self._pending = None
+        ev.synchronize()
+        code = int(self._skip_host[0])
+        if code == 0:
+            return
+        view, target, iteration, stats, s, group = args
+        self.adam.t -= 1  # the device skipped this step's update
+        if stats is not None:
+            stats.steps -= _world(group)
+        if code == 1:  # non-finite loss: skipped, as fit2d.py:70-71
+            self.skipped_steps += 1
+            return
+        try:  # instance overflow: grow the buffers and run the step for real
+            self.eng.instances()
+        except N.NativeError:
+            pass
+        redo, _ = self._step_sync(view, target, iteration, stats, s, group, True)
+        loss.copy_(redo)  # the step's returned loss becomes the re-run's
+
     def step(self, view, target: torch.Tensor, iteration: int, stats: IntervalStats | None = None,
              s: float = 0.3, group=None, check_finite: bool = True):
         """fit2d.py:62-78.  Returns (loss tensor of this rank, frame)."""
+        if not self.pipelined:
+            return self._step_sync(view, target, iteration, stats, s, group, check_finite)
+        self.flush()
+        eng, ds, cfg = self.eng, self.ds, self.cfg
+        f = eng.forward(ds, view, s, sync=False)
+        lossfn = self.loss_for(f.width, f.height)
+        dL = lossfn(f.color, target)
+        n = ds.n
+        if self.d_beta is None or self.d_beta.shape[0] < n:
+            self.d_beta = torch.empty((max(n, 1), 3), dtype=torch.float32, device=eng.device)
+        lossfn.sums[2].zero_()
+        v = lossfn.value_tensor()
+        # the step's fate on the device: 2 overflow > 1 non-finite > 0 run
+        over = eng.n_inst_dev[1] > eng.capacity
+        code = torch.where(over, 2, torch.where(torch.isfinite(v), 0, 1).to(torch.int64))
+        self._skip_dev.copy_(code.reshape(1))
+        if _world(group) > 1:
+            dist.all_reduce(self._skip_dev, op=dist.ReduceOp.MAX, group=group)
+        # read the flag back now: waiting for it at the next step then waits
+        # for this step's forward and loss only, not for its backward + Adam
+        self._skip_host.copy_(self._skip_dev, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        grads = eng.backward(ds, view, s, f.final_T, f.last_idx, dL, rebin=False)
+        allreduce_gradients(grads, group)
+        if stats is not None:
+            stats.add(grads, views=_world(group), skip=self._skip_dev)
+        N.check(N.lib().ssg_regularize(n, ds.beta.data_ptr(), ds.opacity_logits.data_ptr(), grads.d_eta.data_ptr(),
+                                       cfg.lambda_beta_reg, cfg.lambda_opacity_reg, self.d_beta.data_ptr(),
+                                       grads.d_opacity_logits.data_ptr(), lossfn.sums.data_ptr(),
+                                       _stream(eng.device)), "ssg_regularize")
+        self.adam.step(grads, iteration, d_beta=self.d_beta[:n], skip=self._skip_dev)
+        loss = lossfn.value_tensor()
+        self._pending = (ev, (view, target, iteration, stats, s, group), loss)
+        return loss, f
+
+    def _step_sync(self, view, target: torch.Tensor, iteration: int, stats: IntervalStats | None,
+                   s: float, group, check_finite: bool):
         eng, ds, cfg = self.eng, self.ds, self.cfg
         f = eng.forward(ds, view, s, sync=False)  # M is checked with the loss below
         lossfn = self.loss_for(f.width, f.height)
