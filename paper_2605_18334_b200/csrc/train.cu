@@ -16,13 +16,13 @@
 //
 // The 11x11 window is the outer product of one normalised 1-D Gaussian, so
 // every windowed mean is two 11-tap passes over a shared-memory tile.  One
-// CTA produces a 16x16 block of outputs for all three channels; the loss
+// CTA produces a 32x32 block of outputs, channel by channel; the loss
 // values are accumulated in fp64 with one atomic per CTA.
 #include "ssg_common.cuh"
 
 namespace ssg {
 
-constexpr int kWin = 11, kHalo = kWin - 1, kLT = 16, kLR = kLT + kHalo;  // tile, tile + halo
+constexpr int kWin = 11, kHalo = kWin - 1;
 constexpr float kC1 = 0.01f * 0.01f, kC2 = 0.03f * 0.03f;
 
 __constant__ float c_gauss[kWin];
@@ -40,21 +40,42 @@ __device__ __forceinline__ double block_sum(double v, double *s_red) {
     return tot;
 }
 
+// The two passes below work on 32x32 output blocks (256 threads) one
+// channel at a time.  Both separable 11-tap passes are register-blocked: a
+// horizontal task produces 4 adjacent outputs of one row from 14 staged
+// inputs, a vertical task 4 adjacent outputs of one column from 14 rows, so
+// each shared-memory load feeds ~4 FMAs instead of 1.  The adjoint maps are
+// planar in `gm` ([3c + k][Hv][Wv]): coalesced stores and loads.
+constexpr int kBT = 32, kBR = kBT + kHalo, kBS = kBR + 1;  // block, block + halo, padded row stride
+constexpr int kGrp = kBT / 4;                               // 4-wide groups per block row
+
+// 11-tap weighted sums of 4 consecutive outputs from 14 inputs
+__device__ __forceinline__ void taps4(const float (&v)[14], float (&o)[4]) {
+#pragma unroll
+    for (int q = 0; q < 4; q++) o[q] = 0.f;
+#pragma unroll
+    for (int u = 0; u < kWin; u++) {
+        const float w = c_gauss[u];
+#pragma unroll
+        for (int q = 0; q < 4; q++) o[q] = fmaf(w, v[q + u], o[q]);
+    }
+}
+
 // Pass 1: per valid window (output (i, j) covers input rows i..i+10, columns
 // j..j+10) and channel: SSIM s and the three adjoint maps of losses.py:86-93
-// (g_mu_x, g_wxx, g_wxy), plus the L1 and SSIM sums.  gm layout: (Hv, Wv, 9).
-__global__ void __launch_bounds__(kLT * kLT) k_loss_stats(const float *__restrict__ img, const float *__restrict__ tgt,
-                                                          int H, int W, int with_ssim, float inv_n,
-                                                          float *__restrict__ gm, double *__restrict__ sums) {
-    __shared__ float sx[3][kLR][kLR], sy[3][kLR][kLR];
-    __shared__ float hs[5][3][kLR][kLT];
-    __shared__ double s_red[kLT * kLT / 32];
-    const int tx = threadIdx.x % kLT, ty = threadIdx.x / kLT;
-    const int i0 = blockIdx.y * kLT, j0 = blockIdx.x * kLT;
+// (g_mu_x, g_wxx, g_wxy), plus the L1 and SSIM sums.
+__global__ void __launch_bounds__(256) k_loss_stats(const float *__restrict__ img, const float *__restrict__ tgt,
+                                                    int H, int W, int with_ssim, float inv_n,
+                                                    float *__restrict__ gm, double *__restrict__ sums) {
+    __shared__ float sx[kBR * kBS], sy[kBR * kBS];
+    __shared__ float hs[5][kBR][kBT + 1];  // +1: conflict-free 4-wide row writes
+    __shared__ double s_red[8];
+    const int t = threadIdx.x;
+    const int i0 = blockIdx.y * kBT, j0 = blockIdx.x * kBT;
     double l1 = 0.0, ss = 0.0;
-    // L1 over the tile's own 16x16 pixels (every pixel counted once)
-    {
-        const int i = i0 + ty, j = j0 + tx;
+    // L1 over the block's own pixels (every pixel counted once)
+    for (int q = t; q < kBT * kBT; q += 256) {
+        const int i = i0 + q / kBT, j = j0 + q % kBT;
         if (i < H && j < W)
             for (int c = 0; c < 3; c++) {
                 const size_t p = ((size_t)i * W + j) * 3 + c;
@@ -62,71 +83,86 @@ __global__ void __launch_bounds__(kLT * kLT) k_loss_stats(const float *__restric
             }
     }
     if (with_ssim) {
-        for (int q = threadIdx.x; q < kLR * kLR; q += blockDim.x) {
-            const int r = q / kLR, cc = q % kLR;
-            const int i = i0 + r, j = j0 + cc;
-            const bool in = i < H && j < W;
-            for (int c = 0; c < 3; c++) {
-                const size_t p = ((size_t)i * W + j) * 3 + c;
-                sx[c][r][cc] = in ? img[p] : 0.0f;
-                sy[c][r][cc] = in ? tgt[p] : 0.0f;
-            }
-        }
-        __syncthreads();
-        // horizontal pass: rows 0..kLR-1 of the region, output columns 0..kLT-1
-        for (int q = threadIdx.x; q < kLR * kLT; q += blockDim.x) {
-            const int r = q / kLT, cc = q % kLT;
-            for (int c = 0; c < 3; c++) {
-                float a = 0.f, b = 0.f, xx = 0.f, yy = 0.f, xy = 0.f;
-#pragma unroll
-                for (int u = 0; u < kWin; u++) {
-                    const float wgt = c_gauss[u], x = sx[c][r][cc + u], y = sy[c][r][cc + u];
-                    a = fmaf(wgt, x, a);
-                    b = fmaf(wgt, y, b);
-                    xx = fmaf(wgt, x * x, xx);
-                    yy = fmaf(wgt, y * y, yy);
-                    xy = fmaf(wgt, x * y, xy);
-                }
-                hs[0][c][r][cc] = a;
-                hs[1][c][r][cc] = b;
-                hs[2][c][r][cc] = xx;
-                hs[3][c][r][cc] = yy;
-                hs[4][c][r][cc] = xy;
-            }
-        }
-        __syncthreads();
         const int Hv = H - kHalo, Wv = W - kHalo;
-        const int i = i0 + ty, j = j0 + tx;
-        if (i < Hv && j < Wv) {
-            for (int c = 0; c < 3; c++) {
-                float st[5];
+        const size_t plane = (size_t)Hv * Wv;
+        const int vx = t % kBT, vg = t / kBT;  // vertical task: column vx, rows 4vg..4vg+3
+        for (int c = 0; c < 3; c++) {
+            for (int q = t; q < kBR * kBR; q += 256) {
+                const int r = q / kBR, cc = q % kBR;
+                const int i = i0 + r, j = j0 + cc;
+                const bool in = i < H && j < W;
+                const size_t p = ((size_t)i * W + j) * 3 + c;
+                sx[r * kBS + cc] = in ? img[p] : 0.0f;
+                sy[r * kBS + cc] = in ? tgt[p] : 0.0f;
+            }
+            __syncthreads();
+            // horizontal: row r, columns 4g..4g+3 of the block
+            for (int q = t; q < kBR * kGrp; q += 256) {
+                const int r = q / kGrp, g = q % kGrp;
+                float x[14], y[14], o[4];
 #pragma unroll
-                for (int k = 0; k < 5; k++) {
-                    float acc = 0.f;
-#pragma unroll
-                    for (int u = 0; u < kWin; u++) acc = fmaf(c_gauss[u], hs[k][c][ty + u][tx], acc);
-                    st[k] = acc;
+                for (int u = 0; u < 14; u++) {
+                    x[u] = sx[r * kBS + 4 * g + u];
+                    y[u] = sy[r * kBS + 4 * g + u];
                 }
-                const float mx = st[0], my = st[1];
-                const float vx = st[2] - mx * mx, vy = st[3] - my * my, cov = st[4] - mx * my;
+                taps4(x, o);
+#pragma unroll
+                for (int k = 0; k < 4; k++) hs[0][r][4 * g + k] = o[k];
+                taps4(y, o);
+#pragma unroll
+                for (int k = 0; k < 4; k++) hs[1][r][4 * g + k] = o[k];
+                float pr[14];
+#pragma unroll
+                for (int u = 0; u < 14; u++) pr[u] = x[u] * x[u];
+                taps4(pr, o);
+#pragma unroll
+                for (int k = 0; k < 4; k++) hs[2][r][4 * g + k] = o[k];
+#pragma unroll
+                for (int u = 0; u < 14; u++) pr[u] = y[u] * y[u];
+                taps4(pr, o);
+#pragma unroll
+                for (int k = 0; k < 4; k++) hs[3][r][4 * g + k] = o[k];
+#pragma unroll
+                for (int u = 0; u < 14; u++) pr[u] = x[u] * y[u];
+                taps4(pr, o);
+#pragma unroll
+                for (int k = 0; k < 4; k++) hs[4][r][4 * g + k] = o[k];
+            }
+            __syncthreads();
+            // vertical: column vx, rows 4vg..4vg+3 -> SSIM terms
+            float st[5][4];
+#pragma unroll
+            for (int m = 0; m < 5; m++) {
+                float v[14];
+#pragma unroll
+                for (int u = 0; u < 14; u++) v[u] = hs[m][4 * vg + u][vx];
+                taps4(v, st[m]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const int i = i0 + 4 * vg + q, j = j0 + vx;
+                if (i >= Hv || j >= Wv) continue;
+                const float mx = st[0][q], my = st[1][q];
+                const float vxx = st[2][q] - mx * mx, vyy = st[3][q] - my * my, cov = st[4][q] - mx * my;
                 const float a1 = 2.f * mx * my + kC1, a2 = 2.f * cov + kC2;
-                const float b1 = mx * mx + my * my + kC1, b2 = vx + vy + kC2;
-                const float s = (a1 * a2) / (b1 * b2);
-                ss += s;
+                const float b1 = mx * mx + my * my + kC1, b2 = vxx + vyy + kC2;
+                const float sv = (a1 * a2) / (b1 * b2);
+                ss += sv;
                 // losses.py:86-93, divided by n = Hv * Wv * 3
                 const float g_a1 = a2 / (b1 * b2) * inv_n, g_a2 = a1 / (b1 * b2) * inv_n;
-                const float g_b1 = -s / b1 * inv_n, g_b2 = -s / b2 * inv_n;
+                const float g_b1 = -sv / b1 * inv_n, g_b2 = -sv / b2 * inv_n;
                 const float g_mu = 2.f * my * g_a1 + 2.f * mx * g_b1 - 2.f * mx * g_b2 - my * 2.f * g_a2;
-                float *o = gm + ((size_t)i * Wv + j) * 9 + 3 * c;
-                o[0] = g_mu;
-                o[1] = g_b2;
-                o[2] = 2.f * g_a2;
+                const size_t o = (size_t)i * Wv + j;
+                gm[(3 * c) * plane + o] = g_mu;
+                gm[(3 * c + 1) * plane + o] = g_b2;
+                gm[(3 * c + 2) * plane + o] = 2.f * g_a2;
             }
+            __syncthreads();  // sx / sy / hs reused by the next channel
         }
     }
     const double t1 = block_sum(l1, s_red);
     const double t2 = block_sum(ss, s_red);
-    if (threadIdx.x == 0) {
+    if (t == 0) {
         atomicAdd(&sums[0], t1);
         if (with_ssim) atomicAdd(&sums[1], t2);
     }
@@ -135,55 +171,59 @@ __global__ void __launch_bounds__(kLT * kLT) k_loss_stats(const float *__restric
 // Pass 2: dL/dpixel = (1 - l) sign(x - y) / size - l * dSSIM/dx, with
 // dSSIM/dx = full(g_mu) + 2 x full(g_wxx) + y full(g_wxy) (losses.py:94-96,
 // 112).  Full convolution: output (i, j) gathers windows i-10..i, j-10..j.
-__global__ void __launch_bounds__(kLT * kLT) k_loss_grad(const float *__restrict__ img, const float *__restrict__ tgt,
-                                                         const float *__restrict__ gm, int H, int W, int with_ssim,
-                                                         float w_l1, float w_ssim, float *__restrict__ dL) {
-    __shared__ float sg[9][kLR][kLR];
-    __shared__ float hs[9][kLR][kLT];
-    const int tx = threadIdx.x % kLT, ty = threadIdx.x / kLT;
-    const int i0 = blockIdx.y * kLT, j0 = blockIdx.x * kLT;
+__global__ void __launch_bounds__(256) k_loss_grad(const float *__restrict__ img, const float *__restrict__ tgt,
+                                                   const float *__restrict__ gm, int H, int W, int with_ssim,
+                                                   float w_l1, float w_ssim, float *__restrict__ dL) {
+    __shared__ float sg[3][kBR * kBS];
+    __shared__ float hs[3][kBR][kBT + 1];
+    const int t = threadIdx.x;
+    const int i0 = blockIdx.y * kBT, j0 = blockIdx.x * kBT;
     const int Hv = H - kHalo, Wv = W - kHalo;
-    if (with_ssim) {
-        // region rows i0-10 .. i0+15, columns j0-10 .. j0+15 of the gm maps
-        for (int q = threadIdx.x; q < kLR * kLR; q += blockDim.x) {
-            const int r = q / kLR, cc = q % kLR;
-            const int i = i0 - kHalo + r, j = j0 - kHalo + cc;
-            const bool in = i >= 0 && j >= 0 && i < Hv && j < Wv;
-            const float *src = gm + ((size_t)(in ? i : 0) * Wv + (in ? j : 0)) * 9;
-#pragma unroll
-            for (int k = 0; k < 9; k++) sg[k][r][cc] = in ? src[k] : 0.0f;
-        }
-        __syncthreads();
-        for (int q = threadIdx.x; q < kLR * kLT; q += blockDim.x) {
-            const int r = q / kLT, cc = q % kLT;
-#pragma unroll
-            for (int k = 0; k < 9; k++) {
-                float acc = 0.f;
-#pragma unroll
-                for (int u = 0; u < kWin; u++) acc = fmaf(c_gauss[u], sg[k][r][cc + u], acc);
-                hs[k][r][cc] = acc;
-            }
-        }
-        __syncthreads();
-    }
-    const int i = i0 + ty, j = j0 + tx;
-    if (i >= H || j >= W) return;
+    const size_t plane = (size_t)(with_ssim ? Hv : 0) * (with_ssim ? Wv : 0);
+    const int vx = t % kBT, vg = t / kBT;
     for (int c = 0; c < 3; c++) {
-        const size_t p = ((size_t)i * W + j) * 3 + c;
-        const float x = img[p], y = tgt[p], d = x - y;
-        float g = w_l1 * (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f));
+        float f[3][4];
         if (with_ssim) {
-            float f[3];
+            // gm rows i0-10 .. i0+31, columns j0-10 .. j0+31 of channel c's three maps
+            for (int q = t; q < kBR * kBR; q += 256) {
+                const int r = q / kBR, cc = q % kBR;
+                const int i = i0 - kHalo + r, j = j0 - kHalo + cc;
+                const bool in = i >= 0 && j >= 0 && i < Hv && j < Wv;
+                const size_t o = in ? (size_t)i * Wv + j : 0;
+#pragma unroll
+                for (int k = 0; k < 3; k++) sg[k][r * kBS + cc] = in ? gm[(3 * c + k) * plane + o] : 0.0f;
+            }
+            __syncthreads();
+            for (int q = t; q < 3 * kBR * kGrp; q += 256) {
+                const int k = q / (kBR * kGrp), rem = q % (kBR * kGrp);
+                const int r = rem / kGrp, g = rem % kGrp;
+                float v[14], o[4];
+#pragma unroll
+                for (int u = 0; u < 14; u++) v[u] = sg[k][r * kBS + 4 * g + u];
+                taps4(v, o);
+#pragma unroll
+                for (int e = 0; e < 4; e++) hs[k][r][4 * g + e] = o[e];
+            }
+            __syncthreads();
 #pragma unroll
             for (int k = 0; k < 3; k++) {
-                float acc = 0.f;
+                float v[14];
 #pragma unroll
-                for (int u = 0; u < kWin; u++) acc = fmaf(c_gauss[u], hs[3 * c + k][ty + u][tx], acc);
-                f[k] = acc;
+                for (int u = 0; u < 14; u++) v[u] = hs[k][4 * vg + u][vx];
+                taps4(v, f[k]);
             }
-            g -= w_ssim * (f[0] + 2.f * x * f[1] + y * f[2]);
         }
-        dL[p] = g;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int i = i0 + 4 * vg + q, j = j0 + vx;
+            if (i >= H || j >= W) continue;
+            const size_t p = ((size_t)i * W + j) * 3 + c;
+            const float x = img[p], y = tgt[p], d = x - y;
+            float g = w_l1 * (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f));
+            if (with_ssim) g -= w_ssim * (f[0][q] + 2.f * x * f[1][q] + y * f[2][q]);
+            dL[p] = g;
+        }
+        if (with_ssim) __syncthreads();  // sg / hs reused by the next channel
     }
 }
 
@@ -263,12 +303,12 @@ extern "C" int ssg_image_loss(const float *rendered, const float *target, int32_
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(sums, 0, 2 * sizeof(double), st);
     if (e != cudaSuccess) { set_error("memset sums", e); return SSG_ERR_CUDA; }
-    const dim3 grid((width + kLT - 1) / kLT, (height + kLT - 1) / kLT);
+    const dim3 grid((width + kBT - 1) / kBT, (height + kBT - 1) / kBT);
     const float inv_n = with_ssim ? 1.0f / (3.0f * (float)(width - kHalo) * (float)(height - kHalo)) : 0.0f;
-    k_loss_stats<<<grid, kLT * kLT, 0, st>>>(rendered, target, height, width, with_ssim, inv_n, scratch, sums);
+    k_loss_stats<<<grid, 256, 0, st>>>(rendered, target, height, width, with_ssim, inv_n, scratch, sums);
     const float w_l1 = (1.0f - lambda_ssim) / (3.0f * (float)width * (float)height);
-    k_loss_grad<<<grid, kLT * kLT, 0, st>>>(rendered, target, scratch, height, width, with_ssim, w_l1, lambda_ssim,
-                                            dL_dpixels);
+    k_loss_grad<<<grid, 256, 0, st>>>(rendered, target, scratch, height, width, with_ssim, w_l1, lambda_ssim,
+                                      dL_dpixels);
     return check_launch("ssg_image_loss");
 }
 
