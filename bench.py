@@ -420,13 +420,14 @@ def main():
     t_dom = stage_ms[dom] * 1e-3
     achieved = FP32_PER_PAIR[dom] * pairs / t_dom
     kname = {"blend_fwd": "k_blend_forward", "blend_bwd": "k_blend_backward"}[dom]
-    try:  # DRAM bytes of the kernel from the committed ncu --set full capture
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(kname)
+    try:  # DRAM bytes and issue-slot utilisation of the kernel from the committed ncu --set full capture
+        ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic, issue_busy = ncu.get(kname), ncu.get("issue_slots_busy", {}).get(kname)
     except (OSError, ValueError):
-        traffic = None
+        traffic, issue_busy = None, None
     roofline = {"bound": "fp32", "kernel": kname,
                 "achieved": achieved / 1e12, "peak": r_fp32 / 1e12, "unit": "Tinstr/s (FP32 lane)",
-                "frac": achieved / r_fp32, "traffic": traffic,
+                "frac": achieved / r_fp32, "traffic": traffic, "ncu_issue_slots_busy": issue_busy,
                 "traffic_note": "DRAM bytes per launch (profiles/ncu_traffic.json); the blend kernels are "
                                 "issue-bound, DRAM ~1 % busy",
                 "algorithmic": f"{FP32_PER_PAIR[dom]} FP32 instr/pair x {pairs} tile-synchronous "
