@@ -169,6 +169,10 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
     float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
     int nc = 0, li = -1;
     int done = !inside;
+#ifdef SSG_BLEND_STATS
+    __shared__ int sTileH[kThreads / 32];
+    if (lane == 0) sTileH[warp] = 0;
+#endif
     const uint32_t aA = smem_addr(s.A), aB = smem_addr(s.B), aC = smem_addr(s.C);
     const uint32_t aX = smem_addr(s.X), aD = smem_addr(s.D);
 
@@ -178,6 +182,9 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
             stage_splat(splat, inst_prim[base + threadIdx.x], ox, oy, s, threadIdx.x);
         __syncthreads();
         const int cnt = min(kBatch, end - base);
+#ifdef SSG_BLEND_STATS
+        int bh = 0;  // this warp's hits in the batch (imbalance diagnostics)
+#endif
         for (int c0 = 0; c0 < cnt; c0 += 32) {
             if (__all_sync(0xffffffffu, done)) break;
             const int i = c0 + lane;
@@ -188,6 +195,7 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
             uint32_t lbits = 0;  // instances of this chunk the lane's pixel blended
 #ifdef SSG_BLEND_STATS
             if (lane == 0) SSG_STAT(0, __popc(mask));
+            bh += __popc(mask);
 #endif
             while (mask) {
                 const int bit = __ffs(mask) - 1;
@@ -239,7 +247,31 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
                 if (lane == 0) blend_mask[mask_word(start, tile, (base - start + c0) >> 5, warp)] = bmask;
             }
         }
+#ifdef SSG_BLEND_STATS
+        {   // per batch: the slowest warp's hits vs the warps' total (barrier imbalance)
+            __shared__ int sH[kThreads / 32];
+            if (lane == 0) sH[warp] = bh;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int mx = 0, sm = 0;
+                for (int w = 0; w < kThreads / 32; w++) { mx = max(mx, sH[w]); sm += sH[w]; }
+                SSG_STAT(2, mx);
+                SSG_STAT(3, sm);
+            }
+            if (lane == 0) sTileH[warp] += bh;
+            __syncthreads();
+        }
+#endif
     }
+#ifdef SSG_BLEND_STATS
+    __syncthreads();
+    if (threadIdx.x == 0) {  // per tile: the slowest warp's hits vs the total
+        int mx = 0, sm = 0;
+        for (int w = 0; w < kThreads / 32; w++) { mx = max(mx, sTileH[w]); sm += sTileH[w]; }
+        SSG_STAT(4, mx);
+        SSG_STAT(5, sm);
+    }
+#endif
     if (inside) {  // :158-166
         const int64_t pix = (int64_t)py * W + px;
         color[3 * pix] = C0 + T * bg0;

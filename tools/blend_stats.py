@@ -17,6 +17,8 @@ from paper_2605_18334_b200.engine import DeviceScene, Engine
 from paper_2605_18334_b200.synthetic import frustum_scene, frustum_view
 
 NAMES = {0: "fwd hits (warp x instance, exact ellipse test)", 1: "fwd hits with a blending pixel",
+         2: "fwd sum over batches of the slowest warp's hits", 3: "fwd sum over batches of all warps' hits",
+         4: "fwd sum over tiles of the slowest warp's hits", 5: "fwd sum over tiles of all warps' hits",
          16: "bwd visited (warp x instance)", 17: "bwd visited with a contributing pixel",
          18: "bwd contributing pixels"}
 
@@ -38,6 +40,9 @@ def main():
     for i, name in NAMES.items():
         print(f"{i:3d} {name:45s} {buf[i]:>16,d}")
     print("M", f.n_instances)
+    if buf[3]:
+        print(f"fwd barrier imbalance: 8 x max / total = {8 * buf[2] / buf[3]:.3f} per batch, "
+              f"{8 * buf[4] / max(buf[5], 1):.3f} per tile (1 = balanced)")
 
 
 if __name__ == "__main__":
