@@ -29,6 +29,9 @@ def _ptr(t):
 def densify_and_prune(ds: DeviceScene, stats, cfg, adam=None, max_radii=None) -> dict:
     """stats: g_uv (n) fp64, g_z (n) fp32, d_mu (n,3) fp64 device tensors
     (IntervalStats.bundle()); mutates ds, adam, cfg.tau_z and stats.g_z."""
+    tr = getattr(adam, "_trainer", None)
+    if tr is not None and getattr(tr, "pipelined", False):
+        tr.flush()  # resolve the last pipelined step before the scene changes
     n = ds.n
     report = {"n_cloned": 0, "n_split": 0, "n_pruned": 0, "n_primitives": n}
     if n == 0:

@@ -166,6 +166,9 @@ class IntervalStats:
         self.steps += views
 
     def bundle(self):
+        tr = getattr(self, "_trainer", None)
+        if tr is not None:  # a pipelined step may still owe its view-count correction
+            tr.flush()
         d = max(self.steps, 1)
         return dataclasses.make_dataclass("Stats", ["g_uv", "g_z", "d_mu"])(
             self.uv_sum / d, self.z_max, self.mu_sum / d)
@@ -258,6 +261,8 @@ class Trainer:
         self._skip_dev = torch.zeros(1, dtype=torch.int32, device=eng.device)
         self._skip_host = torch.zeros(1, dtype=torch.int32, pin_memory=True) if pipelined else None
         self.skipped_steps = 0  # pipelined steps skipped on the device (non-finite loss)
+        if pipelined:
+            adam._trainer = self  # densify_and_prune flushes through it
 
     def loss_for(self, W: int, H: int) -> ImageLoss:
         key = (W, H)
@@ -318,6 +323,7 @@ class Trainer:
         grads = eng.backward(ds, view, s, f.final_T, f.last_idx, dL, rebin=False)
         allreduce_gradients(grads, group)
         if stats is not None:
+            stats._trainer = self  # bundle() flushes first
             stats.add(grads, views=_world(group), skip=self._skip_dev)
         N.check(N.lib().ssg_regularize(n, ds.beta.data_ptr(), ds.opacity_logits.data_ptr(), grads.d_eta.data_ptr(),
                                        cfg.lambda_beta_reg, cfg.lambda_opacity_reg, self.d_beta.data_ptr(),
@@ -372,9 +378,9 @@ def training_step(eng: Engine, ds: DeviceScene, adam: DeviceAdam, view, target: 
                   group=None) -> torch.Tensor:
     """One view-parallel step (fit2d.py:62-78 + the gradient all-reduce).
     Returns the (device) loss of this rank."""
-    tr = getattr(adam, "_trainer", None)
+    tr = getattr(adam, "_step_trainer", None)
     if tr is None or tr.eng is not eng or tr.ds is not ds:
         tr = Trainer(eng, ds, adam)
-        adam._trainer = tr
+        adam._step_trainer = tr
     loss, _ = tr.step(view, target, iteration, stats=stats, s=s, group=group)
     return loss

@@ -109,3 +109,34 @@ def test_pipelined_overflow_reruns_the_step():
     _close(start, views, targets, a, b)
     assert a[1].t == b[1].t == 8
     assert b[2].steps == 8
+
+
+def test_pipelined_flushes_before_densify():
+    """stats.bundle() and densify_and_prune resolve the pending step first:
+    the skipped step (non-finite loss just before densification) is not
+    counted in the statistics nor in Adam's step count."""
+    from paper_2605_18334_b200.densify import densify_and_prune
+    start, views, targets = _setup(4)
+    eng = Engine()
+    ds = DeviceScene.from_host(start)
+    cfg = TrainConfig()
+    adam = DeviceAdam(ds, cfg)
+    stats = IntervalStats(ds.n, eng.device)
+    tr = Trainer(eng, ds, adam, pipelined=True)
+    for it in range(4):
+        tgt = targets[it % 3]
+        if it == 3:
+            tgt = tgt.clone()
+            tgt[1, 1, 1] = float("nan")
+        tr.step(views[it % 3], tgt, it, stats=stats)
+    b = stats.bundle()  # flushes: step 3 was skipped on the device
+    assert stats.steps == 3 and adam.t == 3 and tr.skipped_steps == 1
+    rep = densify_and_prune(ds, b, cfg, adam=adam)
+    assert rep["n_primitives"] == ds.n
+    stats = IntervalStats(ds.n, eng.device)
+    for it in range(4, 7):
+        tr.step(views[it % 3], targets[it % 3], it, stats=stats)
+    tr.flush()
+    assert adam.t == 6 and stats.steps == 3
+    for f in FIELDS:
+        assert bool(torch.isfinite(getattr(ds, f)).all()), f
