@@ -401,11 +401,9 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
 #ifdef SSG_BLEND_STATS
             if (lane == 0) SSG_STAT(16, __popc(mask));
 #endif
-            while (mask) {
-                const int bit = 31 - __clz(mask);
-                mask &= ~(1u << bit);
-                const int j = c0 + bit;
-                const int k = lo + j;
+            // per-lane replay of instance j (global index k): updates T, R
+            // and writes the 12 slot values g (zero off-contribution)
+            auto replay = [&](int j, int k, float (&g)[12], bool &live, bool &contrib) {
                 // Branch-free per lane (every visited instance has a
                 // contributing pixel, so no warp-wide skip is lost): lanes that
                 // do not contribute compute with a zero weight and keep T, R;
@@ -416,8 +414,7 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                 const float cb = lds32(aD + 4 * j);
                 const float dx = fx - A.x, dy = fy - A.y;
                 const float power = -0.5f * (A.z * dx * dx + B.x * dy * dy) - A.w * dx * dy;
-                const bool live = k <= li && power >= B.y && power <= 0.0f;                // :263-264, :265-269
-                if (!blend_mask && !__any_sync(0xffffffffu, live)) continue;  // test-driven walk: empty hit
+                live = k <= li && power >= B.y && power <= 0.0f;                           // :263-264, :265-269
                 const float pw = fminf(power, 0.0f);   // == power on live lanes; finite exps elsewhere
                 const bool skewed = (B.z != 0.0f || B.w != 0.0f);                          // warp-uniform
                 float E = 1.0f, z = 0.0f, o = C.x;
@@ -429,13 +426,12 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                 const float G = fast_exp2(pw * SSG_LOG2E);
                 const float Aval = o * G * E;
                 const float alpha = fminf(Aval, SSG_ALPHA_MAX);
-                const bool contrib = live && alpha >= SSG_ALPHA_SKIP;
+                contrib = live && alpha >= SSG_ALPHA_SKIP;
                 const float Tn = T * fast_rcp(1.0f - alpha);                                   // :280
                 T = contrib ? Tn : T;
                 const float e0 = C.z - R0, e1 = C.w - R1, e2 = cb - R2;
                 const float d_alpha = T * (e0 * d0 + e1 * d1 + e2 * d2);
                 const float aT = contrib ? alpha * T : 0.0f;
-                float g[12];
                 g[9] = aT * d0;
                 g[10] = aT * d1;
                 g[11] = aT * d2;
@@ -459,14 +455,21 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                 R1 = fmaf(ae, e1, R1);
                 R2 = fmaf(ae, e2, R2);
 #ifdef SSG_BLEND_STATS
-                {
-                    const unsigned cbal = __ballot_sync(0xffffffffu, contrib);
-                    if (lane == 0) {
-                        SSG_STAT(17, cbal != 0);
-                        SSG_STAT(18, __popc(cbal));
-                    }
+                const unsigned cbal = __ballot_sync(0xffffffffu, contrib);
+                if (lane == 0) {
+                    SSG_STAT(17, cbal != 0);
+                    SSG_STAT(18, __popc(cbal));
                 }
 #endif
+            };
+            while (mask) {
+                const int bit = 31 - __clz(mask);
+                mask &= ~(1u << bit);
+                const int j = c0 + bit;
+                float g[12];
+                bool live, contrib;
+                replay(j, lo + j, g, live, contrib);
+                if (!blend_mask && !__any_sync(0xffffffffu, live)) continue;  // test-driven walk: empty hit
                 // with the forward's mask every visited instance has a
                 // contributing pixel; without it, skip empty hits
                 if (blend_mask || __any_sync(0xffffffffu, contrib)) {
