@@ -462,21 +462,33 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                 }
 #endif
             };
-            while (mask) {
-                const int bit = 31 - __clz(mask);
-                mask &= ~(1u << bit);
-                const int j = c0 + bit;
-                float g[12];
-                bool live, contrib;
-                replay(j, lo + j, g, live, contrib);
-                if (!blend_mask && !__any_sync(0xffffffffu, live)) continue;  // test-driven walk: empty hit
-                // with the forward's mask every visited instance has a
-                // contributing pixel; without it, skip empty hits
-                if (blend_mask || __any_sync(0xffffffffu, contrib)) {
-                    // the 12 holder lanes add their component straight into the
-                    // primitive's accumulator row, or (plugin slot mode) the
-                    // per-instance (M,12) slot row of _core.pyx:309-312
-                    // (raster/backward.py:70-73)
+            // the 12 holder lanes add their component straight into the
+            // primitive's accumulator row, or (plugin slot mode) the
+            // per-instance (M,12) slot row of _core.pyx:309-312
+            // (raster/backward.py:70-73).  Two loops, so the visit itself
+            // carries no mask-mode test.
+            if (blend_mask) {
+                // the forward's mask: every visited instance has a contributing pixel
+                while (mask) {
+                    const int bit = 31 - __clz(mask);
+                    mask &= ~(1u << bit);
+                    const int j = c0 + bit;
+                    float g[12];
+                    bool live, contrib;
+                    replay(j, lo + j, g, live, contrib);
+                    const float v = warp_reduce_transposed12(g, lane);
+                    if (holder) atomicAdd(sRow[j] + my_comp, v);
+                }
+            } else {
+                // test-driven walk: skip empty hits
+                while (mask) {
+                    const int bit = 31 - __clz(mask);
+                    mask &= ~(1u << bit);
+                    const int j = c0 + bit;
+                    float g[12];
+                    bool live, contrib;
+                    replay(j, lo + j, g, live, contrib);
+                    if (!__any_sync(0xffffffffu, live) || !__any_sync(0xffffffffu, contrib)) continue;
                     const float v = warp_reduce_transposed12(g, lane);
                     if (holder) atomicAdd(sRow[j] + my_comp, v);
                 }
