@@ -51,16 +51,29 @@ def _validate(scene, view, frame, dL_dpixels):
 
 
 def _device_backward(scene, view, frame, dL):
+    """Upload, recompute projection + binning (backward.py:49-53), replay.
+    The frame and dL_dpixels uploads run on a second stream while the
+    recomputed projection and binning (which need only the scene) run."""
+    from ..engine import camera_struct
     eng = default_engine()
     dev = eng.device
     ds = DeviceScene.from_host(scene, dev)
-    final_T = torch.from_numpy(np.ascontiguousarray(frame.final_T, dtype=np.float64)).to(
-        dev, non_blocking=True).float()
-    last_idx = torch.from_numpy(np.ascontiguousarray(frame.last_idx, dtype=np.int64)).to(
-        dev, non_blocking=True).int()
-    dL_dev = torch.from_numpy(dL).to(dev, non_blocking=True).float()
-    g = eng.backward(ds, view, frame.s, final_T, last_idx, dL_dev, rebin=True,
-                     expect_m=frame.n_instances)
+    main = torch.cuda.current_stream(dev)
+    side = eng.lane_stream()
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        final_T = torch.from_numpy(np.ascontiguousarray(frame.final_T, dtype=np.float64)).to(
+            dev, non_blocking=True).float()
+        last_idx = torch.from_numpy(np.ascontiguousarray(frame.last_idx, dtype=np.int64)).to(
+            dev, non_blocking=True).int()
+        dL_dev = torch.from_numpy(dL).to(dev, non_blocking=True).float()
+    m = eng.project_and_bin(ds, camera_struct(view, frame.s))
+    if m != frame.n_instances:
+        raise FrameMismatchError("instance count differs from the forward pass")
+    main.wait_stream(side)
+    for t in (final_T, last_idx, dL_dev):
+        t.record_stream(main)
+    g = eng.backward(ds, view, frame.s, final_T, last_idx, dL_dev, rebin=False)
     return eng, g
 
 
