@@ -69,6 +69,7 @@ constexpr int kFixMax = 32;
 constexpr unsigned long long kReady = 1ull << 63;  // tile_sums flag (final phase)
 constexpr int kMaxPasses = 8;                 // 64-bit keys, byte digits
 constexpr int kSub = kThreads / 256;          // threads per digit in the prefix sums
+constexpr int kPre = 4;                       // tiles per multi-tile prefix sweep
 static_assert(kThreads % 256 == 0, "prefix sums map 256 digits x kSub threads");
 
 __host__ __device__ inline int64_t num_tiles(int64_t n) { return (n + kTile - 1) / kTile; }
@@ -103,6 +104,7 @@ struct Smem {
     uint32_t tstart[256];         // tile-local start of each digit run
     uint32_t excl[256];           // global start of this tile's digit run
     uint32_t red[2][kSub][256];   // prefix sums: partial (before tile, total) per sub-thread
+    uint32_t pre[4][256];         // multi-tile prefix sweep: counts before each of 4 tiles
     uint32_t swarp[kWarps];
     uint64_t sum64[kWarps];
     unsigned long long kmin, kmax;
@@ -133,6 +135,55 @@ __device__ __forceinline__ void scan256(const uint32_t *in, uint32_t *out, uint3
         out[t] = pre + x - v;
     }
     __syncthreads();
+}
+
+// Multi-tile CTAs (ntiles > grid): prefix sums over a pass's count table for
+// up to kPre of this CTA's tiles (tile, tile + grid, ...) in ONE sweep:
+// digit totals (first sweep of the pass -> s.base) and, per tile g, the
+// counts of the tiles before it (s.pre[g]).  16 B loads (4 digits), 16 lanes
+// per digit quad, reduced by shuffles.  (With one tile per CTA the plain
+// 4-byte sweep in the kernel is cheaper.)
+__device__ __forceinline__ void prefix_sweep(const uint32_t *cnt, int64_t ntiles, int64_t tile, bool first, Smem &s) {
+    const int t = threadIdx.x;
+    const int d4 = t >> 4, j = t & 15;  // digits 4*d4 .. 4*d4+3, sweep lane j
+    int64_t tl[kPre];
+#pragma unroll
+    for (int g = 0; g < kPre; g++) tl[g] = tile + (int64_t)g * gridDim.x;  // may be >= ntiles
+    const int64_t qend = first ? ntiles : (tl[kPre - 1] < ntiles ? tl[kPre - 1] : ntiles);
+    uint4 tot = make_uint4(0, 0, 0, 0), pre[kPre];
+#pragma unroll
+    for (int g = 0; g < kPre; g++) pre[g] = make_uint4(0, 0, 0, 0);
+#pragma unroll 4
+    for (int64_t q = j; q < qend; q += 16) {
+        const uint4 c = __ldcg(reinterpret_cast<const uint4 *>(cnt + (size_t)q * 256) + d4);
+        tot.x += c.x; tot.y += c.y; tot.z += c.z; tot.w += c.w;
+#pragma unroll
+        for (int g = 0; g < kPre; g++)
+            if (q < tl[g]) {
+                pre[g].x += c.x; pre[g].y += c.y; pre[g].z += c.z; pre[g].w += c.w;
+            }
+    }
+#pragma unroll
+    for (int off = 8; off >= 1; off >>= 1) {
+        tot.x += __shfl_xor_sync(0xffffffffu, tot.x, off);
+        tot.y += __shfl_xor_sync(0xffffffffu, tot.y, off);
+        tot.z += __shfl_xor_sync(0xffffffffu, tot.z, off);
+        tot.w += __shfl_xor_sync(0xffffffffu, tot.w, off);
+#pragma unroll
+        for (int g = 0; g < kPre; g++) {
+            pre[g].x += __shfl_xor_sync(0xffffffffu, pre[g].x, off);
+            pre[g].y += __shfl_xor_sync(0xffffffffu, pre[g].y, off);
+            pre[g].z += __shfl_xor_sync(0xffffffffu, pre[g].z, off);
+            pre[g].w += __shfl_xor_sync(0xffffffffu, pre[g].w, off);
+        }
+    }
+    if (j == 0) {
+        if (first) reinterpret_cast<uint4 *>(s.wcnt[0])[d4] = tot;
+#pragma unroll
+        for (int g = 0; g < kPre; g++) reinterpret_cast<uint4 *>(s.pre[g])[d4] = pre[g];
+    }
+    __syncthreads();
+    if (first) scan256(s.wcnt[0], s.base, s.swarp);  // bucket bases of this pass
 }
 
 static __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_depth_sort(Args a) {
@@ -228,10 +279,17 @@ static __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_depth_sort
                 return kk == kInvalid ? ~0ull : kk - kmin;
             };
 
-            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                // prefix sums over the count table: digit totals (first tile
-                // only; -> bucket bases) and counts of the tiles before this one
-                {
+            const bool multi = ntiles > (int64_t)gridDim.x;  // some CTA owns several tiles
+            int ti = 0;                                       // index of `tile` among this CTA's
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ti++) {
+                if (multi) {
+                    // one sweep of the count table per group of kPre tiles
+                    if (ti % kPre == 0) prefix_sweep(cnt, ntiles, tile, ti == 0, s);
+                    if (t < 256) s.excl[t] = s.pre[ti % kPre][t];
+                    __syncthreads();
+                } else {
+                    // prefix sums over the count table: digit totals (-> bucket
+                    // bases) and counts of the tiles before this one
                     const int d = t & 255, j = t >> 8;
                     const bool first = tile == blockIdx.x;
                     const int64_t qend = first ? ntiles : tile;
