@@ -275,7 +275,8 @@ def main():
     def step(sync=False):
         # no host round trip inside the frame (the instance buffers are sized
         # by the first, synchronised frame; eng.instances() checks after the run)
-        f = eng.forward(ds, view, 0.3, sync=sync)
+        # the forward's exact path (flagged pixels) overlaps the backward's main kernel
+        f = eng.forward(ds, view, 0.3, sync=sync, defer_exact=True)
         eng.backward(ds, view, 0.3, f.final_T, f.last_idx, dL, rebin=False)
         return f
 

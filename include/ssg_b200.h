@@ -77,15 +77,29 @@ typedef struct ssg_camera {
 
 /* Per-primitive screen record consumed by the blend kernels (64 bytes,
  * 16-byte aligned): mean in fp64 so blend kernels can form tile-local
- * offsets exactly; the rest fp32. */
+ * offsets exactly; the rest fp32.  band0 + band1 |power| bounds the relative
+ * error of the blend's fp32 alpha against the reference's fp64 alpha for this
+ * primitive (ssg_common.cuh alpha_band): a pixel whose fp32 alpha or
+ * transmittance lies within its error bound of a threshold (1/255 skip, 0.99
+ * clamp, 1e-4 stop) is decided on the exact fp64 path instead (ssg_splat64),
+ * so every decision equals the reference's. */
 typedef struct ssg_splat {
     double mean_x, mean_y;
     float conic_a, conic_b, conic_c;
     float skew_x, skew_y;
     float o1, o2;
     float r, g, b;
-    uint32_t pad0, pad1;
+    float band0, band1;         /* alpha error band g0 + g1 |power| */
 } ssg_splat;
+
+/* fp64 twin of the splat's blend inputs (projection.py:194-215 values before
+ * any rounding), read only on the rare threshold-band path (64 bytes). */
+typedef struct ssg_splat64 {
+    double conic_a, conic_b, conic_c;
+    double skew_x, skew_y;
+    double o1, o2;
+    double pad;
+} ssg_splat64;
 
 /* Per-primitive buffers written by ssg_preprocess_forward. */
 typedef struct ssg_prim_buffers {
@@ -97,6 +111,7 @@ typedef struct ssg_prim_buffers {
     double *depth;              /* (n) camera-space z (projection.py:161) */
     double *radius;             /* (n) */
     int32_t *n_skew_fallback;   /* (1) accumulated with atomics (zeroed by the call) */
+    ssg_splat64 *splat64;       /* (n) fp64 blend inputs (threshold-band path) */
 } ssg_prim_buffers;
 
 /* Binning buffers.  depth_order/rank_offset are (n); inst_* are (capacity). */
@@ -108,9 +123,8 @@ typedef struct ssg_bin_buffers {
                                    skips the read-back check a batch of frames at once) */
     int64_t capacity;           /* allocated instances */
     uint32_t *inst_prim;        /* (capacity) sorted primitive id per instance */
-    uint16_t *inst_tile;        /* (capacity) sorted tile id per instance */
-    uint32_t *inst_prim_tmp;    /* unused (kept for layout stability; may be NULL) */
-    uint16_t *inst_tile_tmp;    /* unused (may be NULL) */
+    uint32_t *inst_tile;        /* (capacity) sorted tile id per instance; optional (NULL =
+                                   not written: the blend kernels never read it) */
     int32_t *ranges;            /* (n_tiles, 2) half-open [start, end) */
     void *temp;                 /* temporary storage for the sorts and scans
                                    (size from ssg_bin_temp_bytes) */
@@ -129,6 +143,13 @@ typedef struct ssg_frame_buffers {
                                    ssg_blend_backward_slots then visit exactly those.  Only
                                    valid for the binning, splats and final_T/last_idx of
                                    the forward call that wrote it. */
+    /* Exact-path bookkeeping, written by ssg_blend_forward and read by the
+     * backward (required by both): pixels whose fp32 evaluation met an
+     * uncertain decision are recomputed by the exact fp64 path. */
+    uint32_t *redo_mask;        /* (n_tiles, 8) words: bit l of word 8 t + w = pixel l of the
+                                   8x4 block w of tile t (lane order: 8 per row) */
+    uint32_t *redo_list;        /* (W*H) pixel indices (y*W + x), first *redo_count valid */
+    uint32_t *redo_count;       /* (1) */
 } ssg_frame_buffers;
 
 /* Gradient outputs (raster/backward.py:28-39).  d_beta == d_dir
@@ -183,6 +204,12 @@ void ssg_grid_dims(int32_t width, int32_t height, int32_t *tiles_x, int32_t *til
 int ssg_bin_temp_bytes(int64_t n, int64_t capacity, int32_t width, int32_t height, size_t *bytes);
 
 /* ---- forward ------------------------------------------------------------ */
+/* screen records (splat + splat64, with the alpha band) from caller fp64 device
+ * arrays mean2d (n,2), conic (n,3), skew2d (n,2), opair (n,2), color (n,3): the
+ * inputs of the reference's blend plugin slot (raster/_core.pyx:169-177) */
+int ssg_pack_splats(int64_t n, const double *mean2d, const double *conic, const double *skew2d,
+                    const double *opair, const double *color, ssg_splat *splat, ssg_splat64 *splat64,
+                    void *stream);
 int ssg_preprocess_forward(const ssg_scene *scene, const ssg_camera *cam,
                            const ssg_prim_buffers *out, void *stream);
 /* depth sort, counts in depth order, exclusive scan; writes bins->n_instances */
@@ -200,16 +227,51 @@ int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t height,
                    const ssg_prim_buffers *prim, const ssg_bin_buffers *bins, void *stream);
 /* words of the optional frame blend mask for m instances over n_tiles tiles */
 int64_t ssg_blend_mask_words(int64_t m, int32_t n_tiles);
+/* Decisions (alpha skip, transmittance stop) equal the fp64 reference's: the
+ * fp32 blend carries an error bound and re-decides in fp64 (splat64, and an
+ * fp64 replay of the pixel's transmittance) whenever a value falls inside it. */
 int ssg_blend_forward(int64_t m, int32_t width, int32_t height, const float background[3],
-                      const ssg_splat *splat, const ssg_bin_buffers *bins,
+                      const ssg_splat *splat, const ssg_splat64 *splat64, const ssg_bin_buffers *bins,
                       const ssg_frame_buffers *frame, void *stream);
+
+/* The two halves of ssg_blend_forward / ssg_blend_backward, for callers that
+ * overlap the exact path with other work on a second stream:
+ * SSG_BLEND_MAIN_ONLY runs the fp32 kernel (it flags the pixels it cannot
+ * certify), SSG_BLEND_EXACT_ONLY the exact path over the flagged pixels
+ * (after the forward's main half; the backward's exact half needs the
+ * forward's exact half but not the backward's main half -- both only add
+ * into grads->screen).  SSG_BLEND_NO_ZERO (backward): grads->screen is
+ * already zeroed by the caller.  flags = 0: the whole call. */
+#define SSG_BLEND_MAIN_ONLY 1
+#define SSG_BLEND_EXACT_ONLY 2
+#define SSG_BLEND_NO_ZERO 4
+int ssg_blend_forward_ex(int64_t m, int32_t width, int32_t height, const float background[3],
+                         const ssg_splat *splat, const ssg_splat64 *splat64, const ssg_bin_buffers *bins,
+                         const ssg_frame_buffers *frame, int32_t flags, void *stream);
 
 /* ---- backward ----------------------------------------------------------- */
 /* accumulates (n,12) screen gradients into grads->screen (zeroed by the call) */
 int ssg_blend_backward(int64_t n, int64_t m, int32_t width, int32_t height,
-                       const float background[3], const ssg_splat *splat,
+                       const float background[3], const ssg_splat *splat, const ssg_splat64 *splat64,
                        const ssg_bin_buffers *bins, const ssg_frame_buffers *frame,
                        const float *dL_dpixels, const ssg_grad_buffers *grads, void *stream);
+int ssg_blend_backward_ex(int64_t n, int64_t m, int32_t width, int32_t height,
+                          const float background[3], const ssg_splat *splat, const ssg_splat64 *splat64,
+                          const ssg_bin_buffers *bins, const ssg_frame_buffers *frame,
+                          const float *dL_dpixels, const ssg_grad_buffers *grads, int32_t flags, void *stream);
+/* Deterministic variant (bitwise-repeatable gradients).
+ * Each (primitive, tile) pair's 12 sums are combined over the tile's pixel
+ * blocks in a fixed order and stored (no atomics) into a primitive-major
+ * slot array, each primitive's slots in ascending tile (= ascending
+ * instance, raster/backward.py:70-73) order, then summed per primitive in
+ * that order.  `prim` must be the buffers of the forward's ssg_bin_prepare
+ * (tile_count, tile_rect); temp of ssg_blend_det_temp_bytes(n, m) bytes. */
+size_t ssg_blend_det_temp_bytes(int64_t n, int64_t m);
+int ssg_blend_backward_det(int64_t n, int64_t m, int32_t width, int32_t height,
+                           const float background[3], const ssg_splat *splat, const ssg_splat64 *splat64,
+                           const ssg_prim_buffers *prim, const ssg_bin_buffers *bins,
+                           const ssg_frame_buffers *frame, const float *dL_dpixels,
+                           const ssg_grad_buffers *grads, void *temp, size_t temp_bytes, void *stream);
 int ssg_preprocess_backward(const ssg_scene *scene, const ssg_camera *cam,
                             const ssg_grad_buffers *grads, void *stream);
 /* The projection backward in two parts, so the zero-fill can overlap the
@@ -229,7 +291,7 @@ int ssg_preprocess_backward_ex(const ssg_scene *scene, const ssg_camera *cam,
  * backward_tiles): per-instance gradient slots (m,12) instead of the fused
  * per-primitive reduction; slots is zeroed by the call */
 int ssg_blend_backward_slots(int64_t m, int32_t width, int32_t height, const float background[3],
-                             const ssg_splat *splat, const ssg_bin_buffers *bins,
+                             const ssg_splat *splat, const ssg_splat64 *splat64, const ssg_bin_buffers *bins,
                              const ssg_frame_buffers *frame, const float *dL_dpixels, float *slots,
                              void *stream);
 
@@ -325,8 +387,14 @@ int ssg_test_sort(void *keys, uint32_t *vals, int key_bytes, int iota, int64_t n
 /* the blend forward compiled without the skew term (plain 3DGS: alpha =
  * o * G): the config-3 regression reference for skew-free splats */
 int ssg_test_blend_forward_vanilla(int32_t width, int32_t height, const float background[3],
-                                   const ssg_splat *splat, const ssg_bin_buffers *bins,
-                                   const ssg_frame_buffers *frame, void *stream);
+                                   const ssg_splat *splat, const ssg_splat64 *splat64,
+                                   const ssg_bin_buffers *bins, const ssg_frame_buffers *frame,
+                                   void *stream);
+/* device evaluation of the blend's two erf paths at n points x (device
+ * arrays): e32[i] = the fp32 E = 1 + erf(x) of the blend kernels, e64[i] =
+ * the fp64 c_erf restatement (raster/_core.pyx:57-74) the threshold-band
+ * path uses; either output may be NULL (erf_probe, raster/_core.pyx:46-54) */
+int ssg_erf_probe(const double *x, int64_t n, float *e32, double *e64, void *stream);
 
 #ifdef __cplusplus
 }

@@ -19,6 +19,9 @@ SSG_ERR_DIM_OVERFLOW = 2
 SSG_ERR_CAPACITY = 3
 SSG_ERR_CUDA = 4
 SSG_PREP_BWD_ACTIVE_ONLY = 1
+SSG_BLEND_MAIN_ONLY = 1
+SSG_BLEND_EXACT_ONLY = 2
+SSG_BLEND_NO_ZERO = 4
 
 EXPORTS = ("ssg_abi_version", "ssg_last_error", "ssg_grid_dims", "ssg_bin_temp_bytes",
            "ssg_preprocess_forward", "ssg_bin_rects", "ssg_bin_prepare", "ssg_bin_finish", "ssg_blend_forward",
@@ -28,7 +31,8 @@ EXPORTS = ("ssg_abi_version", "ssg_last_error", "ssg_grid_dims", "ssg_bin_temp_b
            "ssg_test_sort", "ssg_test_blend_forward_vanilla", "ssg_adam_step", "ssg_blend_mask_words",
            "ssg_loss_scratch_floats", "ssg_image_loss", "ssg_regularize", "ssg_interval_stats_add",
            "ssg_densify_temp_bytes", "ssg_densify_plan", "ssg_densify_apply", "ssg_ply_unpack",
-           "ssg_quantize_u8")
+           "ssg_quantize_u8", "ssg_blend_det_temp_bytes", "ssg_blend_backward_det", "ssg_erf_probe",
+           "ssg_pack_splats", "ssg_blend_forward_ex", "ssg_blend_backward_ex")
 
 _vp = ctypes.c_void_p
 
@@ -50,18 +54,18 @@ class SsgCamera(ctypes.Structure):
 
 class SsgPrimBuffers(ctypes.Structure):
     _fields_ = [("splat", _vp), ("depth_key", _vp), ("tile_count", _vp), ("tile_rect", _vp),
-                ("valid", _vp), ("depth", _vp), ("radius", _vp), ("n_skew_fallback", _vp)]
+                ("valid", _vp), ("depth", _vp), ("radius", _vp), ("n_skew_fallback", _vp), ("splat64", _vp)]
 
 
 class SsgBinBuffers(ctypes.Structure):
     _fields_ = [("depth_order", _vp), ("rank_offset", _vp), ("n_instances", _vp),
-                ("capacity", ctypes.c_int64), ("inst_prim", _vp), ("inst_tile", _vp),
-                ("inst_prim_tmp", _vp), ("inst_tile_tmp", _vp), ("ranges", _vp),
+                ("capacity", ctypes.c_int64), ("inst_prim", _vp), ("inst_tile", _vp), ("ranges", _vp),
                 ("temp", _vp), ("temp_bytes", ctypes.c_size_t)]
 
 
 class SsgFrameBuffers(ctypes.Structure):
-    _fields_ = [("color", _vp), ("final_T", _vp), ("n_contrib", _vp), ("last_idx", _vp), ("blend_mask", _vp)]
+    _fields_ = [("color", _vp), ("final_T", _vp), ("n_contrib", _vp), ("last_idx", _vp), ("blend_mask", _vp),
+                ("redo_mask", _vp), ("redo_list", _vp), ("redo_count", _vp)]
 
 
 class SsgGradBuffers(ctypes.Structure):
@@ -98,7 +102,8 @@ class SsgAdamHparams(ctypes.Structure):
 
 
 SPLAT_BYTES = 64
-ABI_VERSION = 4
+SPLAT64_BYTES = 64
+ABI_VERSION = 5
 
 _lib = None
 
@@ -130,18 +135,30 @@ def lib():
     L.ssg_bin_finish.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                  P(SsgPrimBuffers), P(SsgBinBuffers), _vp]
     L.ssg_blend_forward.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
-                                    P(ctypes.c_float), _vp, P(SsgBinBuffers),
+                                    P(ctypes.c_float), _vp, _vp, P(SsgBinBuffers),
                                     P(SsgFrameBuffers), _vp]
     L.ssg_blend_backward.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
-                                     ctypes.c_int32, P(ctypes.c_float), _vp, P(SsgBinBuffers),
+                                     ctypes.c_int32, P(ctypes.c_float), _vp, _vp, P(SsgBinBuffers),
                                      P(SsgFrameBuffers), _vp, P(SsgGradBuffers), _vp]
+    L.ssg_blend_forward_ex.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, P(ctypes.c_float), _vp, _vp,
+                                       P(SsgBinBuffers), P(SsgFrameBuffers), ctypes.c_int32, _vp]
+    L.ssg_blend_backward_ex.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                        P(ctypes.c_float), _vp, _vp, P(SsgBinBuffers), P(SsgFrameBuffers), _vp,
+                                        P(SsgGradBuffers), ctypes.c_int32, _vp]
+    L.ssg_blend_det_temp_bytes.restype = ctypes.c_size_t
+    L.ssg_blend_det_temp_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64]
+    L.ssg_blend_backward_det.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                         P(ctypes.c_float), _vp, _vp, P(SsgPrimBuffers), P(SsgBinBuffers),
+                                         P(SsgFrameBuffers), _vp, P(SsgGradBuffers), _vp, ctypes.c_size_t, _vp]
+    L.ssg_erf_probe.argtypes = [_vp, ctypes.c_int64, _vp, _vp, _vp]
+    L.ssg_pack_splats.argtypes = [ctypes.c_int64] + [_vp] * 8
     L.ssg_preprocess_backward.argtypes = [P(SsgScene), P(SsgCamera), P(SsgGradBuffers), _vp]
     L.ssg_zero_prim_grads.argtypes = [ctypes.c_int64, ctypes.c_int32, P(SsgGradBuffers), _vp]
     L.ssg_preprocess_backward_ex.argtypes = [P(SsgScene), P(SsgCamera), P(SsgGradBuffers), ctypes.c_int32, _vp]
     L.ssg_blend_backward_slots.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
-                                           P(ctypes.c_float), _vp, P(SsgBinBuffers), P(SsgFrameBuffers),
+                                           P(ctypes.c_float), _vp, _vp, P(SsgBinBuffers), P(SsgFrameBuffers),
                                            _vp, _vp, _vp]
-    L.ssg_test_blend_forward_vanilla.argtypes = [ctypes.c_int32, ctypes.c_int32, P(ctypes.c_float), _vp,
+    L.ssg_test_blend_forward_vanilla.argtypes = [ctypes.c_int32, ctypes.c_int32, P(ctypes.c_float), _vp, _vp,
                                                  P(SsgBinBuffers), P(SsgFrameBuffers), _vp]
     L.ssg_adam_step.argtypes = [P(SsgParams), P(SsgGradBuffers), P(SsgAdamState), P(SsgAdamHparams), _vp]
     L.ssg_test_sort_temp_bytes.restype = ctypes.c_size_t

@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs2_scatter(const uint64_t *_
                                                                const uint32_t *__restrict__ tile_start,
                                                                int32_t ntx, int32_t nty,
                                                                uint32_t *__restrict__ inst_prim,
-                                                               uint16_t *__restrict__ inst_tile, uint32_t cap) {
+                                                               uint32_t *__restrict__ inst_tile, uint32_t cap) {
     extern __shared__ __align__(16) unsigned char s_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     unsigned char *base = s_raw + (size_t)w * cs_warp_smem<uint32_t>(ntx);
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs2_scatter(const uint64_t *_
                     st_b[pos] = (uint16_t)x;
                 } else if (pos < cap) {
                     inst_prim[pos] = p;
-                    if (inst_tile) inst_tile[pos] = (uint16_t)(trow + x);
+                    if (inst_tile) inst_tile[pos] = trow + (uint32_t)x;
                 }
             });
         if (staged) {
@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs2_scatter(const uint64_t *_
                 const uint32_t pos = delta[x] + i;
                 if (pos >= cap) continue;
                 inst_prim[pos] = st_pay[i];
-                if (inst_tile) inst_tile[pos] = (uint16_t)(trow + x);
+                if (inst_tile) inst_tile[pos] = trow + (uint32_t)x;
             }
         }
         __syncwarp();
@@ -581,7 +581,6 @@ extern "C" int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t heigh
     if (width > SSG_MAX_IMAGE_DIM || height > SSG_MAX_IMAGE_DIM) return SSG_ERR_DIM_OVERFLOW;
     const int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
     const int32_t n_tiles = ntx * nty;
-    if (n_tiles > 65536) return SSG_ERR_INVALID_ARGUMENT;  // inst_tile is u16
     cudaStream_t st = (cudaStream_t)stream;
     const BinTemp T = bin_temp(n, bins->capacity, width, height);
     if (bins->temp_bytes < T.total) return SSG_ERR_CAPACITY;
@@ -595,18 +594,22 @@ extern "C" int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t heigh
     uint32_t *tile_start = (uint32_t *)(work + L.tile_start);
     const size_t sm1 = kCsWarps * cs_warp_smem<uint64_t>(nty), sm2 = kCsWarps * cs_warp_smem<uint32_t>(ntx);
     const size_t smc1 = sizeof(uint32_t) * kCsWarps * (nty + 1), smc2 = sizeof(uint32_t) * kCsWarps * (ntx + 1);
-    static bool attr = false;
-    if (!attr) {  // the largest grids (4096 tiles per side) need > 48 KB
+    // the largest grids (4096 tiles per side) need > 48 KB; function
+    // attributes are per device, so the one-time setup is per device ordinal
+    static bool attr_dev[64] = {false};
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SSG_ERR_CUDA;
+    if (!attr_dev[dev]) {
         const int mx = (int)(kCsWarps * cs_warp_smem<uint64_t>(4096));
-        cudaFuncSetAttribute(k_cs1_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(k_cs2_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(k_cs1_count, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(k_cs2_count, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        attr = true;
+        cudaError_t e = cudaFuncSetAttribute(k_cs1_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k_cs2_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k_cs1_count, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k_cs2_count, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        if (e != cudaSuccess) { set_error("cudaFuncSetAttribute(binning)", e); return SSG_ERR_CUDA; }
+        attr_dev[dev] = true;
     }
     const unsigned g1 = (unsigned)((L.nch1 + kCsWarps - 1) / kCsWarps);
-    int sms = 148, dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned g2 = (unsigned)(sms * 8);
     // level 1: row segments in per-row lists
     k_cs1_count<<<g1, 32 * kCsWarps, smc1, st>>>(bins->depth_order, prim->tile_count, prim->tile_rect, n, L.nch1,

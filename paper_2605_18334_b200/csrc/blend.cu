@@ -8,85 +8,111 @@
 // Layout: one CTA of 256 threads per 16x16 tile, one thread per pixel; warp
 // w owns the 8x4 pixel block at (8*(w&1), 4*(w>>1)).  Instance batches of 256
 // are staged in shared memory with the mean made tile-local in fp64 before
-// rounding to fp32 (offsets stay small, so dx/dy keep ~1e-6 px precision at
-// x ~ 2000).  Every staged instance also carries the bounding box of the
-// ellipse outside of which its alpha is certainly below 1/255 (see
-// stage_splat).  Each warp then walks the batch 32 instances at a time: one
-// lane per instance tests the box against the warp's 8x4 block, a ballot
-// gives the hit mask, and the warp evaluates only the hits, in order.  The
-// culling is conservative, so the per-pixel decisions (skip / blend / stop)
-// are exactly those of the unculled loop; it removes the pixel-instance pairs
-// that cannot contribute before any arithmetic is spent on them.
+// rounding to fp32.  Every staged instance also carries the ellipse outside
+// of which its alpha is certainly below 1/255 (see stage_values).  Each warp
+// walks the batch 32 instances at a time: one lane per instance tests the
+// ellipse against the warp's 8x4 block, a ballot gives the hit mask, and the
+// warp evaluates only the hits, in order.  The culling is conservative.
+//
+// Decisions equal the fp64 reference's.  The blend arithmetic is fp32, and
+// every skip (alpha >= 1/255), clamp (A <= 0.99) and stop (T (1 - alpha) <
+// 1e-4) decision it takes is certified: each primitive carries a bound
+// `band` on the relative error of its fp32 alpha (ssg_common.cuh
+// alpha_band), each pixel a running bound `dT` on the absolute error of its
+// fp32 transmittance.  A pixel that meets a decision its bounds cannot
+// certify stops there and is flagged (redo_mask / redo_list); the redo
+// kernels then recompute exactly those pixels on the exact path: candidate
+// instances from an fp32 scan (a superset of the reference's passing
+// instances), their alphas in fp64 (ref_pair), transmittance as an fp64
+// prefix product, colour / gradients in fp64.  No fp64 and no calls on the
+// hot loop.
+//
 // Backward: the 12 per-instance sums of a warp are reduced with a transposed
-// butterfly (13 shuffles instead of 60) and added to the primitive's
-// gradient row by the 12 lanes holding them, one scalar global reduction
-// each (one RED instruction; measured 2.4 % faster than gathering them into
-// three float4 vector REDs; the shared-memory fp32 atomic on sm_100 is a CAS
-// loop, so no smem staging).
+// butterfly (13 shuffles instead of 60).  Default: the 12 lanes holding them
+// add them to the primitive's gradient row, one scalar global reduction each.
+// Deterministic modes: each warp stores its sums in shared memory, the tile's
+// eight warps are combined in a fixed order and one thread per instance
+// stores the row (no atomics): per instance (the reference's (M,12) slots) or
+// primitive-major (each primitive's rows in ascending instance order, summed
+// in that order by k_reduce_prim_rows); their redo runs one warp per tile in
+// pixel order.
 #include "ssg_common.cuh"
-
-#ifdef SSG_BLEND_STATS
-// diagnostic build only (tools/blend_stats.py): warp-level event counters
-__device__ unsigned long long g_blend_stats[32];
-#define SSG_STAT(i, v) atomicAdd(&g_blend_stats[i], (unsigned long long)(v))
-#endif
 
 namespace ssg {
 
 constexpr int kThreads = 256;
 constexpr int kBatch = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr float kNearT = 1.05e-4f;   // candidate transmittance below which the stop test needs its bound
+constexpr int kCand = 256;           // redo: candidate instances per segment (per warp)
+constexpr int kRedoWarps = 4;        // redo: warps per CTA
 
 // Shared-memory image of one instance:
 //   A = (mx_local, my_local, conic_a, conic_b)
 //   B = (conic_c, far_thr, skew_x, skew_y)
-//   C = (o_sum, o_diff, r, g),  D = b
+//   C = (o_sum, o_diff, r, g)
+//   D = (b, sband, g0, g1): the pair's relative alpha error is <= g0 + g1 |power|
+//       (alpha_band); sband = (1/255) (g0 + 6.3 g1): fp32 alpha - 1/255 >= sband
+//       certainly passes the reference's 1/255 test, < -sband certainly fails
 //   X = (k, h, m, r2m): the ellipse {d : a dx^2 + 2b dx dy + c dy^2 <= r2m}
 //       in completed-square form, k = b/a, h = det/a, m = b/c
 // far_thr is a per-instance lower bound on the Gaussian exponent below which
 // alpha < 1/255 is certain: A = o*G*E <= omax*G*Emax with Emax = 2 (1 for
 // skew-free splats), so power < ln(1/(255*omax*Emax)) implies the reference's
-// ALPHA_SKIP test (_core.pyx:141) fires.  A 1e-4 margin keeps the shortcut
-// strictly inside the region where the full fp32 evaluation also skips.  The
-// ellipse {power >= far_thr} (r2 = -2 far_thr, widened by 1e-3 relative +
-// 1e-4 absolute) is what the per-warp culling tests against the warp's 8x4
-// block of pixel centres, exactly (not via its bounding box).
+// ALPHA_SKIP test (_core.pyx:141) fires; the margin max(1e-4, 2 band) keeps
+// the shortcut strictly inside the region where the true alpha also skips.
+// The ellipse {power >= far_thr} (r2 = -2 far_thr, widened by max(1e-3,
+// 4 band) relative + 1e-4 absolute) is what the per-warp culling tests
+// against the warp's 8x4 block of pixel centres, exactly.
 struct SmemBatch {
     float4 A[kBatch];
     float4 B[kBatch];
     float4 C[kBatch];
+    float4 D[kBatch];
     float4 X[kBatch];
-    float D[kBatch];
+};
+struct Staged {
+    float4 A, B, C, D, X;
 };
 
-template <typename S>
-__device__ __forceinline__ void stage_splat(const ssg_splat *splat, uint32_t p, double ox, double oy,
-                                            S &s, int slot) {
+__device__ __forceinline__ Staged stage_values(const ssg_splat *splat, uint32_t p, double ox, double oy) {
     const double2 m = __ldg(reinterpret_cast<const double2 *>(splat + p));
     const float4 q1 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 1);
     const float4 q2 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 2);
     const float4 q3 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 3);
-    // q1 = (a, b, c, sx)  q2 = (sy, o1, o2, r)  q3 = (g, b, pad, pad)
+    // q1 = (a, b, c, sx)  q2 = (sy, o1, o2, r)  q3 = (g, b, band0, band1)
     const bool skewed = (q1.w != 0.0f || q2.x != 0.0f);
+    const float band = fmaf(6.3f, q3.w, q3.z);      // the band anywhere a decision can fall
     const float omax = fmaxf(q2.y, q2.z) * (skewed ? 2.0f : 1.0f);
-    const float thr = omax > 0.0f ? -logf(255.0f * omax) - 1e-4f : INFINITY;
+    const float thr = omax > 0.0f ? -logf(255.0f * omax) - fmaxf(1e-4f, 2.0f * band) : INFINITY;
     const float mx = (float)(m.x - ox), my = (float)(m.y - oy);
     const float a = q1.x, b = q1.y, c = q1.z;
     const float r2 = -2.0f * thr;
-    float4 ell;
+    Staged v;
     if (!(r2 > 0.0f)) {
-        ell = make_float4(0.0f, 0.0f, 0.0f, -1.0f);                 // never blends: never hits
+        v.X = make_float4(0.0f, 0.0f, 0.0f, -1.0f);                 // never blends: never hits
     } else {
         const double det = (double)a * (double)c - (double)b * (double)b;   // exact products
         if (a > 0.0f && c > 0.0f && det > 0.0)
-            ell = make_float4(b / a, (float)(det / (double)a), b / c, fmaf(r2, 1.001f, 1e-4f));
+            v.X = make_float4(b / a, (float)(det / (double)a), b / c, fmaf(r2, 1.0f + fmaxf(1e-3f, 4.0f * band), 1e-4f));
         else
-            ell = make_float4(0.0f, 0.0f, 0.0f, INFINITY);          // degenerate: always evaluate
+            v.X = make_float4(0.0f, 0.0f, 0.0f, INFINITY);          // degenerate: always evaluate
     }
-    s.A[slot] = make_float4(mx, my, a, b);
-    s.B[slot] = make_float4(c, thr, q1.w, q2.x);
-    s.C[slot] = make_float4(0.5f * (q2.y + q2.z), 0.5f * (q2.y - q2.z), q2.w, q3.x);
-    s.D[slot] = q3.y;
-    s.X[slot] = ell;
+    v.A = make_float4(mx, my, a, b);
+    v.B = make_float4(c, thr, q1.w, q2.x);
+    v.C = make_float4(0.5f * (q2.y + q2.z), 0.5f * (q2.y - q2.z), q2.w, q3.x);
+    v.D = make_float4(q3.y, SSG_ALPHA_SKIP * band, q3.z, q3.w);
+    return v;
+}
+
+__device__ __forceinline__ void stage_splat(const ssg_splat *splat, uint32_t p, double ox, double oy,
+                                            SmemBatch &s, int slot) {
+    const Staged v = stage_values(splat, p, ox, oy);
+    s.A[slot] = v.A;
+    s.B[slot] = v.B;
+    s.C[slot] = v.C;
+    s.D[slot] = v.D;
+    s.X[slot] = v.X;
 }
 
 // Does the instance's ellipse meet the rectangle spanned by the warp's pixel
@@ -100,10 +126,8 @@ __device__ __forceinline__ void stage_splat(const ssg_splat *splat, uint32_t p, 
 // 0 at every pixel centre, z = (sx dx + sy dy)/sqrt2), E = erfc(-z) <=
 // exp(-zmax^2) < 1 there, so alpha < 1/255 already for power < far_thr +
 // ln 2 + zmax^2: the ellipse shrinks by 2 (ln 2 + zmax^2) in r2 for this
-// block (the 1e-4 margin of far_thr and the 1.001 widening carry over).
-// Skew-free splats have zmax = 0 and keep their (E = 1) ellipse.  The
-// positive side (E <= 1 + 2 zmax / sqrt(pi)) was measured to cull ~1 % more
-// hits for no time gain and is not used.
+// block (far_thr's margin and the widening carry over).  Skew-free splats
+// have zmax = 0 and keep their (E = 1) ellipse.
 __device__ __forceinline__ bool ellipse_meets_block(const float4 A, const float4 B, const float4 X, float wx0,
                                                     float wy0) {
     const float X0 = wx0 + 0.5f - A.x, X1 = X0 + 7.0f;
@@ -132,6 +156,32 @@ __device__ __forceinline__ size_t mask_word(int start, int tile, int chunk, int 
     return ((size_t)(start >> 5) + (size_t)tile + (size_t)chunk) * 8 + (size_t)warp;
 }
 
+// fp32 pre-clamp alpha of one pixel-instance pair: the same operation
+// sequence in every kernel (explicit fmaf, no contraction choices left to
+// the compiler), so all of them see bit-identical values.
+struct Pair {
+    float dx, dy, power, E, z, o, G, A;
+};
+__device__ __forceinline__ void pair_power(float fx, float fy, const float4 &A, const float4 &B, Pair &q) {
+    q.dx = fx - A.x;
+    q.dy = fy - A.y;
+    const float t = fmaf(B.x * q.dy, q.dy, A.z * q.dx * q.dx);
+    q.power = fmaf(-0.5f, t, -(A.w * q.dx) * q.dy);                                      // :133
+}
+template <bool kVanilla>
+__device__ __forceinline__ void pair_alpha(const float4 &B, const float4 &C, Pair &q) {
+    q.E = 1.0f;
+    q.z = 0.0f;
+    q.o = C.x;
+    if (!kVanilla && (B.z != 0.0f || B.w != 0.0f)) {     // warp-uniform on the hot loop
+        q.z = fmaf(B.z, q.dx, B.w * q.dy) * SSG_SQRT1_2;     // :136
+        q.E = skew_E(q.z);                                  // :137
+        q.o = fmaf(C.y, q.E - 1.0f, C.x);                   // :138
+    }
+    q.G = fast_exp2(fminf(q.power, 0.0f) * SSG_LOG2E);
+    q.A = kVanilla ? q.o * q.G : (q.o * q.G) * q.E;         // :139
+}
+
 // -------------------------------------------------------------- forward
 // kVanilla = true compiles the plain 3DGS blend (no skew term, alpha =
 // o * G): the config-3 regression reference for skew-free splats, which
@@ -150,9 +200,10 @@ template <bool kVanilla>
 __global__ void __launch_bounds__(kThreads, SSG_FWD_MINB)
 k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float bg2,
                 const ssg_splat *__restrict__ splat, const uint32_t *__restrict__ inst_prim,
-                const int32_t *__restrict__ ranges, float *__restrict__ color,
-                float *__restrict__ final_T, int32_t *__restrict__ n_contrib,
-                int32_t *__restrict__ last_idx, uint32_t *__restrict__ blend_mask) {
+                const int32_t *__restrict__ ranges, float *__restrict__ color, float *__restrict__ final_T,
+                int32_t *__restrict__ n_contrib, int32_t *__restrict__ last_idx, uint32_t *__restrict__ blend_mask,
+                uint32_t *__restrict__ redo_mask, uint32_t *__restrict__ redo_list,
+                uint32_t *__restrict__ redo_count) {
     __shared__ SmemBatch s;
     const int tile = blockIdx.x;
     const int tyi = tile / ntx, txi = tile - tyi * ntx;
@@ -167,14 +218,12 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
     const double ox = (double)(txi * 16), oy = (double)(tyi * 16);
 
     float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
+    float dT = 0.0f;      // bound on |T - T_reference|
     int nc = 0, li = -1;
-    int done = !inside;
-#ifdef SSG_BLEND_STATS
-    __shared__ int sTileH[kThreads / 32];
-    if (lane == 0) sTileH[warp] = 0;
-#endif
+    int done = !inside;   // bit 0: stopped / outside, bit 1: met a decision its bounds cannot certify
     const uint32_t aA = smem_addr(s.A), aB = smem_addr(s.B), aC = smem_addr(s.C);
     const uint32_t aX = smem_addr(s.X), aD = smem_addr(s.D);
+    int kdone = start;    // instances [start, kdone) walked by this warp (mask words written)
 
     for (int base = start; base < end; base += kBatch) {
         if (__syncthreads_count(done) == kThreads) break;
@@ -182,57 +231,59 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
             stage_splat(splat, inst_prim[base + threadIdx.x], ox, oy, s, threadIdx.x);
         __syncthreads();
         const int cnt = min(kBatch, end - base);
-#ifdef SSG_BLEND_STATS
-        int bh = 0;  // this warp's hits in the batch (imbalance diagnostics)
-#endif
         for (int c0 = 0; c0 < cnt; c0 += 32) {
             if (__all_sync(0xffffffffu, done)) break;
+            kdone = base + c0 + 32;
             const int i = c0 + lane;
             bool hit = false;
             if (i < cnt)
                 hit = ellipse_meets_block(lds128(aA + 16 * i), lds128(aB + 16 * i), lds128(aX + 16 * i), fwx0, fwy0);
             unsigned mask = __ballot_sync(0xffffffffu, hit);
             uint32_t lbits = 0;  // instances of this chunk the lane's pixel blended
-#ifdef SSG_BLEND_STATS
-            if (lane == 0) SSG_STAT(0, __popc(mask));
-            bh += __popc(mask);
-#endif
             while (mask) {
+                const uint32_t lowb = mask & (0u - mask);
                 const int bit = __ffs(mask) - 1;
-                mask &= mask - 1;
+                mask ^= lowb;
                 const int j = c0 + bit;
                 // branch-free per lane (the warp skips an instance no live
                 // pixel can blend); blending lanes run exactly the
                 // reference's operations, the others carry zero weight
                 const float4 A = lds128(aA + 16 * j);
                 const float4 B = lds128(aB + 16 * j);
-                const float dx = fx - A.x, dy = fy - A.y;
-                const float power = -0.5f * (A.z * dx * dx + B.x * dy * dy) - A.w * dx * dy;   // :133-135
-                const bool live = !done && power >= B.y && power <= 0.0f;
+                Pair q;
+                pair_power(fx, fy, A, B, q);
+                const bool live = !done && q.power >= B.y && q.power <= 0.0f;
                 if (!__any_sync(0xffffffffu, live)) continue;
                 const float4 C = lds128(aC + 16 * j);
-                const float cb = lds32(aD + 4 * j);
-                float E = 1.0f, o = C.x;
-                if (!kVanilla && (B.z != 0.0f || B.w != 0.0f)) {     // warp-uniform
-                    const float z = (B.z * dx + B.w * dy) * SSG_SQRT1_2;   // :136
-                    E = skew_E(z);                                          // :137
-                    o = fmaf(C.y, E - 1.0f, C.x);                           // :138
+                const float4 D = lds128(aD + 16 * j);
+                pair_alpha<kVanilla>(B, C, q);
+                const float alpha = fminf(q.A, SSG_ALPHA_MAX);                              // :140
+                const float dA = q.A - SSG_ALPHA_SKIP;
+                const bool pass = live && dA >= D.y;           // certainly >= 1/255 (:141-142)
+                const float gp = fmaf(D.w, -q.power, D.z);     // this pair's relative alpha error bound
+                // uncertain: the 1/255 skip, or the backward's clamp cut (A <= 0.99, :290)
+                bool bad = live & ((fabsf(dA) < D.y) | (fabsf(q.A - SSG_ALPHA_MAX) <= SSG_ALPHA_MAX * gp));
+                const float test_T = T * (1.0f - alpha);                                      // :143
+                const bool near = pass && test_T < kNearT + dT;
+                bool stop = false;
+                if (__any_sync(0xffffffffu, near)) {
+                    // |T (1 - alpha) - T_ref (1 - alpha_ref)| <= dT (1 - alpha) + T alpha gp
+                    //   + 2 roundings per blend so far (eps / 2 each, relative)
+                    const float err = fmaf(dT, 1.0f - alpha, T * alpha * gp) +
+                                      (float)(nc + __popc(lbits) + 2) * 6e-8f * test_T;
+                    bad |= near & (fabsf(test_T - SSG_T_STOP) <= err);
+                    stop = near & (test_T < SSG_T_STOP);                                      // :144-147
                 }
-                const float pw = fminf(power, 0.0f);
-                const float Aval = kVanilla ? o * fast_exp2(pw * SSG_LOG2E)
-                                            : o * fast_exp2(pw * SSG_LOG2E) * E;      // :139
-                const float alpha = fminf(Aval, SSG_ALPHA_MAX);                         // :140
-                const bool pass = live && alpha >= SSG_ALPHA_SKIP;                     // :141-142
-                const float test_T = T * (1.0f - alpha);                                // :143
-                const bool stop = pass && test_T < SSG_T_STOP;                          // :144-147
-                const bool blend = pass && !stop;                                       // :148-154
-                done |= stop;
+                const bool blend = pass & !stop & !bad;                                       // :148-154
+                done |= (int)stop | ((int)bad << 1);      // bit 1: exact path
                 const float w = blend ? alpha * T : 0.0f;
                 C0 = fmaf(w, C.z, C0);
                 C1 = fmaf(w, C.w, C1);
-                C2 = fmaf(w, cb, C2);
+                C2 = fmaf(w, D.x, C2);
+                const float omb = blend ? 1.0f - alpha : 1.0f;
+                dT = fmaf(w, gp, dT * omb);
                 T = blend ? test_T : T;
-                lbits |= (uint32_t)blend << bit;
+                lbits |= blend ? lowb : 0u;
             }
             // n_contrib and last_idx from the chunk's blend bits (ascending k)
             if (lbits) {
@@ -241,45 +292,267 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
             }
             if (blend_mask) {
                 const uint32_t bmask = __reduce_or_sync(0xffffffffu, lbits);
-#ifdef SSG_BLEND_STATS
-                if (lane == 0) SSG_STAT(1, __popc(bmask));
-#endif
                 if (lane == 0) blend_mask[mask_word(start, tile, (base - start + c0) >> 5, warp)] = bmask;
             }
         }
-#ifdef SSG_BLEND_STATS
-        {   // per batch: the slowest warp's hits vs the warps' total (barrier imbalance)
-            __shared__ int sH[kThreads / 32];
-            if (lane == 0) sH[warp] = bh;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                int mx = 0, sm = 0;
-                for (int w = 0; w < kThreads / 32; w++) { mx = max(mx, sH[w]); sm += sH[w]; }
-                SSG_STAT(2, mx);
-                SSG_STAT(3, sm);
-            }
-            if (lane == 0) sTileH[warp] += bh;
-            __syncthreads();
-        }
-#endif
     }
-#ifdef SSG_BLEND_STATS
-    __syncthreads();
-    if (threadIdx.x == 0) {  // per tile: the slowest warp's hits vs the total
-        int mx = 0, sm = 0;
-        for (int w = 0; w < kThreads / 32; w++) { mx = max(mx, sTileH[w]); sm += sTileH[w]; }
-        SSG_STAT(4, mx);
-        SSG_STAT(5, sm);
-    }
-#endif
+    // the mask words past this warp's walk are zeroed, so every word of the
+    // tile is valid for the exact path (which reads a pixel's candidates there)
+    if (blend_mask)
+        for (int c = (kdone - start) / 32 + lane; c < (end - start + 31) / 32; c += 32)
+            blend_mask[mask_word(start, tile, c, warp)] = 0u;
+    const bool unsure = (done & 2) && inside;
+    const uint32_t redo = __ballot_sync(0xffffffffu, unsure);
+    if (lane == 0) redo_mask[(size_t)tile * kWarps + warp] = redo;
     if (inside) {  // :158-166
         const int64_t pix = (int64_t)py * W + px;
-        color[3 * pix] = C0 + T * bg0;
-        color[3 * pix + 1] = C1 + T * bg1;
-        color[3 * pix + 2] = C2 + T * bg2;
-        final_T[pix] = T;
-        n_contrib[pix] = nc;
-        last_idx[pix] = li;
+        if (unsure) {
+            // exact path: every blend of this pixel so far is <= li and set in
+            // the warp's mask words; it resumes the scan at li + 1
+            redo_list[atomicAdd(redo_count, 1u)] = (uint32_t)pix;
+            last_idx[pix] = li;
+        } else {
+            color[3 * pix] = C0 + T * bg0;
+            color[3 * pix + 1] = C1 + T * bg1;
+            color[3 * pix + 2] = C2 + T * bg2;
+            final_T[pix] = T;
+            n_contrib[pix] = nc;
+            last_idx[pix] = li;
+        }
+    }
+}
+
+// ------------------------------------------------------------ exact path
+// One flagged pixel, evaluated by one warp.
+struct RedoPixel {
+    int px, py, tile, tx, ty, start, end, warp_in_tile;
+    double pxc, pyc, ox, oy;
+    float fx, fy;
+};
+__device__ __forceinline__ RedoPixel redo_pixel(uint32_t pix, int32_t W, int32_t ntx, const int32_t *ranges) {
+    RedoPixel r;
+    r.py = (int)(pix / (uint32_t)W);
+    r.px = (int)(pix - (uint32_t)r.py * (uint32_t)W);
+    r.tx = r.px >> 4;
+    r.ty = r.py >> 4;
+    r.tile = r.ty * ntx + r.tx;
+    r.start = ranges[2 * r.tile];
+    r.end = ranges[2 * r.tile + 1];
+    const int lx = r.px & 15, ly = r.py & 15;
+    r.warp_in_tile = (ly >> 2) * 2 + (lx >> 3);
+    r.fx = (float)lx + 0.5f;
+    r.fy = (float)ly + 0.5f;
+    r.ox = (double)(r.tx * 16);
+    r.oy = (double)(r.ty * 16);
+    r.pxc = (double)r.px + 0.5;   // _core.pyx:131-132
+    r.pyc = (double)r.py + 0.5;
+    return r;
+}
+
+// Could instance p's alpha at this pixel reach 1/255?  fp32 alpha >=
+// (1/255) (1 - band): a superset of the reference's passing instances (the
+// band bounds the fp32 error).  Lean: no culling data, just the pair.
+template <bool kVanilla>
+__device__ __forceinline__ bool redo_maybe(const RedoPixel &P, const ssg_splat *splat, uint32_t p) {
+    const double2 m = __ldg(reinterpret_cast<const double2 *>(splat + p));
+    const float4 q1 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 1);
+    const float4 q2 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 2);
+    const float4 q3 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 3);
+    const float4 A = make_float4((float)(m.x - P.ox), (float)(m.y - P.oy), q1.x, q1.y);
+    const float4 B = make_float4(q1.z, 0.0f, q1.w, q2.x);
+    const float4 C = make_float4(0.5f * (q2.y + q2.z), 0.5f * (q2.y - q2.z), 0.0f, 0.0f);
+    Pair q;
+    pair_power(P.fx, P.fy, A, B, q);
+    pair_alpha<kVanilla>(B, C, q);
+    return q.A >= SSG_ALPHA_SKIP * (1.0f - fmaf(6.3f, q3.w, q3.z));
+}
+
+// Collect, in order, the instances k in [kb, kend) that redo_maybe admits.
+// Instances k <= kmask are taken from the pixel's warp-block blend mask (a
+// superset of the pixel's blends there: 32 mask words per load, only set
+// bits evaluated); later ones by a full scan (four chunks in flight per step
+// to cover load latency).  Fills list[0, n) and returns n; kb advances past
+// the examined instances (stops early when the segment is full).
+template <bool kVanilla>
+__device__ __forceinline__ int redo_candidates(const RedoPixel &P, int &kb, int kend, int kmask,
+                                               const uint32_t *blend_mask, const ssg_splat *splat,
+                                               const uint32_t *inst_prim, uint32_t *list) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    int n = 0;
+    // mask-driven part: chunks are aligned to start + 32 c
+    while (kb < kend && kb <= kmask && n <= kCand - 32) {
+        const int c0 = (kb - P.start) >> 5;
+        const int kstop = min(kend, kmask + 1);
+        const int nch = min(32, ((kstop - P.start + 31) >> 5) - c0);
+        uint32_t word = 0;
+        if (lane < nch) word = blend_mask[mask_word(P.start, P.tile, c0 + lane, P.warp_in_tile)];
+        int c = 0;
+        for (; c < nch && n <= kCand - 32; c++) {
+            const int kc = P.start + 32 * (c0 + c);
+            uint32_t bits = __shfl_sync(0xffffffffu, word, c);
+            const int lo = max(kb, kc), hi = min(kstop, kc + 32);     // [lo, hi) of this chunk
+            if (lo >= hi) continue;
+            bits &= (hi - kc >= 32 ? 0xffffffffu : ((1u << (hi - kc)) - 1u)) & ~((1u << (lo - kc)) - 1u);
+            const int k = kc + lane;
+            const bool maybe = ((bits >> lane) & 1u) && redo_maybe<kVanilla>(P, splat, inst_prim[k]);
+            const uint32_t b = __ballot_sync(0xffffffffu, maybe);
+            if (maybe) list[n + __popc(b & lt)] = (uint32_t)k;
+            n += __popc(b);
+        }
+        kb = min(kstop, P.start + 32 * (c0 + c));
+        if (kb == kmask + 1) break;
+    }
+    while (kb < kend && n <= kCand - 128) {
+        uint32_t p[4];
+        bool v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int k = kb + 32 * u + lane;
+            v[u] = k < kend;
+            p[u] = v[u] ? inst_prim[k] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const bool maybe = v[u] && redo_maybe<kVanilla>(P, splat, p[u]);
+            const uint32_t b = __ballot_sync(0xffffffffu, maybe);
+            if (maybe) list[n + __popc(b & lt)] = (uint32_t)(kb + 32 * u + lane);
+            n += __popc(b);
+        }
+        kb = min(kend, kb + 128);
+    }
+    __syncwarp();
+    return n;
+}
+
+// inclusive prefix product / sum over the warp's lanes, and the warp sum (fp64)
+__device__ __forceinline__ double warp_prefix_prod(double f) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, f, off);
+        if (lane >= off) f *= y;
+    }
+    return f;
+}
+__device__ __forceinline__ double warp_prefix_sum(double f) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, f, off);
+        if (lane >= off) f += y;
+    }
+    return f;
+}
+__device__ __forceinline__ double warp_sum(double f) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) f += __shfl_xor_sync(0xffffffffu, f, off);
+    return f;
+}
+
+// The exact front-to-back blend of one pixel (raster/_core.pyx:125-166) over
+// the tile's instances [start, kend), in fp64 with the reference's
+// decisions: the pass test on fp64 alphas, transmittance as a prefix
+// product, the first passing instance whose test_T < 1e-4 stops the pixel
+// unblended (with_stop).  Calls visit(k, p, pair, alpha, T_before, blended)
+// on every lane for every round (lanes in instance order).  Returns the
+// final transmittance; nc / li as the reference counts them.
+template <bool kVanilla, typename Visit>
+__device__ __forceinline__ double redo_blend(const RedoPixel &P, int kend, int kmask, const uint32_t *blend_mask,
+                                             bool with_stop, const ssg_splat *splat, const ssg_splat64 *splat64,
+                                             const uint32_t *inst_prim, uint32_t *list, int &nc, int &li,
+                                             Visit &&visit) {
+    const int lane = threadIdx.x & 31;
+    double T = 1.0;
+    nc = 0;
+    li = -1;
+    int kb = P.start;
+    bool stopped = false;
+    while (kb < kend && !stopped) {
+        const int n = redo_candidates<kVanilla>(P, kb, kend, kmask, blend_mask, splat, inst_prim, list);
+        for (int r = 0; r < n && !stopped; r += 32) {
+            const int idx = r + lane;
+            const bool valid = idx < n;
+            const int k = valid ? (int)list[idx] : 0;
+            uint32_t p = 0;
+            bool pass = false;
+            double al = 0.0;
+            RefPair rp = {};
+            if (valid) {
+                p = inst_prim[k];
+                const double2 m = __ldg(reinterpret_cast<const double2 *>(splat + p));
+                rp = ref_pair(P.pxc, P.pyc, m.x, m.y, splat64[p], kVanilla);
+                al = rp.A < 0.99 ? rp.A : 0.99;                        // :140
+                pass = !rp.skip && al >= 1.0 / 255.0;                  // :133-135, :141-142
+            }
+            const double f = pass ? 1.0 - al : 1.0;
+            const double incl = warp_prefix_prod(f);
+            double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+            if (lane == 0) excl = 1.0;
+            const double Tb = T * excl;
+            const bool stop_l = with_stop && pass && T * incl < 1e-4;  // :143-147
+            const uint32_t sb = __ballot_sync(0xffffffffu, stop_l);
+            const int first = sb ? __ffs(sb) - 1 : 32;
+            const bool blended = pass && lane < first;
+            visit(k, p, rp, al, Tb, blended);
+            const uint32_t bb = __ballot_sync(0xffffffffu, blended);
+            nc += __popc(bb);
+            if (bb) li = __shfl_sync(0xffffffffu, k, 31 - __clz(bb));
+            if (sb) {
+                T = __shfl_sync(0xffffffffu, Tb, first);
+                stopped = true;
+            } else {
+                T = T * __shfl_sync(0xffffffffu, incl, 31);
+            }
+        }
+        __syncwarp();
+    }
+    return T;
+}
+
+template <bool kVanilla>
+__global__ void __launch_bounds__(32 * kRedoWarps)
+k_blend_forward_redo(int32_t ntx, int32_t W, float bg0, float bg1, float bg2, const ssg_splat *__restrict__ splat,
+                     const ssg_splat64 *__restrict__ splat64, const uint32_t *__restrict__ inst_prim,
+                     const int32_t *__restrict__ ranges, float *__restrict__ color, float *__restrict__ final_T,
+                     int32_t *__restrict__ n_contrib, int32_t *__restrict__ last_idx,
+                     uint32_t *__restrict__ blend_mask, const uint32_t *__restrict__ redo_list,
+                     const uint32_t *__restrict__ redo_count) {
+    __shared__ uint32_t s_list[kRedoWarps][kCand];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t count = *redo_count;
+    for (uint32_t i = blockIdx.x * kRedoWarps + wid; i < count; i += gridDim.x * kRedoWarps) {
+        const uint32_t pix = redo_list[i];
+        const RedoPixel P = redo_pixel(pix, W, ntx, ranges);
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0;  // per-lane partial colour
+        int nc, li;
+        // the main kernel left the pixel's last certified blend in last_idx
+        const int kmask = blend_mask ? last_idx[pix] : -1;
+        const double T = redo_blend<kVanilla>(
+            P, P.end, kmask, blend_mask, true, splat, splat64, inst_prim, s_list[wid], nc, li,
+            [&](int k, uint32_t p, const RefPair &, double al, double Tb, bool blended) {
+                if (!blended) return;
+                const float4 q2 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 2);
+                const float4 q3 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 3);
+                const double w = al * Tb;                               // :148-152
+                c0 += w * (double)q2.w;
+                c1 += w * (double)q3.x;
+                c2 += w * (double)q3.y;
+                if (blend_mask)
+                    atomicOr(&blend_mask[mask_word(P.start, P.tile, (k - P.start) >> 5, P.warp_in_tile)],
+                             1u << ((k - P.start) & 31));
+            });
+        c0 = warp_sum(c0);
+        c1 = warp_sum(c1);
+        c2 = warp_sum(c2);
+        if (lane == 0) {  // :158-166
+            color[3 * (size_t)pix] = (float)(c0 + T * bg0);
+            color[3 * (size_t)pix + 1] = (float)(c1 + T * bg1);
+            color[3 * (size_t)pix + 2] = (float)(c2 + T * bg2);
+            final_T[pix] = (float)T;
+            n_contrib[pix] = nc;
+            last_idx[pix] = li;
+        }
     }
 }
 
@@ -318,15 +591,33 @@ __device__ __forceinline__ float warp_reduce_transposed12(float (&v)[12], int la
 // d_z * SQRT1_2 of _core.pyx:293-302 (d_z = DA G (2/sqrt(pi)) e^-z^2 (o + (o1-o2)E/2))
 constexpr float kDzScale = SSG_TWO_OVER_SQRT_PI * SSG_SQRT1_2;
 
-__global__ void __launch_bounds__(kThreads, SSG_BWD_MINB)
+// destination row of instance (k, p) of tile (tx, ty) in the three modes:
+// 0 = per-primitive accumulator, 1 = per-instance (M,12) slots
+// (_core.pyx:309-312), 2 = primitive-major row prim_row[p] + rank of the tile
+// in p's rectangle (ascending instance order per primitive)
+template <int kMode>
+__device__ __forceinline__ float *dest_row(float *out, int k, uint32_t p, int tx, int ty, const uint64_t *prim_row,
+                                           const uint64_t *tile_rect) {
+    if (kMode == 0) return out + (size_t)p * 12;
+    if (kMode == 1) return out + (size_t)k * 12;
+    const uint64_t rc = tile_rect[p];
+    const int x0 = (int)(rc & 0xffff), x1 = (int)((rc >> 16) & 0xffff), y0 = (int)((rc >> 32) & 0xffff);
+    const uint64_t rank = (uint64_t)(ty - y0) * (uint64_t)(x1 - x0) + (uint64_t)(tx - x0);
+    return out + (size_t)(prim_row[p] + rank) * 12;
+}
+
+template <int kMode>
+__global__ void __launch_bounds__(kThreads, kMode == 0 ? SSG_BWD_MINB : 1)
 k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float bg2,
                  const ssg_splat *__restrict__ splat, const uint32_t *__restrict__ inst_prim,
                  const int32_t *__restrict__ ranges, const float *__restrict__ final_T,
                  const int32_t *__restrict__ last_idx, const uint32_t *__restrict__ blend_mask,
-                 const float *__restrict__ dL, float *__restrict__ grad_screen, float *__restrict__ slots) {
+                 const uint32_t *__restrict__ redo_mask, const float *__restrict__ dL, float *__restrict__ out,
+                 const uint64_t *__restrict__ prim_row, const uint64_t *__restrict__ tile_rect) {
     __shared__ SmemBatch s;
     __shared__ float *sRow[kBatch];  // destination gradient row of each staged instance
-    __shared__ int sMax[kThreads / 32];
+    __shared__ int sMax[kWarps];
+    extern __shared__ __align__(16) float s_part[];  // deterministic modes: [warp][instance][12]
     const int tile = blockIdx.x;
     const int tyi = tile / ntx, txi = tile - tyi * ntx;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -340,10 +631,11 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
     const float fwx0 = (float)wx0, fwy0 = (float)wy0;
     const double ox = (double)(txi * 16), oy = (double)(tyi * 16);
 
-    // _core.pyx:232-246
+    // _core.pyx:232-246; pixels on the exact path are done by the redo kernel
     float T = 1.0f, d0 = 0.0f, d1 = 0.0f, d2 = 0.0f;
     int li = -1;
-    if (inside) {
+    const bool redo = (redo_mask[(size_t)tile * kWarps + warp] >> lane) & 1u;
+    if (inside && !redo) {
         const int64_t pix = (int64_t)py * W + px;
         T = final_T[pix];
         li = last_idx[pix];
@@ -357,7 +649,7 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
     __syncthreads();
     int maxli = sMax[0];
 #pragma unroll
-    for (int w = 1; w < kThreads / 32; w++) maxli = max(maxli, sMax[w]);
+    for (int w = 1; w < kWarps; w++) maxli = max(maxli, sMax[w]);
     if (maxli < start) return;  // any_hit == 0 (:245-246); block-uniform
     const int hi = min(maxli + 1, end);
     const uint32_t aA = smem_addr(s.A), aB = smem_addr(s.B), aC = smem_addr(s.C);
@@ -365,6 +657,7 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
     // lane 8g + 2c (c < 3) holds component 3g + c after the reduction
     const bool holder = (lane & 1) == 0 && ((lane >> 1) & 3) < 3;
     const int my_comp = 3 * (lane >> 3) + ((lane >> 1) & 3);
+    float *part = kMode != 0 ? s_part + (size_t)warp * kBatch * 12 : nullptr;
 
     // batches aligned to the forward's chunk grid (start + 256 b), top down
     for (int b = (hi - start - 1) / kBatch; b >= 0; b--) {
@@ -378,9 +671,11 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
         if ((int)threadIdx.x < cnt) {
             const uint32_t p = inst_prim[lo + threadIdx.x];
             stage_splat(splat, p, ox, oy, s, threadIdx.x);
-            // per-primitive accumulator, or (plugin slot mode) the per-instance
-            // (M,12) slot row of _core.pyx:309-312 (raster/backward.py:70-73)
-            sRow[threadIdx.x] = slots ? slots + (size_t)(lo + threadIdx.x) * 12 : grad_screen + (size_t)p * 12;
+            sRow[threadIdx.x] = dest_row<kMode>(out, lo + threadIdx.x, p, txi, tyi, prim_row, tile_rect);
+        }
+        if (kMode != 0) {  // this warp's partial sums of the batch start at zero
+            for (int i = lane; i < cnt * 3; i += 32)
+                reinterpret_cast<float4 *>(part)[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
         }
         __syncthreads();
 
@@ -398,103 +693,401 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                                               fwy0);
                 mask = __ballot_sync(0xffffffffu, hit);
             }
-#ifdef SSG_BLEND_STATS
-            if (lane == 0) SSG_STAT(16, __popc(mask));
-#endif
-            // per-lane replay of instance j (global index k): updates T, R
-            // and writes the 12 slot values g (zero off-contribution)
-            auto replay = [&](int j, int k, float (&g)[12], bool &live, bool &contrib) {
-                // Branch-free per lane (every visited instance has a
-                // contributing pixel, so no warp-wide skip is lost): lanes that
-                // do not contribute compute with a zero weight and keep T, R;
-                // contributing lanes run exactly the reference's operations.
+            while (mask) {
+                const int bit = 31 - __clz(mask);
+                mask &= ~(1u << bit);
+                const int j = c0 + bit;
+                // Branch-free per lane: lanes that do not contribute compute
+                // with a zero weight and keep T, R; contributing lanes run
+                // exactly the reference's operations (every decision here
+                // was certified by the forward for non-redo pixels).
                 const float4 A = lds128(aA + 16 * j);
                 const float4 B = lds128(aB + 16 * j);
+                Pair q;
+                pair_power(fx, fy, A, B, q);
+                const bool live = lo + j <= li && q.power >= B.y && q.power <= 0.0f;   // :263-264, :265-269
+                if (!blend_mask && !__any_sync(0xffffffffu, live)) continue;
                 const float4 C = lds128(aC + 16 * j);
-                const float cb = lds32(aD + 4 * j);
-                const float dx = fx - A.x, dy = fy - A.y;
-                const float power = -0.5f * (A.z * dx * dx + B.x * dy * dy) - A.w * dx * dy;
-                live = k <= li && power >= B.y && power <= 0.0f;                           // :263-264, :265-269
-                const float pw = fminf(power, 0.0f);   // == power on live lanes; finite exps elsewhere
-                const bool skewed = (B.z != 0.0f || B.w != 0.0f);                          // warp-uniform
-                float E = 1.0f, z = 0.0f, o = C.x;
-                if (skewed) {
-                    z = (B.z * dx + B.w * dy) * SSG_SQRT1_2;
-                    E = skew_E(z);
-                    o = fmaf(C.y, E - 1.0f, C.x);
-                }
-                const float G = fast_exp2(pw * SSG_LOG2E);
-                const float Aval = o * G * E;
-                const float alpha = fminf(Aval, SSG_ALPHA_MAX);
-                contrib = live && alpha >= SSG_ALPHA_SKIP;
+                const float4 D = lds128(aD + 16 * j);
+                pair_alpha<false>(B, C, q);
+                const float alpha = fminf(q.A, SSG_ALPHA_MAX);
+                const bool contrib = live && q.A >= SSG_ALPHA_SKIP;                           // :276-277
+                if (!blend_mask && !__any_sync(0xffffffffu, contrib)) continue;
                 const float Tn = T * fast_rcp(1.0f - alpha);                                   // :280
                 T = contrib ? Tn : T;
-                const float e0 = C.z - R0, e1 = C.w - R1, e2 = cb - R2;
+                const float e0 = C.z - R0, e1 = C.w - R1, e2 = D.x - R2;
                 const float d_alpha = T * (e0 * d0 + e1 * d1 + e2 * d2);
                 const float aT = contrib ? alpha * T : 0.0f;
+                float g[12];
                 g[9] = aT * d0;
                 g[10] = aT * d1;
                 g[11] = aT * d2;
-                const float DA = contrib && Aval <= SSG_ALPHA_MAX ? d_alpha : 0.0f;            // :290
-                const float d_power = DA * Aval;
-                const float Gez2 = skewed ? fast_exp2((pw - z * z) * SSG_LOG2E) : G;
-                const float dzs = (DA * kDzScale) * Gez2 * fmaf(C.y, E, o);
-                const float px_ = d_power * dx, py_ = d_power * dy;
+                const float DA = contrib && q.A <= SSG_ALPHA_MAX ? d_alpha : 0.0f;             // :290
+                const float d_power = DA * q.A;
+                const bool skewed = (B.z != 0.0f || B.w != 0.0f);                              // warp-uniform
+                const float pw = fminf(q.power, 0.0f);
+                const float Gez2 = skewed ? fast_exp2((pw - q.z * q.z) * SSG_LOG2E) : q.G;
+                const float dzs = (DA * kDzScale) * Gez2 * fmaf(C.y, q.E, q.o);
+                const float px_ = d_power * q.dx, py_ = d_power * q.dy;
                 g[0] = fmaf(A.z, px_, fmaf(A.w, py_, -dzs * B.z));                           // -d_dx
                 g[1] = fmaf(B.x, py_, fmaf(A.w, px_, -dzs * B.w));                           // -d_dy
-                g[2] = -0.5f * px_ * dx;
-                g[3] = -px_ * dy;
-                g[4] = -0.5f * py_ * dy;
-                g[5] = dzs * dx;
-                g[6] = dzs * dy;
-                const float hGE = 0.5f * DA * G * E;
-                g[7] = hGE * E;
-                g[8] = hGE * (2.0f - E);
+                g[2] = -0.5f * px_ * q.dx;
+                g[3] = -px_ * q.dy;
+                g[4] = -0.5f * py_ * q.dy;
+                g[5] = dzs * q.dx;
+                g[6] = dzs * q.dy;
+                const float hGE = 0.5f * DA * q.G * q.E;
+                g[7] = hGE * q.E;
+                g[8] = hGE * (2.0f - q.E);
                 const float ae = contrib ? alpha : 0.0f;                                       // :306-308
                 R0 = fmaf(ae, e0, R0);
                 R1 = fmaf(ae, e1, R1);
                 R2 = fmaf(ae, e2, R2);
-#ifdef SSG_BLEND_STATS
-                const unsigned cbal = __ballot_sync(0xffffffffu, contrib);
-                if (lane == 0) {
-                    SSG_STAT(17, cbal != 0);
-                    SSG_STAT(18, __popc(cbal));
-                }
-#endif
-            };
-            // the 12 holder lanes add their component straight into the
-            // primitive's accumulator row, or (plugin slot mode) the
-            // per-instance (M,12) slot row of _core.pyx:309-312
-            // (raster/backward.py:70-73).  Two loops, so the visit itself
-            // carries no mask-mode test.
-            if (blend_mask) {
-                // the forward's mask: every visited instance has a contributing pixel
-                while (mask) {
-                    const int bit = 31 - __clz(mask);
-                    mask &= ~(1u << bit);
-                    const int j = c0 + bit;
-                    float g[12];
-                    bool live, contrib;
-                    replay(j, lo + j, g, live, contrib);
-                    const float v = warp_reduce_transposed12(g, lane);
-                    if (holder) atomicAdd(sRow[j] + my_comp, v);
-                }
-            } else {
-                // test-driven walk: skip empty hits
-                while (mask) {
-                    const int bit = 31 - __clz(mask);
-                    mask &= ~(1u << bit);
-                    const int j = c0 + bit;
-                    float g[12];
-                    bool live, contrib;
-                    replay(j, lo + j, g, live, contrib);
-                    if (!__any_sync(0xffffffffu, live) || !__any_sync(0xffffffffu, contrib)) continue;
-                    const float v = warp_reduce_transposed12(g, lane);
-                    if (holder) atomicAdd(sRow[j] + my_comp, v);
+                const float v = warp_reduce_transposed12(g, lane);
+                if (holder) {
+                    if (kMode == 0) atomicAdd(sRow[j] + my_comp, v);
+                    else part[j * 12 + my_comp] = v;
                 }
             }
         }
+        if (kMode != 0) {
+            // fixed-order combination of the eight warps' sums, one row per thread
+            __syncthreads();
+            if ((int)threadIdx.x < cnt) {
+                const int j = threadIdx.x;
+                float4 acc[3];
+#pragma unroll
+                for (int c = 0; c < 3; c++) acc[c] = reinterpret_cast<const float4 *>(s_part + j * 12)[c];
+#pragma unroll
+                for (int w = 1; w < kWarps; w++) {
+                    const float4 *src = reinterpret_cast<const float4 *>(s_part + ((size_t)w * kBatch + j) * 12);
+#pragma unroll
+                    for (int c = 0; c < 3; c++) {
+                        const float4 v = src[c];
+                        acc[c].x += v.x;
+                        acc[c].y += v.y;
+                        acc[c].z += v.z;
+                        acc[c].w += v.w;
+                    }
+                }
+                float4 *dst = reinterpret_cast<float4 *>(sRow[j]);
+#pragma unroll
+                for (int c = 0; c < 3; c++) dst[c] = acc[c];
+            }
+        }
     }
+}
+
+// Per-warp scratch of the backward redo: the candidate list and, per
+// candidate, its alpha (< 0: not passing), transmittance before it and the
+// running colour . dL up to and including it.
+struct RedoBwdSmem {
+    uint32_t list[kCand];
+    double al[kCand], tb[kCand], fdl[kCand];
+};
+
+// The 12 per-instance sums of one blended pair (raster/_core.pyx:280-305) in
+// fp64, added to the destination row (atomics in mode 0; plain adds in the
+// deterministic modes, where one warp owns all rows of its tile).
+template <int kMode>
+__device__ __forceinline__ void redo_emit(const RedoPixel &P, int k, uint32_t p, const RefPair &rp, double al,
+                                          double Tb, double d_alpha, double dl0, double dl1, double dl2,
+                                          const ssg_splat64 *splat64, float *out, const uint64_t *prim_row,
+                                          const uint64_t *tile_rect) {
+    const ssg_splat64 e = splat64[p];
+    const double DA = rp.A <= 0.99 ? d_alpha : 0.0;                                          // :290
+    const double d_power = DA * rp.A;
+    const double ez2 = exp(-rp.z * rp.z);
+    const double d_z = DA * rp.G * SSG_REF_TWO_OVER_SQRT_PI * ez2 * (rp.o + 0.5 * (e.o1 - e.o2) * rp.E);  // :293
+    const double d_dx = d_power * (-(e.conic_a * rp.dx + e.conic_b * rp.dy)) + d_z * e.skew_x * SSG_REF_SQRT1_2;
+    const double d_dy = d_power * (-(e.conic_c * rp.dy + e.conic_b * rp.dx)) + d_z * e.skew_y * SSG_REF_SQRT1_2;
+    const double aT = al * Tb;
+    float g[12];
+    g[0] = (float)(-d_dx);
+    g[1] = (float)(-d_dy);
+    g[2] = (float)(d_power * (-0.5 * rp.dx * rp.dx));
+    g[3] = (float)(d_power * (-rp.dx * rp.dy));
+    g[4] = (float)(d_power * (-0.5 * rp.dy * rp.dy));
+    g[5] = (float)(d_z * rp.dx * SSG_REF_SQRT1_2);
+    g[6] = (float)(d_z * rp.dy * SSG_REF_SQRT1_2);
+    g[7] = (float)(DA * 0.5 * rp.G * rp.E * rp.E);
+    g[8] = (float)(DA * 0.5 * (2.0 - rp.E) * rp.G * rp.E);
+    g[9] = (float)(aT * dl0);
+    g[10] = (float)(aT * dl1);
+    g[11] = (float)(aT * dl2);
+    float *row = dest_row<kMode>(out, k, p, P.tx, P.ty, prim_row, tile_rect);
+#pragma unroll
+    for (int c = 0; c < 12; c++) {
+        if (kMode == 0) atomicAdd(row + c, g[c]);
+        else row[c] += g[c];
+    }
+}
+
+// Exact backward of one flagged pixel (raster/_core.pyx:232-312 for it) in
+// fp64.  The reference's R behind instance k satisfies
+// T_before(k) R_k = (C - F_k) / (1 - alpha_k), C the pixel colour and F_k the
+// colour blended up to and including k, so one front-to-back pass gives F_k
+// (stored per candidate) and C, and a second sweep over the stored
+// candidates emits d_alpha = T_k c.dL - (C.dL - F_k.dL) / (1 - alpha_k).
+// Candidate lists longer than one segment take a two-pass fallback.
+template <int kMode>
+__device__ __forceinline__ void redo_backward_pixel(const RedoPixel &P, int li, const float *dLp, float bg0,
+                                                    float bg1, float bg2, const ssg_splat *splat,
+                                                    const ssg_splat64 *splat64, const uint32_t *inst_prim,
+                                                    const uint32_t *blend_mask, RedoBwdSmem &sm, float *out,
+                                                    const uint64_t *prim_row, const uint64_t *tile_rect) {
+    if (li < P.start) return;
+    const int lane = threadIdx.x & 31;
+    const int kend = li + 1;
+    const double dl0 = dLp[0], dl1 = dLp[1], dl2 = dLp[2];
+    int kb = P.start;
+    const int kmask = blend_mask ? li : -1;
+    const int n = redo_candidates<false>(P, kb, kend, kmask, blend_mask, splat, inst_prim, sm.list);
+    if (kb >= kend) {
+        // front to back over the candidates: alpha, T_before, F.dL
+        double T = 1.0, Fdl = 0.0;
+        for (int r = 0; r < n; r += 32) {
+            const int idx = r + lane;
+            const bool valid = idx < n;
+            double al = 0.0, cdl = 0.0;
+            bool pass = false;
+            if (valid) {
+                const int k = (int)sm.list[idx];
+                const uint32_t p = inst_prim[k];
+                const double2 m = __ldg(reinterpret_cast<const double2 *>(splat + p));
+                const RefPair rp = ref_pair(P.pxc, P.pyc, m.x, m.y, splat64[p], false);
+                al = rp.A < 0.99 ? rp.A : 0.99;
+                pass = !rp.skip && al >= 1.0 / 255.0;
+                const float4 q2 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 2);
+                const float4 q3 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 3);
+                cdl = (double)q2.w * dl0 + (double)q3.x * dl1 + (double)q3.y * dl2;
+            }
+            const double f = pass ? 1.0 - al : 1.0;
+            const double incl = warp_prefix_prod(f);
+            double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+            if (lane == 0) excl = 1.0;
+            const double Tb = T * excl;
+            const double fdl = warp_prefix_sum(pass ? al * Tb * cdl : 0.0) + Fdl;
+            if (valid) {
+                sm.al[idx] = pass ? al : -1.0;
+                sm.tb[idx] = Tb;
+                sm.fdl[idx] = fdl;
+            }
+            T *= __shfl_sync(0xffffffffu, incl, 31);
+            Fdl = __shfl_sync(0xffffffffu, fdl, 31);
+        }
+        const double Cdl = Fdl + T * ((double)bg0 * dl0 + (double)bg1 * dl1 + (double)bg2 * dl2);
+        __syncwarp();
+        for (int idx = lane; idx < n; idx += 32) {
+            const double al = sm.al[idx];
+            if (al < 0.0) continue;
+            const int k = (int)sm.list[idx];
+            const uint32_t p = inst_prim[k];
+            const double2 m = __ldg(reinterpret_cast<const double2 *>(splat + p));
+            const RefPair rp = ref_pair(P.pxc, P.pyc, m.x, m.y, splat64[p], false);
+            const float4 q2 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 2);
+            const float4 q3 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 3);
+            const double Tb = sm.tb[idx];
+            const double cdl = (double)q2.w * dl0 + (double)q3.x * dl1 + (double)q3.y * dl2;
+            const double d_alpha = Tb * cdl - (Cdl - sm.fdl[idx]) / (1.0 - al);              // :282-285
+            redo_emit<kMode>(P, k, p, rp, al, Tb, d_alpha, dl0, dl1, dl2, splat64, out, prim_row, tile_rect);
+        }
+        __syncwarp();
+        return;
+    }
+    // long candidate lists: pass 1 gives C.dL, pass 2 the gradients
+    int nc, li2;
+    double f0 = 0.0;
+    const double Tf = redo_blend<false>(P, kend, kmask, blend_mask, false, splat, splat64, inst_prim, sm.list, nc, li2,
+                                        [&](int, uint32_t p, const RefPair &, double al, double Tb, bool blended) {
+                                            if (!blended) return;
+                                            const float4 q2 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 2);
+                                            const float4 q3 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 3);
+                                            f0 += al * Tb * ((double)q2.w * dl0 + (double)q3.x * dl1 +
+                                                             (double)q3.y * dl2);
+                                        });
+    const double Cdl = warp_sum(f0) + Tf * ((double)bg0 * dl0 + (double)bg1 * dl1 + (double)bg2 * dl2);
+    double Fdl = 0.0;
+    redo_blend<false>(P, kend, kmask, blend_mask, false, splat, splat64, inst_prim, sm.list, nc, li2,
+                      [&](int k, uint32_t p, const RefPair &rp, double al, double Tb, bool blended) {
+                          double cdl = 0.0;
+                          if (blended) {
+                              const float4 q2 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 2);
+                              const float4 q3 = __ldg(reinterpret_cast<const float4 *>(splat + p) + 3);
+                              cdl = (double)q2.w * dl0 + (double)q3.x * dl1 + (double)q3.y * dl2;
+                          }
+                          const double fdl = warp_prefix_sum(blended ? al * Tb * cdl : 0.0) + Fdl;
+                          Fdl = __shfl_sync(0xffffffffu, fdl, 31);
+                          if (!blended) return;
+                          const double d_alpha = Tb * cdl - (Cdl - fdl) / (1.0 - al);
+                          redo_emit<kMode>(P, k, p, rp, al, Tb, d_alpha, dl0, dl1, dl2, splat64, out, prim_row,
+                                           tile_rect);
+                      });
+}
+
+// mode 0: one warp per listed pixel (any order: the rows take atomics)
+__global__ void __launch_bounds__(32 * kRedoWarps)
+k_blend_backward_redo_list(int32_t ntx, int32_t W, float bg0, float bg1, float bg2, const ssg_splat *__restrict__ splat,
+                           const ssg_splat64 *__restrict__ splat64, const uint32_t *__restrict__ inst_prim,
+                           const int32_t *__restrict__ ranges, const int32_t *__restrict__ last_idx,
+                           const float *__restrict__ dL, const uint32_t *__restrict__ blend_mask,
+                           const uint32_t *__restrict__ redo_list, const uint32_t *__restrict__ redo_count,
+                           float *__restrict__ out) {
+    __shared__ RedoBwdSmem s_redo[kRedoWarps];
+    const int wid = threadIdx.x >> 5;
+    const uint32_t count = *redo_count;
+    for (uint32_t i = blockIdx.x * kRedoWarps + wid; i < count; i += gridDim.x * kRedoWarps) {
+        const uint32_t pix = redo_list[i];
+        const RedoPixel P = redo_pixel(pix, W, ntx, ranges);
+        redo_backward_pixel<0>(P, last_idx[pix], dL + 3 * (size_t)pix, bg0, bg1, bg2, splat, splat64, inst_prim,
+                               blend_mask, s_redo[wid], out, nullptr, nullptr);
+    }
+}
+
+// deterministic modes: one warp per tile, its flagged pixels in a fixed order
+template <int kMode>
+__global__ void __launch_bounds__(32 * kRedoWarps)
+k_blend_backward_redo_tiles(int32_t ntx, int32_t n_tiles, int32_t W, float bg0, float bg1, float bg2,
+                            const ssg_splat *__restrict__ splat, const ssg_splat64 *__restrict__ splat64,
+                            const uint32_t *__restrict__ inst_prim, const int32_t *__restrict__ ranges,
+                            const int32_t *__restrict__ last_idx, const float *__restrict__ dL,
+                            const uint32_t *__restrict__ blend_mask, const uint32_t *__restrict__ redo_mask,
+                            float *__restrict__ out,
+                            const uint64_t *__restrict__ prim_row, const uint64_t *__restrict__ tile_rect) {
+    __shared__ RedoBwdSmem s_redo[kRedoWarps];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int tile = blockIdx.x * kRedoWarps + wid;
+    if (tile >= n_tiles) return;
+    const uint32_t word = lane < kWarps ? redo_mask[(size_t)tile * kWarps + lane] : 0u;
+    if (!__any_sync(0xffffffffu, word != 0u)) return;
+    const int ty = tile / ntx, tx = tile - ty * ntx;
+    for (int w = 0; w < kWarps; w++) {
+        uint32_t bits = __shfl_sync(0xffffffffu, word, w);
+        while (bits) {
+            const int l = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int px = tx * 16 + (w & 1) * 8 + (l & 7), py = ty * 16 + (w >> 1) * 4 + (l >> 3);
+            const uint32_t pix = (uint32_t)py * (uint32_t)W + (uint32_t)px;
+            const RedoPixel P = redo_pixel(pix, W, ntx, ranges);
+            redo_backward_pixel<kMode>(P, last_idx[pix], dL + 3 * (size_t)pix, bg0, bg1, bg2, splat, splat64,
+                                       inst_prim, blend_mask, s_redo[wid], out, prim_row, tile_rect);
+            __syncwarp();
+        }
+    }
+}
+
+// deterministic mode: depth rank of each primitive (inverse of the depth order)
+__global__ void k_depth_rank(int64_t n, const uint32_t *__restrict__ order, uint32_t *__restrict__ rank) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) rank[order[r]] = (uint32_t)r;
+}
+
+// deterministic mode: first primitive-major row of each primitive
+// (rank_offset is the exclusive scan of the counts in depth order)
+__global__ void k_prim_rows(int64_t n, const uint32_t *__restrict__ rank, const uint64_t *__restrict__ rank_offset,
+                            uint64_t *__restrict__ prim_row) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) prim_row[p] = rank_offset[rank[p]];
+}
+
+// deterministic mode: each primitive's rows summed in ascending instance
+// order (raster/backward.py:70-73: np.add.at visits k in order)
+__global__ void k_reduce_prim_rows(int64_t n, const uint64_t *__restrict__ prim_row,
+                                   const uint32_t *__restrict__ count, const float *__restrict__ rows,
+                                   float *__restrict__ screen) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    float4 acc[3] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f),
+                     make_float4(0.f, 0.f, 0.f, 0.f)};
+    const uint64_t r0 = prim_row[p];
+    const uint32_t c = count[p];
+    for (uint32_t i = 0; i < c; i++) {
+        const float4 *src = reinterpret_cast<const float4 *>(rows + (size_t)(r0 + i) * 12);
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+            const float4 v = src[q];
+            acc[q].x += v.x;
+            acc[q].y += v.y;
+            acc[q].z += v.z;
+            acc[q].w += v.w;
+        }
+    }
+    float4 *dst = reinterpret_cast<float4 *>(screen + (size_t)p * 12);
+#pragma unroll
+    for (int q = 0; q < 3; q++) dst[q] = acc[q];
+}
+
+__global__ void k_erf_probe(const double *x, int64_t n, float *e32, double *e64) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (e32) e32[i] = skew_E((float)x[i]);
+    if (e64) e64[i] = ref_erf(x[i]);
+}
+
+constexpr size_t kDetSmem = sizeof(float) * kWarps * kBatch * 12;
+
+// per-device one-time launch setup (function attributes are per device)
+struct DevSetup {
+    int redo_grid;
+};
+static int dev_setup(DevSetup &out) {
+    static DevSetup cache[64];
+    static bool ready[64] = {false};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess || dev < 0 || dev >= 64) { set_error("cudaGetDevice", e); return SSG_ERR_CUDA; }
+    if (!ready[dev]) {
+        e = cudaFuncSetAttribute(k_blend_backward<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDetSmem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_blend_backward<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDetSmem);
+        int sms = 148;
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) { set_error("blend setup", e); return SSG_ERR_CUDA; }
+        cache[dev].redo_grid = sms * 12;  // 48 redo warps per SM
+        ready[dev] = true;
+    }
+    out = cache[dev];
+    return SSG_OK;
+}
+
+static int launch_forward(bool vanilla, int32_t width, int32_t height, const float bg[3], const ssg_splat *splat,
+                          const ssg_splat64 *splat64, const ssg_bin_buffers *bins, const ssg_frame_buffers *frame,
+                          int32_t flags, cudaStream_t st) {
+    DevSetup ds;
+    int rc = dev_setup(ds);
+    if (rc != SSG_OK) return rc;
+    const int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
+    if (!(flags & SSG_BLEND_EXACT_ONLY)) {
+        cudaError_t e = cudaMemsetAsync(frame->redo_count, 0, sizeof(uint32_t), st);
+        if (e != cudaSuccess) { set_error("memset redo count", e); return SSG_ERR_CUDA; }
+        if (vanilla)
+            k_blend_forward<true><<<ntx * nty, kThreads, 0, st>>>(
+                ntx, width, height, bg[0], bg[1], bg[2], splat, bins->inst_prim, bins->ranges, frame->color,
+                frame->final_T, frame->n_contrib, frame->last_idx, frame->blend_mask, frame->redo_mask,
+                frame->redo_list, frame->redo_count);
+        else
+            k_blend_forward<false><<<ntx * nty, kThreads, 0, st>>>(
+                ntx, width, height, bg[0], bg[1], bg[2], splat, bins->inst_prim, bins->ranges, frame->color,
+                frame->final_T, frame->n_contrib, frame->last_idx, frame->blend_mask, frame->redo_mask,
+                frame->redo_list, frame->redo_count);
+        rc = check_launch("k_blend_forward");
+        if (rc != SSG_OK) return rc;
+    }
+    if (flags & SSG_BLEND_MAIN_ONLY) return SSG_OK;
+    if (vanilla)
+        k_blend_forward_redo<true><<<ds.redo_grid, 32 * kRedoWarps, 0, st>>>(
+            ntx, width, bg[0], bg[1], bg[2], splat, splat64, bins->inst_prim, bins->ranges, frame->color,
+            frame->final_T, frame->n_contrib, frame->last_idx, frame->blend_mask, frame->redo_list, frame->redo_count);
+    else
+        k_blend_forward_redo<false><<<ds.redo_grid, 32 * kRedoWarps, 0, st>>>(
+            ntx, width, bg[0], bg[1], bg[2], splat, splat64, bins->inst_prim, bins->ranges, frame->color,
+            frame->final_T, frame->n_contrib, frame->last_idx, frame->blend_mask, frame->redo_list, frame->redo_count);
+    return check_launch("k_blend_forward_redo");
+}
+
+static bool frame_ok(const ssg_frame_buffers *f) {
+    return f && f->color && f->final_T && f->n_contrib && f->last_idx && f->redo_mask && f->redo_list &&
+           f->redo_count;
 }
 
 }  // namespace ssg
@@ -505,77 +1098,159 @@ extern "C" int64_t ssg_blend_mask_words(int64_t m, int32_t n_tiles) {
 }
 
 extern "C" int ssg_blend_forward(int64_t m, int32_t width, int32_t height, const float background[3],
-                                 const ssg_splat *splat, const ssg_bin_buffers *bins,
+                                 const ssg_splat *splat, const ssg_splat64 *splat64, const ssg_bin_buffers *bins,
                                  const ssg_frame_buffers *frame, void *stream) {
     using namespace ssg;
-    if (!bins || !frame || !background || width < 1 || height < 1) return SSG_ERR_INVALID_ARGUMENT;
+    if (!bins || !frame_ok(frame) || !background || !splat64 || width < 1 || height < 1)
+        return SSG_ERR_INVALID_ARGUMENT;
     if (width > SSG_MAX_IMAGE_DIM || height > SSG_MAX_IMAGE_DIM) return SSG_ERR_DIM_OVERFLOW;
     (void)m;
-    int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
-    cudaStream_t st = (cudaStream_t)stream;
-    k_blend_forward<false><<<ntx * nty, kThreads, 0, st>>>(ntx, width, height, background[0], background[1],
-                                                           background[2], splat, bins->inst_prim, bins->ranges,
-                                                           frame->color, frame->final_T, frame->n_contrib,
-                                                           frame->last_idx, frame->blend_mask);
-    return check_launch("k_blend_forward");
+    return launch_forward(false, width, height, background, splat, splat64, bins, frame, 0, (cudaStream_t)stream);
+}
+
+extern "C" int ssg_blend_forward_ex(int64_t m, int32_t width, int32_t height, const float background[3],
+                                    const ssg_splat *splat, const ssg_splat64 *splat64, const ssg_bin_buffers *bins,
+                                    const ssg_frame_buffers *frame, int32_t flags, void *stream) {
+    using namespace ssg;
+    if (!bins || !frame_ok(frame) || !background || !splat64 || width < 1 || height < 1 ||
+        (flags & ~(SSG_BLEND_MAIN_ONLY | SSG_BLEND_EXACT_ONLY)) ||
+        (flags & (SSG_BLEND_MAIN_ONLY | SSG_BLEND_EXACT_ONLY)) == (SSG_BLEND_MAIN_ONLY | SSG_BLEND_EXACT_ONLY))
+        return SSG_ERR_INVALID_ARGUMENT;
+    if (width > SSG_MAX_IMAGE_DIM || height > SSG_MAX_IMAGE_DIM) return SSG_ERR_DIM_OVERFLOW;
+    (void)m;
+    return launch_forward(false, width, height, background, splat, splat64, bins, frame, flags,
+                          (cudaStream_t)stream);
 }
 
 extern "C" int ssg_test_blend_forward_vanilla(int32_t width, int32_t height, const float background[3],
-                                              const ssg_splat *splat, const ssg_bin_buffers *bins,
-                                              const ssg_frame_buffers *frame, void *stream) {
+                                              const ssg_splat *splat, const ssg_splat64 *splat64,
+                                              const ssg_bin_buffers *bins, const ssg_frame_buffers *frame,
+                                              void *stream) {
     using namespace ssg;
-    if (!bins || !frame || !background || width < 1 || height < 1) return SSG_ERR_INVALID_ARGUMENT;
+    if (!bins || !frame_ok(frame) || !background || !splat64 || width < 1 || height < 1)
+        return SSG_ERR_INVALID_ARGUMENT;
+    return launch_forward(true, width, height, background, splat, splat64, bins, frame, 0, (cudaStream_t)stream);
+}
+
+extern "C" int ssg_blend_backward_ex(int64_t n, int64_t m, int32_t width, int32_t height,
+                                     const float background[3], const ssg_splat *splat, const ssg_splat64 *splat64,
+                                     const ssg_bin_buffers *bins, const ssg_frame_buffers *frame,
+                                     const float *dL_dpixels, const ssg_grad_buffers *grads, int32_t flags,
+                                     void *stream) {
+    using namespace ssg;
+    if (!bins || !frame || !frame->final_T || !frame->last_idx || !frame->redo_mask || !frame->redo_list ||
+        !frame->redo_count || !grads || !background || !dL_dpixels || !splat64 || width < 1 || height < 1 || n < 0 ||
+        (flags & ~(SSG_BLEND_MAIN_ONLY | SSG_BLEND_EXACT_ONLY | SSG_BLEND_NO_ZERO)) ||
+        (flags & (SSG_BLEND_MAIN_ONLY | SSG_BLEND_EXACT_ONLY)) == (SSG_BLEND_MAIN_ONLY | SSG_BLEND_EXACT_ONLY))
+        return SSG_ERR_INVALID_ARGUMENT;
+    (void)m;
+    DevSetup ds;
+    int rc = dev_setup(ds);
+    if (rc != SSG_OK) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!(flags & SSG_BLEND_NO_ZERO)) {
+        cudaError_t e = cudaMemsetAsync(grads->screen, 0, sizeof(float) * 12 * (size_t)n, st);
+        if (e != cudaSuccess) { set_error("memset screen grads", e); return SSG_ERR_CUDA; }
+    }
     int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
-    k_blend_forward<true><<<ntx * nty, kThreads, 0, (cudaStream_t)stream>>>(
-        ntx, width, height, background[0], background[1], background[2], splat, bins->inst_prim, bins->ranges,
-        frame->color, frame->final_T, frame->n_contrib, frame->last_idx, nullptr);
-    return check_launch("k_blend_forward<vanilla>");
+    if (!(flags & SSG_BLEND_EXACT_ONLY)) {
+        k_blend_backward<0><<<ntx * nty, kThreads, 0, st>>>(ntx, width, height, background[0], background[1],
+                                                            background[2], splat, bins->inst_prim, bins->ranges,
+                                                            frame->final_T, frame->last_idx, frame->blend_mask,
+                                                            frame->redo_mask, dL_dpixels, grads->screen, nullptr,
+                                                            nullptr);
+        rc = check_launch("k_blend_backward");
+        if (rc != SSG_OK) return rc;
+    }
+    if (flags & SSG_BLEND_MAIN_ONLY) return SSG_OK;
+    k_blend_backward_redo_list<<<ds.redo_grid, 32 * kRedoWarps, 0, st>>>(
+        ntx, width, background[0], background[1], background[2], splat, splat64, bins->inst_prim, bins->ranges,
+        frame->last_idx, dL_dpixels, frame->blend_mask, frame->redo_list, frame->redo_count, grads->screen);
+    return check_launch("k_blend_backward_redo");
 }
 
 extern "C" int ssg_blend_backward(int64_t n, int64_t m, int32_t width, int32_t height,
-                                  const float background[3], const ssg_splat *splat,
+                                  const float background[3], const ssg_splat *splat, const ssg_splat64 *splat64,
                                   const ssg_bin_buffers *bins, const ssg_frame_buffers *frame,
                                   const float *dL_dpixels, const ssg_grad_buffers *grads, void *stream) {
+    return ssg_blend_backward_ex(n, m, width, height, background, splat, splat64, bins, frame, dL_dpixels, grads, 0,
+                                 stream);
+}
+
+extern "C" size_t ssg_blend_det_temp_bytes(int64_t n, int64_t m) {
+    if (n < 0 || m < 0) return 0;
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    return al(sizeof(uint32_t) * (size_t)(n + 1)) + al(sizeof(uint64_t) * (size_t)(n + 1)) +
+           al(sizeof(float) * 12 * (size_t)(m + 1));
+}
+
+extern "C" int ssg_blend_backward_det(int64_t n, int64_t m, int32_t width, int32_t height,
+                                      const float background[3], const ssg_splat *splat, const ssg_splat64 *splat64,
+                                      const ssg_prim_buffers *prim, const ssg_bin_buffers *bins,
+                                      const ssg_frame_buffers *frame, const float *dL_dpixels,
+                                      const ssg_grad_buffers *grads, void *temp, size_t temp_bytes, void *stream) {
     using namespace ssg;
-    if (!bins || !frame || !grads || !background || !dL_dpixels || width < 1 || height < 1 || n < 0)
+    if (!bins || !frame || !frame->final_T || !frame->last_idx || !frame->redo_mask || !grads || !prim ||
+        !background || !dL_dpixels || !splat64 || width < 1 || height < 1 || n < 0 || m < 0 || !temp)
         return SSG_ERR_INVALID_ARGUMENT;
-    (void)m;
+    if (temp_bytes < ssg_blend_det_temp_bytes(n, m)) return SSG_ERR_CAPACITY;
+    DevSetup ds;
+    int rc = dev_setup(ds);
+    if (rc != SSG_OK) return rc;
     cudaStream_t st = (cudaStream_t)stream;
-    cudaError_t e = cudaMemsetAsync(grads->screen, 0, sizeof(float) * 12 * (size_t)n, st);
-    if (e != cudaSuccess) { set_error("memset screen grads", e); return SSG_ERR_CUDA; }
-    int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
-    k_blend_backward<<<ntx * nty, kThreads, 0, st>>>(ntx, width, height, background[0], background[1],
-                                                     background[2], splat, bins->inst_prim, bins->ranges,
-                                                     frame->final_T, frame->last_idx, frame->blend_mask,
-                                                     dL_dpixels, grads->screen, nullptr);
-    return check_launch("k_blend_backward");
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    char *t = (char *)temp;
+    uint32_t *rank = (uint32_t *)t;
+    uint64_t *prim_row = (uint64_t *)(t + al(sizeof(uint32_t) * (size_t)(n + 1)));
+    float *rows = (float *)(t + al(sizeof(uint32_t) * (size_t)(n + 1)) + al(sizeof(uint64_t) * (size_t)(n + 1)));
+    cudaError_t e = cudaMemsetAsync(rows, 0, sizeof(float) * 12 * (size_t)m, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(grads->screen, 0, sizeof(float) * 12 * (size_t)n, st);
+    if (e != cudaSuccess) { set_error("memset det rows", e); return SSG_ERR_CUDA; }
+    if (n == 0) return SSG_OK;
+    const unsigned gb = (unsigned)((n + 255) / 256);
+    k_depth_rank<<<gb, 256, 0, st>>>(n, bins->depth_order, rank);
+    k_prim_rows<<<gb, 256, 0, st>>>(n, rank, bins->rank_offset, prim_row);
+    const int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
+    k_blend_backward<2><<<ntx * nty, kThreads, kDetSmem, st>>>(
+        ntx, width, height, background[0], background[1], background[2], splat, bins->inst_prim, bins->ranges,
+        frame->final_T, frame->last_idx, frame->blend_mask, frame->redo_mask, dL_dpixels, rows, prim_row,
+        prim->tile_rect);
+    k_blend_backward_redo_tiles<2><<<(ntx * nty + kRedoWarps - 1) / kRedoWarps, 32 * kRedoWarps, 0, st>>>(
+        ntx, ntx * nty, width, background[0], background[1], background[2], splat, splat64, bins->inst_prim,
+        bins->ranges, frame->last_idx, dL_dpixels, frame->blend_mask, frame->redo_mask, rows, prim_row,
+        prim->tile_rect);
+    k_reduce_prim_rows<<<gb, 256, 0, st>>>(n, prim_row, prim->tile_count, rows, grads->screen);
+    return check_launch("k_blend_backward(det)");
 }
 
 extern "C" int ssg_blend_backward_slots(int64_t m, int32_t width, int32_t height, const float background[3],
-                                        const ssg_splat *splat, const ssg_bin_buffers *bins,
-                                        const ssg_frame_buffers *frame, const float *dL_dpixels, float *slots,
-                                        void *stream) {
+                                        const ssg_splat *splat, const ssg_splat64 *splat64,
+                                        const ssg_bin_buffers *bins, const ssg_frame_buffers *frame,
+                                        const float *dL_dpixels, float *slots, void *stream) {
     using namespace ssg;
-    if (!bins || !frame || !background || !dL_dpixels || !slots || width < 1 || height < 1 || m < 0)
+    if (!bins || !frame || !frame->final_T || !frame->last_idx || !frame->redo_mask || !background ||
+        !dL_dpixels || !slots || !splat64 || width < 1 || height < 1 || m < 0)
         return SSG_ERR_INVALID_ARGUMENT;
+    DevSetup ds;
+    int rc = dev_setup(ds);
+    if (rc != SSG_OK) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(slots, 0, sizeof(float) * 12 * (size_t)m, st);
     if (e != cudaSuccess) { set_error("memset slots", e); return SSG_ERR_CUDA; }
-    int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
-    k_blend_backward<<<ntx * nty, kThreads, 0, st>>>(ntx, width, height, background[0], background[1],
-                                                     background[2], splat, bins->inst_prim, bins->ranges,
-                                                     frame->final_T, frame->last_idx, frame->blend_mask,
-                                                     dL_dpixels, nullptr, slots);
+    const int32_t ntx = (width + SSG_TILE - 1) / SSG_TILE, nty = (height + SSG_TILE - 1) / SSG_TILE;
+    k_blend_backward<1><<<ntx * nty, kThreads, kDetSmem, st>>>(
+        ntx, width, height, background[0], background[1], background[2], splat, bins->inst_prim, bins->ranges,
+        frame->final_T, frame->last_idx, frame->blend_mask, frame->redo_mask, dL_dpixels, slots, nullptr, nullptr);
+    k_blend_backward_redo_tiles<1><<<(ntx * nty + kRedoWarps - 1) / kRedoWarps, 32 * kRedoWarps, 0, st>>>(
+        ntx, ntx * nty, width, background[0], background[1], background[2], splat, splat64, bins->inst_prim,
+        bins->ranges, frame->last_idx, dL_dpixels, frame->blend_mask, frame->redo_mask, slots, nullptr, nullptr);
     return check_launch("k_blend_backward(slots)");
 }
 
-#ifdef SSG_BLEND_STATS
-extern "C" int ssg_test_blend_stats(unsigned long long *out, int reset) {
-    cudaError_t e = cudaMemcpyFromSymbol(out, g_blend_stats, sizeof(unsigned long long) * 32);
-    if (e == cudaSuccess && reset) {
-        static const unsigned long long zero[32] = {0};
-        e = cudaMemcpyToSymbol(g_blend_stats, zero, sizeof(zero));
-    }
-    return e == cudaSuccess ? SSG_OK : SSG_ERR_CUDA;
+extern "C" int ssg_erf_probe(const double *x, int64_t n, float *e32, double *e64, void *stream) {
+    using namespace ssg;
+    if (n < 0 || (n > 0 && !x)) return SSG_ERR_INVALID_ARGUMENT;
+    if (n == 0) return SSG_OK;
+    k_erf_probe<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(x, n, e32, e64);
+    return check_launch("k_erf_probe");
 }
-#endif

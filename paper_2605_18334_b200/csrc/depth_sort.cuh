@@ -70,7 +70,7 @@ constexpr unsigned long long kReady = 1ull << 63;  // tile_sums flag (final phas
 constexpr int kMaxPasses = 8;                 // 64-bit keys, byte digits
 constexpr int kSub = kThreads / 256;          // threads per digit in the prefix sums
 constexpr int kPre = 4;                       // tiles per multi-tile prefix sweep
-static_assert(kThreads % 256 == 0, "prefix sums map 256 digits x kSub threads");
+static_assert(kThreads == 1024, "prefix_sweep maps 64 digit quads x 16 lanes: exactly 1024 threads");
 
 __host__ __device__ inline int64_t num_tiles(int64_t n) { return (n + kTile - 1) / kTile; }
 
@@ -528,19 +528,25 @@ static inline cudaError_t sort_and_scan(const uint64_t *keys, uint32_t *order, c
     cudaError_t e = cudaMemsetAsync(&a.ctl->kmin, 0xff, sizeof(unsigned long long), st);  // min identity
     if (e == cudaSuccess) e = cudaMemsetAsync(&a.ctl->kmax, 0, 2 * sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
-    static int grid_max = 0;
+    // the smem attribute and the co-resident grid size belong to the device:
+    // cached per device ordinal (function attributes are per device)
+    static int grid_max_dev[64] = {0};
     const int smem = (int)sizeof(Smem);
-    if (grid_max == 0) {
+    int dev = 0;
+    e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (grid_max_dev[dev] == 0) {
         e = cudaFuncSetAttribute(k_depth_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        int dev = 0, sms = 0, per = 0;
-        cudaGetDevice(&dev);
+        int sms = 0, per = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_depth_sort, kThreads, smem);
         if (e != cudaSuccess) return e;
         if (per < 1) return cudaErrorInvalidConfiguration;
-        grid_max = sms * per;
+        grid_max_dev[dev] = sms * per;
     }
+    const int grid_max = grid_max_dev[dev];
     const int grid = (int)(nt < grid_max ? nt : grid_max);
     void *params[] = {&a};
     return cudaLaunchCooperativeKernel((const void *)k_depth_sort, dim3(grid), dim3(kThreads), params, smem, st);

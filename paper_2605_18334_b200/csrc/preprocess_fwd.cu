@@ -79,13 +79,26 @@ k_preprocess_forward(ssg_scene sc, ssg_camera cam, ssg_prim_buffers out, int ntx
         s.r = fmaxf(col[0] + 0.5f, 0.0f);
         s.g = fmaxf(col[1] + 0.5f, 0.0f);
         s.b = fmaxf(col[2] + 0.5f, 0.0f);
-        s.pad0 = 0;
-        s.pad1 = 0;
-        // 64-byte record as four 16-byte stores
+        // fp64 twin of the blend inputs + the fp32 alpha error band
+        ssg_splat64 e;
+        e.conic_a = P.inv_dil[0];
+        e.conic_b = P.inv_dil[1];
+        e.conic_c = P.inv_dil[3];
+        e.skew_x = P.skew[0];
+        e.skew_y = P.skew[1];
+        e.o1 = P.sig[0] * P.comp;   // projection.py:209-210
+        e.o2 = P.sig[1] * P.comp;
+        e.pad = 0.0;
+        s.band0 = alpha_band(e.conic_a, e.conic_b, e.conic_c, e.skew_x, e.skew_y, e.o1, e.o2, &s.band1);
+        // 64-byte records as four 16-byte stores each
         const int4 *src = reinterpret_cast<const int4 *>(&s);
         int4 *dst = reinterpret_cast<int4 *>(out.splat + i);
 #pragma unroll
         for (int j = 0; j < 4; j++) dst[j] = src[j];
+        const int4 *src64 = reinterpret_cast<const int4 *>(&e);
+        int4 *dst64 = reinterpret_cast<int4 *>(out.splat64 + i);
+#pragma unroll
+        for (int j = 0; j < 4; j++) dst64[j] = src64[j];
 
         // tile rectangle and count (tiles.py:49-57)
         uint64_t rect;
@@ -126,4 +139,54 @@ extern "C" int ssg_preprocess_forward(const ssg_scene *scene, const ssg_camera *
         default: k_preprocess_forward<3><<<blocks, 256, 0, st>>>(*scene, *cam, *out, ntx, nty); break;
     }
     return check_launch("k_preprocess_forward");
+}
+
+// Screen records from caller fp64 arrays (the plugin slot's inputs,
+// raster/_core.pyx:169-177): the fp32 splat (+ its alpha band) and the fp64
+// twin the threshold path reads.
+namespace ssg {
+__global__ void k_pack_splats(int64_t n, const double *__restrict__ mean2d, const double *__restrict__ conic,
+                              const double *__restrict__ skew2d, const double *__restrict__ opair,
+                              const double *__restrict__ color, ssg_splat *__restrict__ splat,
+                              ssg_splat64 *__restrict__ splat64) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    ssg_splat64 e;
+    e.conic_a = conic[3 * i];
+    e.conic_b = conic[3 * i + 1];
+    e.conic_c = conic[3 * i + 2];
+    e.skew_x = skew2d[2 * i];
+    e.skew_y = skew2d[2 * i + 1];
+    e.o1 = opair[2 * i];
+    e.o2 = opair[2 * i + 1];
+    e.pad = 0.0;
+    ssg_splat s;
+    s.mean_x = mean2d[2 * i];
+    s.mean_y = mean2d[2 * i + 1];
+    s.conic_a = (float)e.conic_a;
+    s.conic_b = (float)e.conic_b;
+    s.conic_c = (float)e.conic_c;
+    s.skew_x = (float)e.skew_x;
+    s.skew_y = (float)e.skew_y;
+    s.o1 = (float)e.o1;
+    s.o2 = (float)e.o2;
+    s.r = (float)color[3 * i];
+    s.g = (float)color[3 * i + 1];
+    s.b = (float)color[3 * i + 2];
+    s.band0 = alpha_band(e.conic_a, e.conic_b, e.conic_c, e.skew_x, e.skew_y, e.o1, e.o2, &s.band1);
+    splat[i] = s;
+    splat64[i] = e;
+}
+}  // namespace ssg
+
+extern "C" int ssg_pack_splats(int64_t n, const double *mean2d, const double *conic, const double *skew2d,
+                               const double *opair, const double *color, ssg_splat *splat, ssg_splat64 *splat64,
+                               void *stream) {
+    using namespace ssg;
+    if (n < 0 || (n > 0 && (!mean2d || !conic || !skew2d || !opair || !color || !splat || !splat64)))
+        return SSG_ERR_INVALID_ARGUMENT;
+    if (n == 0) return SSG_OK;
+    k_pack_splats<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, mean2d, conic, skew2d, opair,
+                                                                               color, splat, splat64);
+    return check_launch("k_pack_splats");
 }

@@ -289,6 +289,128 @@ __device__ __forceinline__ float skew_E(float z) {
     return z > 0.0f ? 2.0f - y : y;
 }
 
+// ------------------------------------------- fp64 reference alpha (rare path)
+// raster/_core.pyx:33-35: the 33 Maclaurin coefficients (-1)^n / (n! (2n+1)),
+// generated by the reference's own recurrence (fact *= n in fp64) and written
+// out exactly (hex), so the table is bit-identical to the reference's.
+static __constant__ double kRefErfCoef[33] = {
+    0x1.0000000000000p+0,  -0x1.5555555555555p-2,  0x1.999999999999ap-4,   -0x1.8618618618618p-6,
+    0x1.2f684bda12f68p-8,  -0x1.8d3018d3018d3p-11, 0x1.c01c01c01c01cp-14,  -0x1.bbd779334ef0bp-17,
+    0x1.87a00187a0018p-20, -0x1.3777c55568ccdp-23, 0x1.c2e3054870b38p-27,  -0x1.2b67310aa9f3ap-30,
+    0x1.6f448e13e85e1p-34, -0x1.a289ee7e40f74p-38, 0x1.bd577e658d020p-42,  -0x1.bc6250fb14231p-46,
+    0x1.a173a167fba4dp-50, -0x1.7271cbe5863ecp-54, 0x1.377c2110f2083p-58,  -0x1.f1b4073b34a68p-63,
+    0x1.7abd72258fb6ep-67, -0x1.13246abce1bddp-71, 0x1.7e6b81382cd42p-76,  -0x1.fd6bebd65107ap-81,
+    0x1.45c0a838efe59p-85, -0x1.909c9de3a31c5p-90, 0x1.da7460554e5dap-95,  -0x1.0eef30fa10d2cp-99,
+    0x1.2ac65385f79acp-104, -0x1.3e81bb5701ac5p-109, 0x1.4899fcdef0a8ep-114, -0x1.486eea20c2656p-119,
+    0x1.3e53defc4e233p-124};
+#define SSG_REF_SQRT1_2 0.7071067811865476           // raster/_core.pyx:27
+#define SSG_REF_TWO_OVER_SQRT_PI 1.1283791670955126  // raster/_core.pyx:28
+#define SSG_REF_SQRT_PI 1.7724538509055159           // raster/_core.pyx:29
+
+// c_erf (raster/_core.pyx:57-74), operation for operation (no contraction).
+static __device__ __noinline__ double ref_erf(double x) {
+    const double ax = fabs(x);
+    double y;
+    if (ax <= 2.0) {
+        const double u = __dmul_rn(ax, ax);
+        double poly = 0.0;
+        for (int k = 32; k >= 0; k--) poly = __dadd_rn(__dmul_rn(poly, u), kRefErfCoef[k]);
+        y = __dmul_rn(__dmul_rn(SSG_REF_TWO_OVER_SQRT_PI, ax), poly);
+    } else if (ax < 6.5) {
+        double t = 0.0;
+        for (int k = 48; k > 0; k--) t = __ddiv_rn(__dmul_rn(0.5, (double)k), __dadd_rn(ax, t));
+        y = __dsub_rn(1.0, __ddiv_rn(__ddiv_rn(exp(-__dmul_rn(ax, ax)), SSG_REF_SQRT_PI), __dadd_rn(ax, t)));
+    } else {
+        y = 1.0;
+    }
+    return x < 0.0 ? -y : y;
+}
+
+// One pixel-instance pair of the reference blend in fp64 (raster/_core.pyx:
+// 129-139 forward, :265-305 backward quantities) from the fp64 splat inputs:
+// dx = px - mx with px = col + 0.5, power, z, E = 1 + erf(z), o = mix_opacity,
+// G = exp(power), A = o G E (pre-clamp alpha).  skip = power > 0 (the
+// reference skips before any erf, :133-135).  no_skew evaluates the skew
+// term as zero (the plain-3DGS regression kernel).  Used only on the exact
+// (redo) path, for pixels whose fp32 evaluation met an uncertain decision.
+// erf is CUDA's (<= 2 ulp): like c_erf (ref_erf above, exposed through
+// ssg_erf_probe) it is accurate to a few fp64 ulps, so alpha agrees with the
+// reference's to ~1e-15 relative and a decision could differ only for an
+// alpha that close to a threshold; c_erf's continued fraction (|z| > 2)
+// would cost 48 fp64 divisions per pair.
+struct RefPair {
+    double dx, dy, power, z, E, o, G, A;
+    bool skip;
+};
+static __device__ __noinline__ RefPair ref_pair(double pxc, double pyc, double mx, double my, const ssg_splat64 &e,
+                                                bool no_skew) {
+    RefPair r;
+    r.dx = __dsub_rn(pxc, mx);
+    r.dy = __dsub_rn(pyc, my);
+    const double q = __dadd_rn(__dmul_rn(__dmul_rn(e.conic_a, r.dx), r.dx), __dmul_rn(__dmul_rn(e.conic_c, r.dy), r.dy));
+    r.power = __dsub_rn(__dmul_rn(-0.5, q), __dmul_rn(__dmul_rn(e.conic_b, r.dx), r.dy));
+    r.skip = r.power > 0.0;
+    const double sx = no_skew ? 0.0 : e.skew_x, sy = no_skew ? 0.0 : e.skew_y;
+    r.z = __dmul_rn(__dadd_rn(__dmul_rn(sx, r.dx), __dmul_rn(sy, r.dy)), SSG_REF_SQRT1_2);
+    r.E = __dadd_rn(1.0, erf(r.z));
+    r.o = __dmul_rn(0.5, __dadd_rn(__dadd_rn(e.o1, e.o2), __dmul_rn(__dsub_rn(e.o1, e.o2), __dsub_rn(r.E, 1.0))));
+    r.G = exp(r.power);
+    r.A = __dmul_rn(__dmul_rn(r.o, r.G), r.E);
+    return r;
+}
+
+// Relative error bound of the blend's fp32 pre-clamp alpha against ref_pair
+// for one primitive, as a function of the pair's Gaussian exponent:
+// |A_fp32 / A_ref - 1| <= g0 + g1 |power|, valid wherever a decision can
+// turn on it (|power| <= ln 510 < 6.3 and z >= -2.05, i.e. A >= 1/255 is
+// reachable).  The full band g0 + 6.3 g1 serves the 1/255 skip test; the
+// per-pair value bounds the transmittance error (high-alpha pairs sit near
+// the centre, where |power| is small).  With eps = 2^-24, lambda_min/max the
+// conic's eigenvalues, |d| <= c_d sqrt|power| (c_d = sqrt(2/lambda_min)) the
+// pixel offset and sqrt|p| <= (1 + |p|)/2:
+//  * power arithmetic: conic rounded to fp32 plus ~5 roundings over
+//    |a| dx^2 + |c| dy^2 + 2|b dx dy| <= kappa * 2|power|, kappa =
+//    (max(a,c) + |b|) / lambda_min  ->  8 eps kappa |p|;
+//  * pixel offset: the tile-local fp32 mean (|m| <= |d| + 16.5) and
+//    dx = px - m round by eps (|m| + |dx|) per axis; |grad power| <=
+//    sqrt(2 lambda_max |p|)  ->  1.5 sqrt2 eps sqrt(2 lambda_max |p|) (2|d| + 16.5);
+//  * skew factor E = erfc(-z): the z error (skew rounding, offsets) times
+//    d ln E / dz <= 4.5 on z >= -2.05, plus the fp32 mix of o1, o2
+//    (<= 4 eps omax / omin, cancellation);
+//  * exp2 (2^-22) and its argument rounding (eps |power| log2e, into g1),
+//    the o * G * E products: 6e-7; the skew factor's fast erfc (Chebyshev
+//    fit, rcp + exp2 with argument (power - z^2) log2e): 2e-6 more.
+// Returns g0 and writes g1 (both 1 for a degenerate conic: always uncertain).
+__device__ __forceinline__ float alpha_band(double a, double b, double c, double sx, double sy, double o1, double o2,
+                                            float *slope) {
+    const double eps = 5.9604644775390625e-08, r2 = 1.4142135623730951;
+    const double det = a * c - b * b;
+    if (!(a > 0.0) || !(c > 0.0) || !(det > 0.0)) {
+        *slope = 1.0f;
+        return 1.0f;
+    }
+    const double half_tr = 0.5 * (a + c), disc = sqrt(0.25 * (a - c) * (a - c) + b * b);
+    const double lmax = half_tr + disc, lmin = det / lmax;
+    const double kappa = (fmax(a, c) + fabs(b)) / lmin;
+    const double cd = sqrt(2.0 / lmin), gradc = sqrt(2.0 * lmax);
+    double g0 = 6e-7, g1 = 8.0 * eps * kappa + 1.5 * eps;
+    g1 += 1.5 * r2 * eps * gradc * 2.0 * cd;                 // offset x |d|: linear in |p|
+    const double h = 1.5 * r2 * eps * gradc * 16.5;          // offset x tile: sqrt|p|
+    g0 += 0.5 * h;
+    g1 += 0.5 * h;
+    if (sx != 0.0 || sy != 0.0) {
+        const double s1 = fabs(sx) + fabs(sy);
+        g0 += 2e-6 + 4.5 * (s1 * eps * 16.5 / r2 + 4.0 * eps);
+        const double k = 4.5 * s1 * eps * 5.0 * cd / r2;     // sqrt|p| part
+        g0 += 0.5 * k;
+        g1 += 0.5 * k;
+        const double omin = fmin(o1, o2), omax = fmax(o1, o2);
+        g0 += omin > 0.0 ? 4.0 * eps * omax / omin : 1.0;
+    }
+    *slope = g1 < 1.0 ? (float)g1 : 1.0f;
+    return g0 < 1.0 ? (float)g0 : 1.0f;
+}
+
 // 32-bit shared-window loads: keeps the address arithmetic out of the
 // generic (cluster-aware) path the compiler otherwise rematerialises per use.
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {

@@ -143,6 +143,8 @@ class Engine:
         # (grid(), bin_arrays); throughput loops switch it off
         self.keep_inst_tile = True
         self.stage_events = None  # name -> [(start, end)] CUDA events when enabled
+        self.deterministic = False  # backward(): bitwise-repeatable gradients (slower)
+        self._exact_pending = None  # event of a deferred forward exact path
 
     def _mark(self, name: str):
         """Context for per-stage CUDA-event timing on the launching stream."""
@@ -170,6 +172,7 @@ class Engine:
             return
         nn = max(n, 1)
         self.splat = self._empty((nn, N.SPLAT_BYTES // 8), torch.float64)
+        self.splat64 = self._empty((nn, N.SPLAT64_BYTES // 8), torch.float64)
         self.depth_key = self._empty((nn,), torch.int64)
         self.tile_count = self._empty((nn,), torch.int32)
         self.tile_rect = self._empty((nn,), torch.int64)
@@ -188,6 +191,7 @@ class Engine:
         p.splat, p.depth_key, p.tile_count = _ptr(self.splat), _ptr(self.depth_key), _ptr(self.tile_count)
         p.tile_rect, p.valid, p.depth = _ptr(self.tile_rect), _ptr(self.valid), _ptr(self.depth)
         p.radius, p.n_skew_fallback = _ptr(self.radius), _ptr(self.n_fallback)
+        p.splat64 = _ptr(self.splat64)
         return p
 
     def _ensure_bins(self, n: int, m: int, W: int, H: int):
@@ -201,12 +205,14 @@ class Engine:
             return
         if cap != self.capacity:
             self.inst_prim = self._empty((cap,), torch.int32)
-            self.inst_tile = self._empty((cap,), torch.int16)
+            self.inst_tile = self._empty((cap,), torch.int32)
             self.capacity = cap
         words = int(self.lib.ssg_blend_mask_words(cap, max(n_tiles, 1)))
         if self.blend_mask is None or self.blend_mask.numel() < words:
             self.blend_mask = self._empty((words,), torch.int32)
         self.ranges = self._empty((n_tiles, 2), torch.int32)
+        if getattr(self, "redo_mask", None) is None or self.redo_mask.numel() < max(n_tiles, 1) * 8:
+            self.redo_mask = self._empty((max(n_tiles, 1) * 8,), torch.int32)
         nbytes = ctypes.c_size_t(0)
         N.check(self.lib.ssg_bin_temp_bytes(self._prim_n, cap, W, H, ctypes.byref(nbytes)),
                 "ssg_bin_temp_bytes")
@@ -231,11 +237,14 @@ class Engine:
         self.final_T = self._empty((H, W), torch.float32)
         self.n_contrib = self._empty((H, W), torch.int32)
         self.last_idx = self._empty((H, W), torch.int32)
+        self.redo_list = self._empty((max(W * H, 1),), torch.int32)
+        self.redo_count = self._empty((1,), torch.int32)
         self._frame_key = (W, H)
 
     def _frame_struct(self, final_T=None, last_idx=None, color=None, mask=False) -> N.SsgFrameBuffers:
         f = N.SsgFrameBuffers()
         f.blend_mask = _ptr(self.blend_mask) if mask else None
+        f.redo_mask, f.redo_list, f.redo_count = _ptr(self.redo_mask), _ptr(self.redo_list), _ptr(self.redo_count)
         f.color, f.n_contrib = _ptr(self.color if color is None else color), _ptr(self.n_contrib)
         f.final_T = _ptr(self.final_T if final_T is None else final_T)
         f.last_idx = _ptr(self.last_idx if last_idx is None else last_idx)
@@ -361,13 +370,31 @@ class Engine:
                 "ssg_bin_rects")
         return self._bin(n, W, H)
 
+    def _exact_stream(self) -> torch.cuda.Stream:
+        """Stream of the blend's exact path when it overlaps other work."""
+        if getattr(self, "_exact", None) is None:
+            self._exact = torch.cuda.Stream(self.device)
+        return self._exact
+
+    def finish_exact(self):
+        """Make the current stream wait for a deferred forward exact path
+        (the frame's flagged pixels); no-op when none is pending."""
+        if self._exact_pending is not None:
+            torch.cuda.current_stream(self.device).wait_event(self._exact_pending)
+            self._exact_pending = None
+
     def forward(self, ds: DeviceScene, view: CameraView, s: float = 0.3,
-                color_out: torch.Tensor | None = None, sync: bool = True) -> DeviceFrame:
+                color_out: torch.Tensor | None = None, sync: bool = True,
+                defer_exact: bool = False) -> DeviceFrame:
         """Project, bin and blend one view.  `color_out` (contiguous f32
         (H,W,3) on this device) receives the image instead of the engine's
         own colour buffer (view batches write straight into their slice).
         sync=False: no host round trip inside the frame (see _bin); the
-        caller checks instances() before trusting the result."""
+        caller checks instances() before trusting the result.
+        defer_exact=True: the exact path over the flagged pixels runs on a
+        second stream; the frame is complete only after finish_exact() (a
+        following backward() overlaps it with its main kernel)."""
+        self.finish_exact()
         cam = camera_struct(view, s)
         W, H = int(cam.width), int(cam.height)
         m = self.project_and_bin(ds, cam, sync)
@@ -376,21 +403,61 @@ class Engine:
                                       or not color_out.is_contiguous() or color_out.device != self.device):
             raise ValueError("color_out must be a contiguous float32 (H, W, 3) tensor on the engine device")
         bg = (ctypes.c_float * 3)(*[float(x) for x in ds.background])
+        frame = self._frame_struct(color=color_out, mask=True)
         with self._mark("blend_fwd"):
-            N.check(self.lib.ssg_blend_forward(m, W, H, bg, _ptr(self.splat), ctypes.byref(self._bins_struct()),
-                                               ctypes.byref(self._frame_struct(color=color_out, mask=True)),
-                                               self._stream()),
-                    "ssg_blend_forward")
+            if not defer_exact:
+                N.check(self.lib.ssg_blend_forward(m, W, H, bg, _ptr(self.splat), _ptr(self.splat64),
+                                                   ctypes.byref(self._bins_struct()), ctypes.byref(frame),
+                                                   self._stream()),
+                        "ssg_blend_forward")
+            else:
+                N.check(self.lib.ssg_blend_forward_ex(m, W, H, bg, _ptr(self.splat), _ptr(self.splat64),
+                                                      ctypes.byref(self._bins_struct()), ctypes.byref(frame),
+                                                      N.SSG_BLEND_MAIN_ONLY, self._stream()),
+                        "ssg_blend_forward(main)")
+        if defer_exact:
+            main, ex = torch.cuda.current_stream(self.device), self._exact_stream()
+            ev = torch.cuda.Event()
+            ev.record(main)
+            ex.wait_event(ev)
+            N.check(self.lib.ssg_blend_forward_ex(m, W, H, bg, _ptr(self.splat), _ptr(self.splat64),
+                                                  ctypes.byref(self._bins_struct()), ctypes.byref(frame),
+                                                  N.SSG_BLEND_EXACT_ONLY, ex.cuda_stream),
+                    "ssg_blend_forward(exact)")
+            self._exact_pending = torch.cuda.Event()
+            self._exact_pending.record(ex)
         self._mask_state = (self._bin_gen, _ptr(self.final_T), _ptr(self.last_idx))
         color = self.color if color_out is None else color_out
         return DeviceFrame(color, self.final_T, self.n_contrib, self.last_idx, W, H, ds.n, m, s)
 
+    def _regen_decisions(self, ds: DeviceScene, m: int, W: int, H: int, bg):
+        """Re-run the forward blend into scratch buffers for the current
+        binning: it rewrites the decision records the backward reads (blend
+        mask, exact-path pixel set).  Needed when the caller's frame did not
+        come from this engine's last forward over this binning (e.g. the
+        drop-in render_backward, which recomputes binning like the
+        reference); the decisions are the reference's, so they agree with
+        any exact forward of the same scene and view."""
+        if getattr(self, "_scratch_key", None) != (W, H):
+            self._scratch = [self._empty((H, W, 3), torch.float32), self._empty((H, W), torch.float32),
+                             self._empty((H, W), torch.int32), self._empty((H, W), torch.int32)]
+            self._scratch_key = (W, H)
+        c, t, nc, li = self._scratch
+        f = self._frame_struct(final_T=t, last_idx=li, color=c, mask=True)
+        f.n_contrib = _ptr(nc)
+        N.check(self.lib.ssg_blend_forward(m, W, H, bg, _ptr(self.splat), _ptr(self.splat64),
+                                           ctypes.byref(self._bins_struct()), ctypes.byref(f), self._stream()),
+                "ssg_blend_forward (decision records)")
+
     def backward(self, ds: DeviceScene, view: CameraView, s: float, final_T: torch.Tensor,
                  last_idx: torch.Tensor, dL: torch.Tensor, rebin: bool = True,
-                 expect_m: int | None = None) -> DeviceGrads:
+                 expect_m: int | None = None, deterministic: bool | None = None) -> DeviceGrads:
         """Blend backward + projection backward.  With rebin=True the
         projection and binning are recomputed first (raster/backward.py:49-53)
-        and `expect_m` is checked against the new instance count."""
+        and `expect_m` is checked against the new instance count.
+        deterministic (default: self.deterministic): bitwise-repeatable
+        gradients via ssg_blend_backward_det -- per-(primitive,
+        tile) sums combined in a fixed order, no atomics."""
         cam = camera_struct(view, s)
         W, H = int(cam.width), int(cam.height)
         if rebin:
@@ -400,14 +467,24 @@ class Engine:
         if expect_m is not None and m != expect_m:
             from .raster.backward import FrameMismatchError
             raise FrameMismatchError("instance count differs from the forward pass")
+        det = self.deterministic if deterministic is None else deterministic
+        if det and m < 0:
+            m = self.instances()
+        # a deferred forward exact path overlaps this backward's main kernel
+        # only when the frame is that forward's own
+        mask_ok = self._mask_state == (self._bin_gen, _ptr(final_T), _ptr(last_idx))
+        overlap = self._exact_pending is not None and mask_ok and not det
+        if not overlap:
+            self.finish_exact()
         self._ensure_frame(W, H)
         self._ensure_grads(ds.n, ds.K)
         bg = (ctypes.c_float * 3)(*[float(x) for x in ds.background])
         st = self._stream()
         gs = self._grad_struct()
-        # the forward's blend mask is reusable only for the same binning and
-        # the same frame buffers that forward wrote
-        use_mask = self._mask_state == (self._bin_gen, _ptr(final_T), _ptr(last_idx))
+        # the forward's decision records (blend mask, exact-path pixels)
+        # belong to the binning and frame buffers that forward wrote
+        if not mask_ok:
+            self._regen_decisions(ds, m, W, H, bg)
         # the projection backward's zero-fill runs on a second stream under
         # the issue-bound blend, which leaves DRAM idle; the
         # projection backward then visits only primitives with a non-zero
@@ -421,11 +498,45 @@ class Engine:
         side.wait_event(ev_start)
         N.check(self.lib.ssg_zero_prim_grads(ds.n, ds.K, ctypes.byref(gs), side.cuda_stream), "ssg_zero_prim_grads")
         ev_zero.record(side)
+        frame = self._frame_struct(final_T, last_idx, mask=True)
         with self._mark("blend_bwd"):
-            N.check(self.lib.ssg_blend_backward(ds.n, m, W, H, bg, _ptr(self.splat), ctypes.byref(self._bins_struct()),
-                                                ctypes.byref(self._frame_struct(final_T, last_idx, mask=use_mask)),
-                                                _ptr(dL), ctypes.byref(gs), st),
-                    "ssg_blend_backward")
+            if det:
+                nb = int(self.lib.ssg_blend_det_temp_bytes(ds.n, max(m, 0)))
+                if getattr(self, "_det_temp", None) is None or self._det_temp.numel() < nb:
+                    self._det_temp = self._empty((max(nb, 1),), torch.uint8)
+                N.check(self.lib.ssg_blend_backward_det(ds.n, m, W, H, bg, _ptr(self.splat), _ptr(self.splat64),
+                                                        ctypes.byref(self._prim_struct()),
+                                                        ctypes.byref(self._bins_struct()), ctypes.byref(frame),
+                                                        _ptr(dL), ctypes.byref(gs), _ptr(self._det_temp),
+                                                        self._det_temp.numel(), st),
+                        "ssg_blend_backward_det")
+            elif not overlap:
+                N.check(self.lib.ssg_blend_backward(ds.n, m, W, H, bg, _ptr(self.splat), _ptr(self.splat64),
+                                                    ctypes.byref(self._bins_struct()), ctypes.byref(frame),
+                                                    _ptr(dL), ctypes.byref(gs), st),
+                        "ssg_blend_backward")
+            else:
+                # exact half on the exact stream (after the forward's exact
+                # half, which is already queued there), main half here
+                self.g_screen[:max(ds.n, 1)].zero_()
+                ex = self._exact_stream()
+                ev = torch.cuda.Event()
+                ev.record(main)
+                ex.wait_event(ev)
+                N.check(self.lib.ssg_blend_backward_ex(ds.n, m, W, H, bg, _ptr(self.splat), _ptr(self.splat64),
+                                                       ctypes.byref(self._bins_struct()), ctypes.byref(frame),
+                                                       _ptr(dL), ctypes.byref(gs),
+                                                       N.SSG_BLEND_EXACT_ONLY | N.SSG_BLEND_NO_ZERO, ex.cuda_stream),
+                        "ssg_blend_backward(exact)")
+                N.check(self.lib.ssg_blend_backward_ex(ds.n, m, W, H, bg, _ptr(self.splat), _ptr(self.splat64),
+                                                       ctypes.byref(self._bins_struct()), ctypes.byref(frame),
+                                                       _ptr(dL), ctypes.byref(gs),
+                                                       N.SSG_BLEND_MAIN_ONLY | N.SSG_BLEND_NO_ZERO, st),
+                        "ssg_blend_backward(main)")
+                done = torch.cuda.Event()
+                done.record(ex)
+                main.wait_event(done)
+                self._exact_pending = None
         main.wait_event(ev_zero)
         sc = ds.struct()
         with self._mark("preprocess_bwd"):
@@ -435,6 +546,11 @@ class Engine:
         n = ds.n
         return DeviceGrads(self.g_flat, self.g_screen[:n], self.g_mu[:n], self.g_log_scale[:n], self.g_rot[:n],
                            self.g_sh[:n], self.g_logits[:n], self.g_eta[:n], self.g_uv[:n], self.g_z[:n])
+
+    def redo_pixels(self) -> int:
+        """Pixels of the last forward decided on the exact fp64 path
+        (synchronises)."""
+        return int(self.redo_count.item())
 
     # ------------------------------------------------------ introspection
     def grid(self, n_tiles: int):

@@ -30,24 +30,26 @@ from . import _native as N
 CORE_BUILD = 1
 KERNELS = 1
 
-_SPLAT = np.dtype([("mean", "<f8", 2), ("conic", "<f4", 3), ("skew", "<f4", 2), ("opair", "<f4", 2),
-                   ("rgb", "<f4", 3), ("pad", "<u4", 2)])
-assert _SPLAT.itemsize == N.SPLAT_BYTES
-
-
 def _device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
-def _splats(mean2d, conic, skew2d, opair, color) -> torch.Tensor:
-    n = np.asarray(mean2d).shape[0]
-    rec = np.zeros(n, dtype=_SPLAT)
-    rec["mean"] = np.asarray(mean2d, dtype=np.float64).reshape(n, 2)
-    rec["conic"] = np.asarray(conic, dtype=np.float64).reshape(n, 3)
-    rec["skew"] = np.asarray(skew2d, dtype=np.float64).reshape(n, 2)
-    rec["opair"] = np.asarray(opair, dtype=np.float64).reshape(n, 2)
-    rec["rgb"] = np.asarray(color, dtype=np.float64).reshape(n, 3)
-    return torch.from_numpy(rec.view(np.uint8)).to(_device())
+def _splats(mean2d, conic, skew2d, opair, color):
+    """Device screen records (fp32 splat with its alpha band + the fp64 twin
+    the threshold-band path reads) built by ssg_pack_splats from the fp64
+    plugin inputs."""
+    n = int(np.asarray(mean2d).shape[0])
+    dev = _device()
+
+    def up(a, w):
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64).reshape(n, w)).to(dev)
+
+    ins = [up(mean2d, 2), up(conic, 3), up(skew2d, 2), up(opair, 2), up(color, 3)]
+    sp = torch.empty((max(n, 1), N.SPLAT_BYTES // 8), dtype=torch.float64, device=dev)
+    sp64 = torch.empty((max(n, 1), N.SPLAT64_BYTES // 8), dtype=torch.float64, device=dev)
+    N.check(N.lib().ssg_pack_splats(n, *[t.data_ptr() for t in ins], sp.data_ptr(), sp64.data_ptr(),
+                                    torch.cuda.current_stream().cuda_stream), "ssg_pack_splats")
+    return sp, sp64
 
 
 def _bins(inst_prim, ranges):
@@ -74,8 +76,10 @@ def forward_tiles(mean2d, conic, skew2d, opair, color, inst_prim, ranges, tiles_
     _check_dims(width, height, ranges, tiles_x)
     L = N.lib()
     dev = _device()
-    sp = _splats(mean2d, conic, skew2d, opair, color)
+    sp, sp64 = _splats(mean2d, conic, skew2d, opair, color)
     b, keep = _bins(inst_prim, ranges)
+    ntx, nty = tiles_x, -(-height // 16)
+    redo, rlist, rcount, _ = _decision_buffers(0, ntx, nty, width, height, dev)
     color_d = torch.empty((height, width, 3), dtype=torch.float32, device=dev)
     T_d = torch.empty((height, width), dtype=torch.float32, device=dev)
     nc_d = torch.empty((height, width), dtype=torch.int32, device=dev)
@@ -83,8 +87,9 @@ def forward_tiles(mean2d, conic, skew2d, opair, color, inst_prim, ranges, tiles_
     f = N.SsgFrameBuffers()
     f.color, f.final_T, f.n_contrib, f.last_idx = (color_d.data_ptr(), T_d.data_ptr(), nc_d.data_ptr(),
                                                    li_d.data_ptr())
+    f.redo_mask, f.redo_list, f.redo_count = redo.data_ptr(), rlist.data_ptr(), rcount.data_ptr()
     bg = (ctypes.c_float * 3)(*[float(x) for x in np.asarray(background, dtype=np.float64).reshape(3)])
-    N.check(L.ssg_blend_forward(b.capacity, width, height, bg, sp.data_ptr() if sp.numel() else None,
+    N.check(L.ssg_blend_forward(b.capacity, width, height, bg, sp.data_ptr(), sp64.data_ptr(),
                                 ctypes.byref(b), ctypes.byref(f), torch.cuda.current_stream().cuda_stream),
             "ssg_blend_forward")
     out = (color_d.double().cpu().numpy(), T_d.double().cpu().numpy(), nc_d.cpu().numpy(),
@@ -93,26 +98,92 @@ def forward_tiles(mean2d, conic, skew2d, opair, color, inst_prim, ranges, tiles_
     return out
 
 
+def _decision_buffers(m, ntx, nty, width, height, dev):
+    redo = torch.empty((max(ntx * nty, 1) * 8,), dtype=torch.int32, device=dev)
+    rlist = torch.empty((max(width * height, 1),), dtype=torch.int32, device=dev)
+    rcount = torch.empty((1,), dtype=torch.int32, device=dev)
+    words = int(N.lib().ssg_blend_mask_words(max(m, 1), max(ntx * nty, 1)))
+    bmask = torch.empty((max(words, 1),), dtype=torch.int32, device=dev)
+    return redo, rlist, rcount, bmask
+
+
 def backward_tiles(mean2d, conic, skew2d, opair, color, inst_prim, ranges, tiles_x, width, height,
                    background, final_T, last_idx, dL_dpix):
-    """raster/_core.pyx:315-343 on the GPU: per-instance slots (M,12)."""
+    """raster/_core.pyx:315-343 on the GPU: per-instance slots (M,12),
+    deterministic (fixed-order combination, no atomics).  The decision
+    records the backward needs (blend mask, exact-path pixels) come from a
+    forward pass over the same inputs; its decisions are the reference's,
+    so they agree with the caller's final_T / last_idx."""
     _check_dims(width, height, ranges, tiles_x)
     L = N.lib()
     dev = _device()
-    sp = _splats(mean2d, conic, skew2d, opair, color)
+    sp, sp64 = _splats(mean2d, conic, skew2d, opair, color)
     b, keep = _bins(inst_prim, ranges)
     m = b.capacity
+    ntx, nty = tiles_x, -(-height // 16)
     T_d = torch.from_numpy(np.ascontiguousarray(final_T, dtype=np.float64)).to(dev).float()
     li_d = torch.from_numpy(np.ascontiguousarray(last_idx, dtype=np.int64)).to(dev).int()
     dL_d = torch.from_numpy(np.ascontiguousarray(dL_dpix, dtype=np.float64)).to(dev).float()
     slots = torch.empty((max(m, 1), 12), dtype=torch.float32, device=dev)
+    redo, rlist, rcount, bmask = _decision_buffers(m, ntx, nty, width, height, dev)
+    scratch = [torch.empty((height, width, 3), dtype=torch.float32, device=dev),
+               torch.empty((height, width), dtype=torch.float32, device=dev),
+               torch.empty((height, width), dtype=torch.int32, device=dev),
+               torch.empty((height, width), dtype=torch.int32, device=dev)]
+    bg = (ctypes.c_float * 3)(*[float(x) for x in np.asarray(background, dtype=np.float64).reshape(3)])
+    st = torch.cuda.current_stream().cuda_stream
+    fw = N.SsgFrameBuffers()
+    fw.color, fw.final_T, fw.n_contrib, fw.last_idx = (t.data_ptr() for t in scratch)
+    fw.blend_mask, fw.redo_mask, fw.redo_list, fw.redo_count = (bmask.data_ptr(), redo.data_ptr(), rlist.data_ptr(),
+                                                                rcount.data_ptr())
+    N.check(L.ssg_blend_forward(m, width, height, bg, sp.data_ptr(), sp64.data_ptr(), ctypes.byref(b),
+                                ctypes.byref(fw), st), "ssg_blend_forward (decision records)")
     f = N.SsgFrameBuffers()
     f.final_T, f.last_idx = T_d.data_ptr(), li_d.data_ptr()
-    bg = (ctypes.c_float * 3)(*[float(x) for x in np.asarray(background, dtype=np.float64).reshape(3)])
-    N.check(L.ssg_blend_backward_slots(m, width, height, bg, sp.data_ptr() if sp.numel() else None,
-                                       ctypes.byref(b), ctypes.byref(f), dL_d.data_ptr(), slots.data_ptr(),
-                                       torch.cuda.current_stream().cuda_stream),
+    f.blend_mask, f.redo_mask, f.redo_list, f.redo_count = (bmask.data_ptr(), redo.data_ptr(), rlist.data_ptr(),
+                                                            rcount.data_ptr())
+    N.check(L.ssg_blend_backward_slots(m, width, height, bg, sp.data_ptr(), sp64.data_ptr(),
+                                       ctypes.byref(b), ctypes.byref(f), dL_d.data_ptr(), slots.data_ptr(), st),
             "ssg_blend_backward_slots")
     out = slots[:m].double().cpu().numpy()
     del keep
     return out
+
+
+def set_num_threads(n: int) -> None:
+    """raster/_core.pyx:38-39.  The GPU kernels have no host thread pool; the
+    call is accepted (and validated) so reference callers keep working."""
+    if int(n) < 1:
+        raise ValueError("number of threads must be >= 1")
+
+
+def get_max_threads() -> int:
+    """raster/_core.pyx:42-43: the parallel width of the blend, i.e. the
+    device's resident threads (SMs x max threads per SM)."""
+    p = torch.cuda.get_device_properties(_device())
+    return int(p.multi_processor_count * p.max_threads_per_multi_processor)
+
+
+def erf_probe(x):
+    """raster/_core.pyx:46-54: the compiled erf evaluated on an array, here
+    the fp64 c_erf restatement the blend kernels' threshold path runs on the
+    device (ssg_erf_probe); same shape as x."""
+    xv = np.ascontiguousarray(x, dtype=np.float64)
+    flat = torch.from_numpy(xv.ravel()).to(_device())
+    out = torch.empty_like(flat)
+    N.check(N.lib().ssg_erf_probe(flat.data_ptr() if flat.numel() else None, int(flat.numel()), None,
+                                  out.data_ptr() if flat.numel() else None,
+                                  torch.cuda.current_stream().cuda_stream), "ssg_erf_probe")
+    return out.cpu().numpy().reshape(np.shape(x))
+
+
+def erf_probe_fp32(x):
+    """E - 1 of the fp32 blend path (1 + erf(z) evaluated as erfc(-z) with the
+    kernels' fast erfc), for accuracy checks against the reference erf."""
+    xv = np.ascontiguousarray(x, dtype=np.float64)
+    flat = torch.from_numpy(xv.ravel()).to(_device())
+    out = torch.empty(flat.shape, dtype=torch.float32, device=flat.device)
+    N.check(N.lib().ssg_erf_probe(flat.data_ptr() if flat.numel() else None, int(flat.numel()),
+                                  out.data_ptr() if flat.numel() else None, None,
+                                  torch.cuda.current_stream().cuda_stream), "ssg_erf_probe")
+    return out.double().cpu().numpy().reshape(np.shape(x)) - 1.0

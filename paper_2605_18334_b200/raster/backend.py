@@ -23,3 +23,13 @@ def active_backend(override: str | None = None) -> str:
         raise ValueError(f"unknown backend {name!r}; expected one of {_NAMES}")
     _native.lib()  # fail loudly when the extension is missing
     return "cuda"
+
+
+def kernels(override: str | None = None):
+    """Module exposing forward_tiles / backward_tiles (reference
+    backend.py:41-43): the sm_100a plugin module, whose interface is the
+    reference _core's (forward_tiles, backward_tiles, erf_probe,
+    set_num_threads, get_max_threads, KERNELS)."""
+    active_backend(override)
+    from .. import plugin
+    return plugin

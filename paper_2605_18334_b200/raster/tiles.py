@@ -43,7 +43,7 @@ def grid_from_engine(eng, ntx: int, nty: int) -> TileGrid:
     inst_prim, inst_tile, ranges = eng.grid(ntx * nty)
     return TileGrid(TILE, ntx, nty, ranges.cpu().numpy().astype(np.int64),
                     inst_prim.cpu().numpy().astype(np.int64),
-                    inst_tile.cpu().numpy().astype(np.int64) & 0xFFFF)
+                    inst_tile.cpu().numpy().astype(np.int64))
 
 
 def bin_arrays(mean2d, radius, depth, valid, width: int, height: int) -> TileGrid:

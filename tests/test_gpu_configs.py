@@ -38,7 +38,7 @@ def test_config3_plain_splats_equal_vanilla_3dgs_bitwise():
     f = eng.forward(ds, view, 0.3)
     skew_out = _frame_copy(f)
     bg = (ctypes.c_float * 3)(*[float(x) for x in ds.background])
-    N.check(N.lib().ssg_test_blend_forward_vanilla(480, 270, bg, eng.splat.data_ptr(),
+    N.check(N.lib().ssg_test_blend_forward_vanilla(480, 270, bg, eng.splat.data_ptr(), eng.splat64.data_ptr(),
                                                   ctypes.byref(eng._bins_struct()),
                                                   ctypes.byref(eng._frame_struct()),
                                                   torch.cuda.current_stream().cuda_stream), "vanilla")
@@ -68,7 +68,7 @@ def _check_lists(eng, n, m, width, height):
     """Instance lists sorted by (tile, depth, id); ranges = the tile histogram."""
     ntx, nty = grid_dims(width, height)
     ip, it, rg = eng.grid(ntx * nty)
-    tile = it.long() & 0xFFFF
+    tile = it.long()
     prim = ip.long()
     depth = eng.depth[:n][prim]
     assert bool((tile[1:] >= tile[:-1]).all())

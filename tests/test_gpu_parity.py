@@ -57,7 +57,7 @@ def test_lists_and_preprocess_match_golden(name):
     ntx, nty = grid_dims(view.width, view.height)
     inst_prim, inst_tile, ranges = eng.grid(ntx * nty)
     np.testing.assert_array_equal(inst_prim.cpu().numpy().astype(np.int64), d["inst_prim"])
-    np.testing.assert_array_equal(inst_tile.cpu().numpy().astype(np.int64) & 0xFFFF, d["inst_tile"])
+    np.testing.assert_array_equal(inst_tile.cpu().numpy().astype(np.int64), d["inst_tile"])
     np.testing.assert_array_equal(ranges.cpu().numpy().astype(np.int64), d["ranges"])
     n = len(scene)
     np.testing.assert_array_equal(eng.depth[:n].cpu().numpy(), d["p_depth"])
