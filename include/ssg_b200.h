@@ -245,6 +245,8 @@ int ssg_blend_forward(int64_t m, int32_t width, int32_t height, const float back
 #define SSG_BLEND_MAIN_ONLY 1
 #define SSG_BLEND_EXACT_ONLY 2
 #define SSG_BLEND_NO_ZERO 4
+/* (forward, test mode) every pixel takes the exact fp64 path */
+#define SSG_BLEND_ALL_EXACT 8
 int ssg_blend_forward_ex(int64_t m, int32_t width, int32_t height, const float background[3],
                          const ssg_splat *splat, const ssg_splat64 *splat64, const ssg_bin_buffers *bins,
                          const ssg_frame_buffers *frame, int32_t flags, void *stream);

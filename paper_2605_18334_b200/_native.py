@@ -22,6 +22,7 @@ SSG_PREP_BWD_ACTIVE_ONLY = 1
 SSG_BLEND_MAIN_ONLY = 1
 SSG_BLEND_EXACT_ONLY = 2
 SSG_BLEND_NO_ZERO = 4
+SSG_BLEND_ALL_EXACT = 8
 
 EXPORTS = ("ssg_abi_version", "ssg_last_error", "ssg_grid_dims", "ssg_bin_temp_bytes",
            "ssg_preprocess_forward", "ssg_bin_rects", "ssg_bin_prepare", "ssg_bin_finish", "ssg_blend_forward",

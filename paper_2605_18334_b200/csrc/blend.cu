@@ -203,7 +203,7 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
                 const int32_t *__restrict__ ranges, float *__restrict__ color, float *__restrict__ final_T,
                 int32_t *__restrict__ n_contrib, int32_t *__restrict__ last_idx, uint32_t *__restrict__ blend_mask,
                 uint32_t *__restrict__ redo_mask, uint32_t *__restrict__ redo_list,
-                uint32_t *__restrict__ redo_count) {
+                uint32_t *__restrict__ redo_count, int all_exact) {
     __shared__ SmemBatch s;
     const int tile = blockIdx.x;
     const int tyi = tile / ntx, txi = tile - tyi * ntx;
@@ -220,7 +220,9 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
     float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
     float dT = 0.0f;      // bound on |T - T_reference|
     int nc = 0, li = -1;
-    int done = !inside;   // bit 0: stopped / outside, bit 1: met a decision its bounds cannot certify
+    // bit 0: stopped / outside, bit 1: met a decision its bounds cannot certify
+    // (all_exact: every pixel takes the exact path -- a test mode)
+    int done = !inside ? 1 : (all_exact ? 2 : 0);
     const uint32_t aA = smem_addr(s.A), aB = smem_addr(s.B), aC = smem_addr(s.C);
     const uint32_t aX = smem_addr(s.X), aD = smem_addr(s.D);
     int kdone = start;    // instances [start, kdone) walked by this warp (mask words written)
@@ -1064,12 +1066,12 @@ static int launch_forward(bool vanilla, int32_t width, int32_t height, const flo
             k_blend_forward<true><<<ntx * nty, kThreads, 0, st>>>(
                 ntx, width, height, bg[0], bg[1], bg[2], splat, bins->inst_prim, bins->ranges, frame->color,
                 frame->final_T, frame->n_contrib, frame->last_idx, frame->blend_mask, frame->redo_mask,
-                frame->redo_list, frame->redo_count);
+                frame->redo_list, frame->redo_count, (flags & SSG_BLEND_ALL_EXACT) != 0);
         else
             k_blend_forward<false><<<ntx * nty, kThreads, 0, st>>>(
                 ntx, width, height, bg[0], bg[1], bg[2], splat, bins->inst_prim, bins->ranges, frame->color,
                 frame->final_T, frame->n_contrib, frame->last_idx, frame->blend_mask, frame->redo_mask,
-                frame->redo_list, frame->redo_count);
+                frame->redo_list, frame->redo_count, (flags & SSG_BLEND_ALL_EXACT) != 0);
         rc = check_launch("k_blend_forward");
         if (rc != SSG_OK) return rc;
     }
@@ -1113,7 +1115,7 @@ extern "C" int ssg_blend_forward_ex(int64_t m, int32_t width, int32_t height, co
                                     const ssg_frame_buffers *frame, int32_t flags, void *stream) {
     using namespace ssg;
     if (!bins || !frame_ok(frame) || !background || !splat64 || width < 1 || height < 1 ||
-        (flags & ~(SSG_BLEND_MAIN_ONLY | SSG_BLEND_EXACT_ONLY)) ||
+        (flags & ~(SSG_BLEND_MAIN_ONLY | SSG_BLEND_EXACT_ONLY | SSG_BLEND_ALL_EXACT)) ||
         (flags & (SSG_BLEND_MAIN_ONLY | SSG_BLEND_EXACT_ONLY)) == (SSG_BLEND_MAIN_ONLY | SSG_BLEND_EXACT_ONLY))
         return SSG_ERR_INVALID_ARGUMENT;
     if (width > SSG_MAX_IMAGE_DIM || height > SSG_MAX_IMAGE_DIM) return SSG_ERR_DIM_OVERFLOW;

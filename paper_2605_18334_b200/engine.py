@@ -145,6 +145,7 @@ class Engine:
         self.stage_events = None  # name -> [(start, end)] CUDA events when enabled
         self.deterministic = False  # backward(): bitwise-repeatable gradients (slower)
         self._exact_pending = None  # event of a deferred forward exact path
+        self.all_exact = False      # test mode: every pixel on the exact fp64 path
 
     def _mark(self, name: str):
         """Context for per-stage CUDA-event timing on the launching stream."""
@@ -406,14 +407,16 @@ class Engine:
         frame = self._frame_struct(color=color_out, mask=True)
         with self._mark("blend_fwd"):
             if not defer_exact:
-                N.check(self.lib.ssg_blend_forward(m, W, H, bg, _ptr(self.splat), _ptr(self.splat64),
-                                                   ctypes.byref(self._bins_struct()), ctypes.byref(frame),
-                                                   self._stream()),
+                N.check(self.lib.ssg_blend_forward_ex(m, W, H, bg, _ptr(self.splat), _ptr(self.splat64),
+                                                      ctypes.byref(self._bins_struct()), ctypes.byref(frame),
+                                                      N.SSG_BLEND_ALL_EXACT if self.all_exact else 0,
+                                                      self._stream()),
                         "ssg_blend_forward")
             else:
                 N.check(self.lib.ssg_blend_forward_ex(m, W, H, bg, _ptr(self.splat), _ptr(self.splat64),
                                                       ctypes.byref(self._bins_struct()), ctypes.byref(frame),
-                                                      N.SSG_BLEND_MAIN_ONLY, self._stream()),
+                                                      N.SSG_BLEND_MAIN_ONLY | (N.SSG_BLEND_ALL_EXACT if self.all_exact
+                                                                               else 0), self._stream()),
                         "ssg_blend_forward(main)")
         if defer_exact:
             main, ex = torch.cuda.current_stream(self.device), self._exact_stream()
@@ -445,8 +448,9 @@ class Engine:
         c, t, nc, li = self._scratch
         f = self._frame_struct(final_T=t, last_idx=li, color=c, mask=True)
         f.n_contrib = _ptr(nc)
-        N.check(self.lib.ssg_blend_forward(m, W, H, bg, _ptr(self.splat), _ptr(self.splat64),
-                                           ctypes.byref(self._bins_struct()), ctypes.byref(f), self._stream()),
+        N.check(self.lib.ssg_blend_forward_ex(m, W, H, bg, _ptr(self.splat), _ptr(self.splat64),
+                                              ctypes.byref(self._bins_struct()), ctypes.byref(f),
+                                              N.SSG_BLEND_ALL_EXACT if self.all_exact else 0, self._stream()),
                 "ssg_blend_forward (decision records)")
 
     def backward(self, ds: DeviceScene, view: CameraView, s: float, final_T: torch.Tensor,

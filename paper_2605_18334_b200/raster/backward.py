@@ -73,7 +73,9 @@ def _device_backward(scene, view, frame, dL):
     main.wait_stream(side)
     for t in (final_T, last_idx, dL_dev):
         t.record_stream(main)
-    g = eng.backward(ds, view, frame.s, final_T, last_idx, dL_dev, rebin=False)
+    # the reference's gradients are bit-reproducible: the
+    # drop-in uses the deterministic (fixed-order, atomic-free) reduction
+    g = eng.backward(ds, view, frame.s, final_T, last_idx, dL_dev, rebin=False, deterministic=True)
     return eng, g
 
 

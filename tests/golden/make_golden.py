@@ -65,11 +65,20 @@ def cases():
     rng = np.random.default_rng(11)
     yield "dense_400_96x80", fp32_round(random_scene(rng, 400, sh_degree=3, skew_scale=1.0, spread=0.8)), \
         random_view(rng, 96, 80), 0.3, False
+    # skew fallback (projection.py:117-121, 133): primitives whose 3D scales
+    # underflow (exp(-400)^2 = 0) have det_raw = 0 <= 1e-300, so their projected
+    # skew falls back to 0 and their eta VJP is zeroed; mixed into a normal scene
+    rng = np.random.default_rng(23)
+    sc = fp32_round(random_scene(rng, 40, sh_degree=1, skew_scale=1.0))
+    sc.log_scale[::5] = -400.0
+    yield "fallback_mix", sc, random_view(rng, 56, 40), 0.3, False
 
 
-def main():
+def main(only=()):
     assert ref_backend.active_backend() == "cython"
     for name, scene, view, s, kat in cases():
+        if only and name not in only:
+            continue
         frame = render_forward(scene, view, s=s, backend_name="cython")
         proj = project_scene(scene, view, s)
         grid = bin_arrays(proj.mean2d, proj.radius, proj.depth, proj.valid, view.width, view.height)
@@ -95,4 +104,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(tuple(sys.argv[1:]))

@@ -77,27 +77,21 @@ def test_every_sh_degree(deg):
 @pytest.mark.parametrize("wh", [(30000, 40), (40, 30000), (4100, 2100)])
 def test_very_wide_tall_and_large_images(wh):
     """Tile rows / columns far beyond the configs (up to 1875 tiles per row):
-    the per-row / per-tile bucket tables of the counting scatter.  Lists are
-    exact; with millions of pixels a few sit on the fp32-vs-fp64 alpha
-    boundary (alpha ~ 1/255: one splat more or less, n_contrib +-1), so the
-    pixel bar is the at-scale one of tests/test_gpu_parity.py."""
+    the per-row / per-tile bucket tables of the counting scatter, and splats
+    with footprints of 10^4..10^5 pixels.  The north-star bars (the blend's
+    decisions are certified, blend.cu)."""
     rng = np.random.default_rng(wh[0] + wh[1])
     view = random_view(rng, *wh, fov_x=1.2)
     scene = fp32_round(random_scene(rng, 300, sh_degree=1))
     fr = render_forward(scene, view)
     ref = O.render_forward(scene, view)
     assert fr.n_instances == ref.n_instances > 0
-    d = np.abs(fr.color - ref.color).max(axis=2)
-    assert np.mean(d <= 1e-4) >= 0.99999 and d.max() <= 5e-3
-    assert np.mean(fr.n_contrib == ref.n_contrib) >= 0.9999
-    assert np.mean(fr.last_idx == ref.last_idx) >= 0.9999
+    assert np.max(np.abs(fr.color - ref.color)) <= 1e-4
+    np.testing.assert_array_equal(fr.n_contrib, ref.n_contrib)
+    np.testing.assert_array_equal(fr.last_idx, ref.last_idx)
     dL = np.random.default_rng(7).normal(size=(view.height, view.width, 3))
     g = render_backward(scene, view, fr, dL)
     rg = O.render_backward(scene, view, ref, dL)
-    # 300 splats with footprints of 10^4..10^5 pixels each: every gradient is
-    # a long fp32 sum (the oracle's backward fed this frame agrees with it to
-    # the same degree), so the bar here is 99 % <= 1e-3 and all <= 5e-2; the
-    # configs' scenes meet the north-star bar (tests/test_gpu_configs.py)
     for k in GRADS:
         e = G.rel_floor(getattr(g, k), getattr(rg, k))
-        assert np.mean(e <= 1e-3) >= 0.99 and e.max() <= 5e-2, k
+        assert np.mean(e <= 1e-3) >= 0.999 and e.max() <= 1e-2, (k, float(np.mean(e <= 1e-3)), float(e.max()))
