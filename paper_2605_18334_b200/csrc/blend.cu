@@ -40,9 +40,10 @@
 
 namespace ssg {
 
-constexpr int kThreads = 256;
-constexpr int kBatch = 256;
+constexpr int kThreads = 128;       // blend kernels: 4 warps per 16x16 tile
+constexpr int kBatch = 256;          // instances staged per batch (2 per thread)
 constexpr int kWarps = kThreads / 32;
+constexpr int kBlocks = 8;           // 8x4-pixel blocks per tile (the redo mask's words)
 constexpr float kNearT = 1.05e-4f;   // candidate transmittance below which the stop test needs its bound
 constexpr int kCand = 256;           // redo: candidate instances per segment (per warp)
 constexpr int kRedoWarps = 4;        // redo: warps per CTA
@@ -116,7 +117,7 @@ __device__ __forceinline__ void stage_splat(const ssg_splat *splat, uint32_t p, 
 }
 
 // Does the instance's ellipse meet the rectangle spanned by the warp's pixel
-// centres [wx0+0.5, wx0+7.5] x [wy0+0.5, wy0+3.5]?  Minimum of the quadratic
+// centres [wx0+0.5, wx0+7.5] x [wy0+0.5, wy0+7.5]?  Minimum of the quadratic
 // form over the rectangle: 0 if the mean is inside, else the least of the
 // four clamped edge minima, each a sum of non-negative terms
 // a (dx + k dy)^2 + h dy^2 (no cancellation).
@@ -131,7 +132,7 @@ __device__ __forceinline__ void stage_splat(const ssg_splat *splat, uint32_t p, 
 __device__ __forceinline__ bool ellipse_meets_block(const float4 A, const float4 B, const float4 X, float wx0,
                                                     float wy0) {
     const float X0 = wx0 + 0.5f - A.x, X1 = X0 + 7.0f;
-    const float Y0 = wy0 + 0.5f - A.y, Y1 = Y0 + 3.0f;
+    const float Y0 = wy0 + 0.5f - A.y, Y1 = Y0 + 7.0f;
     float r2 = X.w;
     {
         const float zmax = (fmaxf(B.z * X0, B.z * X1) + fmaxf(B.w * Y0, B.w * Y1)) * SSG_SQRT1_2;
@@ -149,11 +150,11 @@ __device__ __forceinline__ bool ellipse_meets_block(const float4 A, const float4
 }
 
 // Word of the per-(tile, warp, 32-instance chunk) blend mask: bit b of word
-// (start/32 + tile + chunk) * 8 + warp is set when some pixel of the warp
-// blended instance start + 32*chunk + b in the forward.  The bases never
-// overlap: consecutive tiles' bases differ by >= ceil(len/32).
+// (start/32 + tile + chunk) * 4 + warp is set when some pixel of the warp's
+// 8x8 block blended instance start + 32*chunk + b in the forward.  The bases
+// never overlap: consecutive tiles' bases differ by >= ceil(len/32).
 __device__ __forceinline__ size_t mask_word(int start, int tile, int chunk, int warp) {
-    return ((size_t)(start >> 5) + (size_t)tile + (size_t)chunk) * 8 + (size_t)warp;
+    return ((size_t)(start >> 5) + (size_t)tile + (size_t)chunk) * kWarps + (size_t)warp;
 }
 
 // fp32 pre-clamp alpha of one pixel-instance pair: the same operation
@@ -182,6 +183,96 @@ __device__ __forceinline__ void pair_alpha(const float4 &B, const float4 &C, Pai
     q.A = kVanilla ? q.o * q.G : (q.o * q.G) * q.E;         // :139
 }
 
+// ---- two pixels per thread (rows y and y + 4 of one column) ------------
+// The blend kernels give each thread the pixel pair (x, y), (x, y + 4): the
+// dx terms are shared, the per-row terms run as packed fp32x2 operations
+// (FFMA2 / FMUL2 / FADD2, one issue slot for two lanes' worth of FP32 work:
+// profiles/r2_ffma2.txt), and every per-instance cost -- shared-memory
+// loads, the culling ballot, loop control, the backward's 12-value warp
+// reduction -- is paid once per 64 pixels instead of 32.  Every packed op
+// is the same IEEE operation per component as the scalar sequence above.
+__device__ __forceinline__ uint64_t pk(float2 a) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+    return r;
+}
+__device__ __forceinline__ float2 upk(uint64_t r) {
+    float2 a;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)), "l"(pk(c)));
+    return upk(r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
+    return upk(r);
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
+    return upk(r);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
+    return upk(r);
+}
+__device__ __forceinline__ float2 sel2(bool px, bool py, float2 a, float2 b) {
+    return make_float2(px ? a.x : b.x, py ? a.y : b.y);
+}
+
+// erfc_pos / skew_E (ssg_common.cuh) on a pair: the same operations per
+// component, the polynomial packed
+__device__ __forceinline__ float2 skew_E2(float2 z) {
+    const float2 x = make_float2(fabsf(z.x), fabsf(z.y));
+    const float2 u = fma2(f2(0.5f), x, f2(1.0f));
+    const float2 t = make_float2(fast_rcp(u.x), fast_rcp(u.y));
+    float2 p = fma2(t, f2(0.17087277f), f2(-0.82215223f));
+    p = fma2(t, p, f2(1.48851587f));
+    p = fma2(t, p, f2(-1.13520398f));
+    p = fma2(t, p, f2(0.27886807f));
+    p = fma2(t, p, f2(-0.18628806f));
+    p = fma2(t, p, f2(0.09678418f));
+    p = fma2(t, p, f2(0.37409196f));
+    p = fma2(t, p, f2(1.00002368f));
+    p = fma2(t, p, f2(-1.26551223f));
+    const float2 a = mul2(fma2(make_float2(-x.x, -x.y), x, p), f2(SSG_LOG2E));
+    const float2 y = mul2(t, make_float2(fast_exp2(a.x), fast_exp2(a.y)));
+    const float2 ny = sub2(f2(2.0f), y);
+    return make_float2(z.x > 0.0f ? ny.x : y.x, z.y > 0.0f ? ny.y : y.y);
+}
+
+struct Pair2 {
+    float dx;
+    float2 dy, power, E, z, o, G, A;
+};
+__device__ __forceinline__ void pair_power2(float fx, float2 fy, const float4 &A, const float4 &B, Pair2 &q) {
+    q.dx = fx - A.x;
+    q.dy = sub2(fy, f2(A.y));
+    const float adx2 = A.z * q.dx * q.dx;
+    const float2 t = fma2(mul2(f2(B.x), q.dy), q.dy, f2(adx2));
+    q.power = fma2(f2(-0.5f), t, mul2(f2(-(A.w * q.dx)), q.dy));                        // :133
+}
+template <bool kVanilla>
+__device__ __forceinline__ void pair_alpha2(const float4 &B, const float4 &C, Pair2 &q) {
+    q.E = f2(1.0f);
+    q.z = f2(0.0f);
+    q.o = f2(C.x);
+    if (!kVanilla && (B.z != 0.0f || B.w != 0.0f)) {     // warp-uniform
+        q.z = mul2(fma2(f2(B.z), f2(q.dx), mul2(f2(B.w), q.dy)), f2(SSG_SQRT1_2));        // :136
+        q.E = skew_E2(q.z);                                                                 // :137
+        q.o = fma2(f2(C.y), sub2(q.E, f2(1.0f)), f2(C.x));                                 // :138
+    }
+    const float2 pl = mul2(make_float2(fminf(q.power.x, 0.0f), fminf(q.power.y, 0.0f)), f2(SSG_LOG2E));
+    q.G = make_float2(fast_exp2(pl.x), fast_exp2(pl.y));
+    q.A = kVanilla ? mul2(q.o, q.G) : mul2(mul2(q.o, q.G), q.E);                           // :139
+}
+
 // -------------------------------------------------------------- forward
 // kVanilla = true compiles the plain 3DGS blend (no skew term, alpha =
 // o * G): the config-3 regression reference for skew-free splats, which
@@ -190,10 +281,10 @@ __device__ __forceinline__ void pair_alpha(const float4 &B, const float4 &C, Pai
 // chunk, which instances any of the warp's pixels blended; the backward
 // then visits exactly those (same arithmetic, same decisions).
 #ifndef SSG_FWD_MINB
-#define SSG_FWD_MINB 5
+#define SSG_FWD_MINB 8
 #endif
 #ifndef SSG_BWD_MINB
-#define SSG_BWD_MINB 5
+#define SSG_BWD_MINB 8
 #endif
 
 template <bool kVanilla>
@@ -208,40 +299,41 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
     const int tile = blockIdx.x;
     const int tyi = tile / ntx, txi = tile - tyi * ntx;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * 4;
-    const int lx = wx0 + (lane & 7), ly = wy0 + (lane >> 3);
+    const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * 8;     // the warp's 8x8 block
+    const int lx = wx0 + (lane & 7), ly = wy0 + (lane >> 3);   // pixels (lx, ly), (lx, ly + 4)
     const int px = txi * 16 + lx, py = tyi * 16 + ly;
-    const bool inside = px < W && py < H;
+    const bool in0 = px < W && py < H, in1 = px < W && py + 4 < H;
     const int start = ranges[2 * tile], end = ranges[2 * tile + 1];
-    const float fx = (float)lx + 0.5f, fy = (float)ly + 0.5f;
+    const float fx = (float)lx + 0.5f;
+    const float2 fy = make_float2((float)ly + 0.5f, (float)ly + 4.5f);
     const float fwx0 = (float)wx0, fwy0 = (float)wy0;
     const double ox = (double)(txi * 16), oy = (double)(tyi * 16);
 
-    float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
-    float dT = 0.0f;      // bound on |T - T_reference|
-    int nc = 0, li = -1;
+    float2 T = f2(1.0f), dT = f2(0.0f);          // dT: bound on |T - T_reference|
+    float2 C0 = f2(0.0f), C1 = f2(0.0f), C2 = f2(0.0f);
+    int nc0 = 0, nc1 = 0, li0 = -1, li1 = -1;
     // bit 0: stopped / outside, bit 1: met a decision its bounds cannot certify
     // (all_exact: every pixel takes the exact path -- a test mode)
-    int done = !inside ? 1 : (all_exact ? 2 : 0);
+    int done0 = !in0 ? 1 : (all_exact ? 2 : 0), done1 = !in1 ? 1 : (all_exact ? 2 : 0);
     const uint32_t aA = smem_addr(s.A), aB = smem_addr(s.B), aC = smem_addr(s.C);
     const uint32_t aX = smem_addr(s.X), aD = smem_addr(s.D);
     int kdone = start;    // instances [start, kdone) walked by this warp (mask words written)
 
     for (int base = start; base < end; base += kBatch) {
-        if (__syncthreads_count(done) == kThreads) break;
-        if (base + (int)threadIdx.x < end)
-            stage_splat(splat, inst_prim[base + threadIdx.x], ox, oy, s, threadIdx.x);
+        if (__syncthreads_count(done0 && done1) == kThreads) break;
+        for (int t = threadIdx.x; t < kBatch && base + t < end; t += kThreads)
+            stage_splat(splat, inst_prim[base + t], ox, oy, s, t);
         __syncthreads();
         const int cnt = min(kBatch, end - base);
         for (int c0 = 0; c0 < cnt; c0 += 32) {
-            if (__all_sync(0xffffffffu, done)) break;
+            if (__all_sync(0xffffffffu, done0 && done1)) break;
             kdone = base + c0 + 32;
             const int i = c0 + lane;
             bool hit = false;
             if (i < cnt)
                 hit = ellipse_meets_block(lds128(aA + 16 * i), lds128(aB + 16 * i), lds128(aX + 16 * i), fwx0, fwy0);
             unsigned mask = __ballot_sync(0xffffffffu, hit);
-            uint32_t lbits = 0;  // instances of this chunk the lane's pixel blended
+            uint32_t lb0 = 0, lb1 = 0;  // instances of this chunk each pixel blended
             while (mask) {
                 const uint32_t lowb = mask & (0u - mask);
                 const int bit = __ffs(mask) - 1;
@@ -252,48 +344,63 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
                 // reference's operations, the others carry zero weight
                 const float4 A = lds128(aA + 16 * j);
                 const float4 B = lds128(aB + 16 * j);
-                Pair q;
-                pair_power(fx, fy, A, B, q);
-                const bool live = !done && q.power >= B.y && q.power <= 0.0f;
-                if (!__any_sync(0xffffffffu, live)) continue;
+                Pair2 q;
+                pair_power2(fx, fy, A, B, q);
+                const bool live0 = !done0 & (q.power.x >= B.y) & (q.power.x <= 0.0f);
+                const bool live1 = !done1 & (q.power.y >= B.y) & (q.power.y <= 0.0f);
+                if (!__any_sync(0xffffffffu, live0 | live1)) continue;
                 const float4 C = lds128(aC + 16 * j);
                 const float4 D = lds128(aD + 16 * j);
-                pair_alpha<kVanilla>(B, C, q);
-                const float alpha = fminf(q.A, SSG_ALPHA_MAX);                              // :140
-                const float dA = q.A - SSG_ALPHA_SKIP;
-                const bool pass = live && dA >= D.y;           // certainly >= 1/255 (:141-142)
-                const float gp = fmaf(D.w, -q.power, D.z);     // this pair's relative alpha error bound
+                pair_alpha2<kVanilla>(B, C, q);
+                const float2 alpha = make_float2(fminf(q.A.x, SSG_ALPHA_MAX), fminf(q.A.y, SSG_ALPHA_MAX));   // :140
+                const float2 dA = sub2(q.A, f2(SSG_ALPHA_SKIP));
+                const bool pass0 = live0 & (dA.x >= D.y), pass1 = live1 & (dA.y >= D.y);   // certainly >= 1/255
+                const float2 gp = fma2(f2(D.w), make_float2(-q.power.x, -q.power.y), f2(D.z));  // alpha error bounds
+                const float2 dc = sub2(q.A, f2(SSG_ALPHA_MAX)), cb = mul2(f2(SSG_ALPHA_MAX), gp);
                 // uncertain: the 1/255 skip, or the backward's clamp cut (A <= 0.99, :290)
-                bool bad = live & ((fabsf(dA) < D.y) | (fabsf(q.A - SSG_ALPHA_MAX) <= SSG_ALPHA_MAX * gp));
-                const float test_T = T * (1.0f - alpha);                                      // :143
-                const bool near = pass && test_T < kNearT + dT;
-                bool stop = false;
-                if (__any_sync(0xffffffffu, near)) {
+                bool bad0 = live0 & ((fabsf(dA.x) < D.y) | (fabsf(dc.x) <= cb.x));
+                bool bad1 = live1 & ((fabsf(dA.y) < D.y) | (fabsf(dc.y) <= cb.y));
+                const float2 oma = sub2(f2(1.0f), alpha);
+                const float2 test_T = mul2(T, oma);                                                // :143
+                const float2 nthr = add2(f2(kNearT), dT);
+                const bool near0 = pass0 & (test_T.x < nthr.x), near1 = pass1 & (test_T.y < nthr.y);
+                bool stop0 = false, stop1 = false;
+                if (__any_sync(0xffffffffu, near0 | near1)) {
                     // |T (1 - alpha) - T_ref (1 - alpha_ref)| <= dT (1 - alpha) + T alpha gp
                     //   + 2 roundings per blend so far (eps / 2 each, relative)
-                    const float err = fmaf(dT, 1.0f - alpha, T * alpha * gp) +
-                                      (float)(nc + __popc(lbits) + 2) * 6e-8f * test_T;
-                    bad |= near & (fabsf(test_T - SSG_T_STOP) <= err);
-                    stop = near & (test_T < SSG_T_STOP);                                      // :144-147
+                    const float e0 = fmaf(dT.x, oma.x, T.x * alpha.x * gp.x) +
+                                     (float)(nc0 + __popc(lb0) + 2) * 6e-8f * test_T.x;
+                    const float e1 = fmaf(dT.y, oma.y, T.y * alpha.y * gp.y) +
+                                     (float)(nc1 + __popc(lb1) + 2) * 6e-8f * test_T.y;
+                    bad0 |= near0 & (fabsf(test_T.x - SSG_T_STOP) <= e0);
+                    bad1 |= near1 & (fabsf(test_T.y - SSG_T_STOP) <= e1);
+                    stop0 = near0 & (test_T.x < SSG_T_STOP);                                    // :144-147
+                    stop1 = near1 & (test_T.y < SSG_T_STOP);
                 }
-                const bool blend = pass & !stop & !bad;                                       // :148-154
-                done |= (int)stop | ((int)bad << 1);      // bit 1: exact path
-                const float w = blend ? alpha * T : 0.0f;
-                C0 = fmaf(w, C.z, C0);
-                C1 = fmaf(w, C.w, C1);
-                C2 = fmaf(w, D.x, C2);
-                const float omb = blend ? 1.0f - alpha : 1.0f;
-                dT = fmaf(w, gp, dT * omb);
-                T = blend ? test_T : T;
-                lbits |= blend ? lowb : 0u;
+                const bool bl0 = pass0 & !stop0 & !bad0, bl1 = pass1 & !stop1 & !bad1;       // :148-154
+                done0 |= (int)stop0 | ((int)bad0 << 1);
+                done1 |= (int)stop1 | ((int)bad1 << 1);
+                const float2 w = sel2(bl0, bl1, mul2(alpha, T), f2(0.0f));
+                C0 = fma2(w, f2(C.z), C0);
+                C1 = fma2(w, f2(C.w), C1);
+                C2 = fma2(w, f2(D.x), C2);
+                const float2 omb = sel2(bl0, bl1, oma, f2(1.0f));
+                dT = fma2(w, gp, mul2(dT, omb));
+                T = sel2(bl0, bl1, test_T, T);
+                lb0 |= bl0 ? lowb : 0u;
+                lb1 |= bl1 ? lowb : 0u;
             }
             // n_contrib and last_idx from the chunk's blend bits (ascending k)
-            if (lbits) {
-                nc += __popc(lbits);
-                li = base + c0 + 31 - __clz(lbits);
+            if (lb0) {
+                nc0 += __popc(lb0);
+                li0 = base + c0 + 31 - __clz(lb0);
+            }
+            if (lb1) {
+                nc1 += __popc(lb1);
+                li1 = base + c0 + 31 - __clz(lb1);
             }
             if (blend_mask) {
-                const uint32_t bmask = __reduce_or_sync(0xffffffffu, lbits);
+                const uint32_t bmask = __reduce_or_sync(0xffffffffu, lb0 | lb1);
                 if (lane == 0) blend_mask[mask_word(start, tile, (base - start + c0) >> 5, warp)] = bmask;
             }
         }
@@ -303,23 +410,43 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
     if (blend_mask)
         for (int c = (kdone - start) / 32 + lane; c < (end - start + 31) / 32; c += 32)
             blend_mask[mask_word(start, tile, c, warp)] = 0u;
-    const bool unsure = (done & 2) && inside;
-    const uint32_t redo = __ballot_sync(0xffffffffu, unsure);
-    if (lane == 0) redo_mask[(size_t)tile * kWarps + warp] = redo;
-    if (inside) {  // :158-166
+    // the redo mask is kept per 8x4 block: rows ly (block 4 (warp >> 1) +
+    // (warp & 1)) and ly + 4 (two blocks further)
+    const bool un0 = (done0 & 2) && in0, un1 = (done1 & 2) && in1;
+    const uint32_t r0 = __ballot_sync(0xffffffffu, un0), r1 = __ballot_sync(0xffffffffu, un1);
+    if (lane == 0) {
+        const int b0 = (warp >> 1) * 4 + (warp & 1);
+        redo_mask[(size_t)tile * kBlocks + b0] = r0;
+        redo_mask[(size_t)tile * kBlocks + b0 + 2] = r1;
+    }
+    // :158-166; pixels on the exact path: every blend so far is <= li and set
+    // in the warp's mask words, the exact path resumes the scan at li + 1
+    if (in0) {
         const int64_t pix = (int64_t)py * W + px;
-        if (unsure) {
-            // exact path: every blend of this pixel so far is <= li and set in
-            // the warp's mask words; it resumes the scan at li + 1
+        if (un0) {
             redo_list[atomicAdd(redo_count, 1u)] = (uint32_t)pix;
-            last_idx[pix] = li;
+            last_idx[pix] = li0;
         } else {
-            color[3 * pix] = C0 + T * bg0;
-            color[3 * pix + 1] = C1 + T * bg1;
-            color[3 * pix + 2] = C2 + T * bg2;
-            final_T[pix] = T;
-            n_contrib[pix] = nc;
-            last_idx[pix] = li;
+            color[3 * pix] = C0.x + T.x * bg0;
+            color[3 * pix + 1] = C1.x + T.x * bg1;
+            color[3 * pix + 2] = C2.x + T.x * bg2;
+            final_T[pix] = T.x;
+            n_contrib[pix] = nc0;
+            last_idx[pix] = li0;
+        }
+    }
+    if (in1) {
+        const int64_t pix = (int64_t)(py + 4) * W + px;
+        if (un1) {
+            redo_list[atomicAdd(redo_count, 1u)] = (uint32_t)pix;
+            last_idx[pix] = li1;
+        } else {
+            color[3 * pix] = C0.y + T.y * bg0;
+            color[3 * pix + 1] = C1.y + T.y * bg1;
+            color[3 * pix + 2] = C2.y + T.y * bg2;
+            final_T[pix] = T.y;
+            n_contrib[pix] = nc1;
+            last_idx[pix] = li1;
         }
     }
 }
@@ -341,7 +468,7 @@ __device__ __forceinline__ RedoPixel redo_pixel(uint32_t pix, int32_t W, int32_t
     r.start = ranges[2 * r.tile];
     r.end = ranges[2 * r.tile + 1];
     const int lx = r.px & 15, ly = r.py & 15;
-    r.warp_in_tile = (ly >> 2) * 2 + (lx >> 3);
+    r.warp_in_tile = (ly >> 3) * 2 + (lx >> 3);
     r.fx = (float)lx + 0.5f;
     r.fy = (float)ly + 0.5f;
     r.ox = (double)(r.tx * 16);
@@ -609,7 +736,7 @@ __device__ __forceinline__ float *dest_row(float *out, int k, uint32_t p, int tx
 }
 
 template <int kMode>
-__global__ void __launch_bounds__(kThreads, kMode == 0 ? SSG_BWD_MINB : 1)
+__global__ void __launch_bounds__(kThreads, kMode == 0 ? SSG_BWD_MINB : 2)
 k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float bg2,
                  const ssg_splat *__restrict__ splat, const uint32_t *__restrict__ inst_prim,
                  const int32_t *__restrict__ ranges, const float *__restrict__ final_T,
@@ -623,30 +750,43 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
     const int tile = blockIdx.x;
     const int tyi = tile / ntx, txi = tile - tyi * ntx;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * 4;
+    const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * 8;
     const int lx = wx0 + (lane & 7), ly = wy0 + (lane >> 3);
     const int px = txi * 16 + lx, py = tyi * 16 + ly;
-    const bool inside = px < W && py < H;
+    const bool in0 = px < W && py < H, in1 = px < W && py + 4 < H;
     const int start = ranges[2 * tile], end = ranges[2 * tile + 1];
     if (end <= start) return;
-    const float fx = (float)lx + 0.5f, fy = (float)ly + 0.5f;
+    const float fx = (float)lx + 0.5f;
+    const float2 fy = make_float2((float)ly + 0.5f, (float)ly + 4.5f);
     const float fwx0 = (float)wx0, fwy0 = (float)wy0;
     const double ox = (double)(txi * 16), oy = (double)(tyi * 16);
 
     // _core.pyx:232-246; pixels on the exact path are done by the redo kernel
-    float T = 1.0f, d0 = 0.0f, d1 = 0.0f, d2 = 0.0f;
-    int li = -1;
-    const bool redo = (redo_mask[(size_t)tile * kWarps + warp] >> lane) & 1u;
-    if (inside && !redo) {
-        const int64_t pix = (int64_t)py * W + px;
-        T = final_T[pix];
-        li = last_idx[pix];
-        d0 = dL[3 * pix];
-        d1 = dL[3 * pix + 1];
-        d2 = dL[3 * pix + 2];
+    float2 T = f2(1.0f), d0 = f2(0.0f), d1 = f2(0.0f), d2 = f2(0.0f);
+    int li0 = -1, li1 = -1;
+    {
+        const int b0 = (warp >> 1) * 4 + (warp & 1);
+        const bool redo0 = (redo_mask[(size_t)tile * kBlocks + b0] >> lane) & 1u;
+        const bool redo1 = (redo_mask[(size_t)tile * kBlocks + b0 + 2] >> lane) & 1u;
+        if (in0 && !redo0) {
+            const int64_t pix = (int64_t)py * W + px;
+            T.x = final_T[pix];
+            li0 = last_idx[pix];
+            d0.x = dL[3 * pix];
+            d1.x = dL[3 * pix + 1];
+            d2.x = dL[3 * pix + 2];
+        }
+        if (in1 && !redo1) {
+            const int64_t pix = (int64_t)(py + 4) * W + px;
+            T.y = final_T[pix];
+            li1 = last_idx[pix];
+            d0.y = dL[3 * pix];
+            d1.y = dL[3 * pix + 1];
+            d2.y = dL[3 * pix + 2];
+        }
     }
-    float R0 = bg0, R1 = bg1, R2 = bg2;
-    const int wmax = __reduce_max_sync(0xffffffffu, li);
+    float2 R0 = f2(bg0), R1 = f2(bg1), R2 = f2(bg2);
+    const int wmax = __reduce_max_sync(0xffffffffu, max(li0, li1));
     if (lane == 0) sMax[warp] = wmax;
     __syncthreads();
     int maxli = sMax[0];
@@ -670,10 +810,10 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
         if (blend_mask && lane < 8 && 32 * lane < cnt)
             words = blend_mask[mask_word(start, tile, b * (kBatch / 32) + lane, warp)];
         __syncthreads();  // previous batch fully consumed
-        if ((int)threadIdx.x < cnt) {
-            const uint32_t p = inst_prim[lo + threadIdx.x];
-            stage_splat(splat, p, ox, oy, s, threadIdx.x);
-            sRow[threadIdx.x] = dest_row<kMode>(out, lo + threadIdx.x, p, txi, tyi, prim_row, tile_rect);
+        for (int t = threadIdx.x; t < cnt; t += kThreads) {
+            const uint32_t p = inst_prim[lo + t];
+            stage_splat(splat, p, ox, oy, s, t);
+            sRow[t] = dest_row<kMode>(out, lo + t, p, txi, tyi, prim_row, tile_rect);
         }
         if (kMode != 0) {  // this warp's partial sums of the batch start at zero
             for (int i = lane; i < cnt * 3; i += 32)
@@ -699,52 +839,75 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                 const int bit = 31 - __clz(mask);
                 mask &= ~(1u << bit);
                 const int j = c0 + bit;
-                // Branch-free per lane: lanes that do not contribute compute
-                // with a zero weight and keep T, R; contributing lanes run
+                const int k = lo + j;
+                // Branch-free per lane: pixels that do not contribute compute
+                // with a zero weight and keep T, R; contributing ones run
                 // exactly the reference's operations (every decision here
                 // was certified by the forward for non-redo pixels).
                 const float4 A = lds128(aA + 16 * j);
                 const float4 B = lds128(aB + 16 * j);
-                Pair q;
-                pair_power(fx, fy, A, B, q);
-                const bool live = lo + j <= li && q.power >= B.y && q.power <= 0.0f;   // :263-264, :265-269
-                if (!blend_mask && !__any_sync(0xffffffffu, live)) continue;
+                Pair2 q;
+                pair_power2(fx, fy, A, B, q);
+                const bool live0 = (k <= li0) & (q.power.x >= B.y) & (q.power.x <= 0.0f);   // :263-264, :265-269
+                const bool live1 = (k <= li1) & (q.power.y >= B.y) & (q.power.y <= 0.0f);
+                if (!blend_mask && !__any_sync(0xffffffffu, live0 | live1)) continue;
                 const float4 C = lds128(aC + 16 * j);
                 const float4 D = lds128(aD + 16 * j);
-                pair_alpha<false>(B, C, q);
-                const float alpha = fminf(q.A, SSG_ALPHA_MAX);
-                const bool contrib = live && q.A >= SSG_ALPHA_SKIP;                           // :276-277
-                if (!blend_mask && !__any_sync(0xffffffffu, contrib)) continue;
-                const float Tn = T * fast_rcp(1.0f - alpha);                                   // :280
-                T = contrib ? Tn : T;
-                const float e0 = C.z - R0, e1 = C.w - R1, e2 = D.x - R2;
-                const float d_alpha = T * (e0 * d0 + e1 * d1 + e2 * d2);
-                const float aT = contrib ? alpha * T : 0.0f;
+                pair_alpha2<false>(B, C, q);
+                const float2 alpha = make_float2(fminf(q.A.x, SSG_ALPHA_MAX), fminf(q.A.y, SSG_ALPHA_MAX));
+                const bool ct0 = live0 & (q.A.x >= SSG_ALPHA_SKIP), ct1 = live1 & (q.A.y >= SSG_ALPHA_SKIP);  // :276
+                if (!blend_mask && !__any_sync(0xffffffffu, ct0 | ct1)) continue;
+                const float2 oma = sub2(f2(1.0f), alpha);
+                const float2 Tn = mul2(T, make_float2(fast_rcp(oma.x), fast_rcp(oma.y)));    // :280
+                T = sel2(ct0, ct1, Tn, T);
+                const float2 e0 = sub2(f2(C.z), R0), e1 = sub2(f2(C.w), R1), e2 = sub2(f2(D.x), R2);
+                const float2 d_alpha = mul2(T, fma2(e2, d2, fma2(e1, d1, mul2(e0, d0))));
+                const float2 aT = sel2(ct0, ct1, mul2(alpha, T), f2(0.0f));
+                // DA = 0 past the clamp (:290)
+                const float2 DA = sel2(ct0 & (q.A.x <= SSG_ALPHA_MAX), ct1 & (q.A.y <= SSG_ALPHA_MAX), d_alpha,
+                                       f2(0.0f));
+                const float2 d_power = mul2(DA, q.A);
+                // d_z (:293) exists for skew-free splats too (z = 0, E = 1: e^-z^2 G = G)
+                const bool skewed = (B.z != 0.0f || B.w != 0.0f);                            // warp-uniform
+                float2 Gez2 = q.G;
+                if (skewed) {
+                    const float2 pw = make_float2(fminf(q.power.x, 0.0f), fminf(q.power.y, 0.0f));
+                    const float2 a2 = mul2(fma2(make_float2(-q.z.x, -q.z.y), q.z, pw), f2(SSG_LOG2E));
+                    Gez2 = make_float2(fast_exp2(a2.x), fast_exp2(a2.y));
+                }
+                const float2 dzs = mul2(mul2(mul2(DA, f2(kDzScale)), Gez2), fma2(f2(C.y), q.E, q.o));
+                const float2 px_ = mul2(d_power, f2(q.dx)), py_ = mul2(d_power, q.dy);
+                // per-pixel terms, then the pair's sum per component
                 float g[12];
-                g[9] = aT * d0;
-                g[10] = aT * d1;
-                g[11] = aT * d2;
-                const float DA = contrib && q.A <= SSG_ALPHA_MAX ? d_alpha : 0.0f;             // :290
-                const float d_power = DA * q.A;
-                const bool skewed = (B.z != 0.0f || B.w != 0.0f);                              // warp-uniform
-                const float pw = fminf(q.power, 0.0f);
-                const float Gez2 = skewed ? fast_exp2((pw - q.z * q.z) * SSG_LOG2E) : q.G;
-                const float dzs = (DA * kDzScale) * Gez2 * fmaf(C.y, q.E, q.o);
-                const float px_ = d_power * q.dx, py_ = d_power * q.dy;
-                g[0] = fmaf(A.z, px_, fmaf(A.w, py_, -dzs * B.z));                           // -d_dx
-                g[1] = fmaf(B.x, py_, fmaf(A.w, px_, -dzs * B.w));                           // -d_dy
-                g[2] = -0.5f * px_ * q.dx;
-                g[3] = -px_ * q.dy;
-                g[4] = -0.5f * py_ * q.dy;
-                g[5] = dzs * q.dx;
-                g[6] = dzs * q.dy;
-                const float hGE = 0.5f * DA * q.G * q.E;
-                g[7] = hGE * q.E;
-                g[8] = hGE * (2.0f - q.E);
-                const float ae = contrib ? alpha : 0.0f;                                       // :306-308
-                R0 = fmaf(ae, e0, R0);
-                R1 = fmaf(ae, e1, R1);
-                R2 = fmaf(ae, e2, R2);
+                {
+                    const float2 g0 = fma2(f2(A.z), px_, fma2(f2(A.w), py_, mul2(dzs, f2(-B.z))));   // -d_dx
+                    const float2 g1 = fma2(f2(B.x), py_, fma2(f2(A.w), px_, mul2(dzs, f2(-B.w))));   // -d_dy
+                    const float2 g2 = mul2(mul2(f2(-0.5f), px_), f2(q.dx));
+                    const float2 g3 = mul2(make_float2(-px_.x, -px_.y), q.dy);
+                    const float2 g4 = mul2(mul2(f2(-0.5f), py_), q.dy);
+                    const float2 g5 = mul2(dzs, f2(q.dx));
+                    const float2 g6 = mul2(dzs, q.dy);
+                    const float2 hGE = mul2(mul2(mul2(f2(0.5f), DA), q.G), q.E);
+                    const float2 g7 = mul2(hGE, q.E);
+                    const float2 g8 = mul2(hGE, sub2(f2(2.0f), q.E));
+                    const float2 g9 = mul2(aT, d0), g10 = mul2(aT, d1), g11 = mul2(aT, d2);
+                    g[0] = g0.x + g0.y;
+                    g[1] = g1.x + g1.y;
+                    g[2] = g2.x + g2.y;
+                    g[3] = g3.x + g3.y;
+                    g[4] = g4.x + g4.y;
+                    g[5] = g5.x + g5.y;
+                    g[6] = g6.x + g6.y;
+                    g[7] = g7.x + g7.y;
+                    g[8] = g8.x + g8.y;
+                    g[9] = g9.x + g9.y;
+                    g[10] = g10.x + g10.y;
+                    g[11] = g11.x + g11.y;
+                }
+                const float2 ae = sel2(ct0, ct1, alpha, f2(0.0f));                               // :306-308
+                R0 = fma2(ae, e0, R0);
+                R1 = fma2(ae, e1, R1);
+                R2 = fma2(ae, e2, R2);
                 const float v = warp_reduce_transposed12(g, lane);
                 if (holder) {
                     if (kMode == 0) atomicAdd(sRow[j] + my_comp, v);
@@ -753,10 +916,9 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
             }
         }
         if (kMode != 0) {
-            // fixed-order combination of the eight warps' sums, one row per thread
+            // fixed-order combination of the warps' sums, one row per thread
             __syncthreads();
-            if ((int)threadIdx.x < cnt) {
-                const int j = threadIdx.x;
+            for (int j = threadIdx.x; j < cnt; j += kThreads) {
                 float4 acc[3];
 #pragma unroll
                 for (int c = 0; c < 3; c++) acc[c] = reinterpret_cast<const float4 *>(s_part + j * 12)[c];
@@ -960,10 +1122,10 @@ k_blend_backward_redo_tiles(int32_t ntx, int32_t n_tiles, int32_t W, float bg0, 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int tile = blockIdx.x * kRedoWarps + wid;
     if (tile >= n_tiles) return;
-    const uint32_t word = lane < kWarps ? redo_mask[(size_t)tile * kWarps + lane] : 0u;
+    const uint32_t word = lane < kBlocks ? redo_mask[(size_t)tile * kBlocks + lane] : 0u;
     if (!__any_sync(0xffffffffu, word != 0u)) return;
     const int ty = tile / ntx, tx = tile - ty * ntx;
-    for (int w = 0; w < kWarps; w++) {
+    for (int w = 0; w < kBlocks; w++) {
         uint32_t bits = __shfl_sync(0xffffffffu, word, w);
         while (bits) {
             const int l = __ffs(bits) - 1;
@@ -1022,7 +1184,7 @@ __global__ void k_reduce_prim_rows(int64_t n, const uint64_t *__restrict__ prim_
 __global__ void k_erf_probe(const double *x, int64_t n, float *e32, double *e64) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    if (e32) e32[i] = skew_E((float)x[i]);
+    if (e32) e32[i] = skew_E2(f2((float)x[i])).x;   // the blend kernels' packed evaluation
     if (e64) e64[i] = ref_erf(x[i]);
 }
 
@@ -1095,8 +1257,8 @@ static bool frame_ok(const ssg_frame_buffers *f) {
 }  // namespace ssg
 
 extern "C" int64_t ssg_blend_mask_words(int64_t m, int32_t n_tiles) {
-    // mask_word(): bases start/32 + tile + chunk, 8 warps each
-    return m < 0 || n_tiles < 0 ? -1 : 8 * (m / 32 + (int64_t)n_tiles + 1);
+    // mask_word(): bases start/32 + tile + chunk, kWarps (4) warps each
+    return m < 0 || n_tiles < 0 ? -1 : (int64_t)ssg::kWarps * (m / 32 + (int64_t)n_tiles + 1);
 }
 
 extern "C" int ssg_blend_forward(int64_t m, int32_t width, int32_t height, const float background[3],
