@@ -40,12 +40,13 @@ METRIC = "fwd+bwd raster ms/frame, 1M skew Gaussians @1080p; views/s at 1/2/4/8 
 # libssg_b200 kernel launches per fwd+bwd frame (all hand-written, no library
 # kernels): preprocess_fwd 1; depth sort + count scan 1 (cooperative);
 # two-level counting scatter 8 (rows: count, rowscan, rowstart, scatter;
-# tiles: count, tilescan, tilestart, scatter); blend_fwd 1; blend_bwd 1;
-# preprocess_bwd 1 (geometry + SH chain fused).
-LAUNCHES_PER_FRAME = 13
+# tiles: count, tilescan, tilestart, scatter); blend_fwd 2 (fp32 kernel +
+# exact path over its flagged pixels); blend_bwd 2 (same); preprocess_bwd 1.
+LAUNCHES_PER_FRAME = 15
 LAUNCHES_NOTE = ("per frame: k_preprocess_forward 1, k_depth_sort 1, k_cs1_{count,rowscan,rowstart,scatter} 4, "
-                 "k_cs2_{count,tilescan,tilestart,scatter} 4, k_blend_forward 1, k_blend_backward 1, "
-                 "k_preprocess_backward 1; no library kernels (cudaMemsetAsync excluded)")
+                 "k_cs2_{count,tilescan,tilestart,scatter} 4, k_blend_forward 1 + k_blend_forward_redo 1, "
+                 "k_blend_backward 1 + k_blend_backward_redo_list 1, k_preprocess_backward 1; no library "
+                 "kernels (cudaMemsetAsync excluded)")
 UNIT = "views/s"
 N_PRIM, WIDTH, HEIGHT = 1_000_000, 1920, 1080
 # per-pair algorithmic instruction counts (fixed, not tuned)
@@ -200,6 +201,98 @@ def tile_pairs(frame, ranges, width, height):
     return int((npix * cnt).sum().item())
 
 
+def view_batch(eng, rank, world, local, barrier, max_over_ranks, reps=3):
+    """BASELINE.json config 4 on the same ranks: the 64-view orbit batch of
+    the 3M G4 scene (1297x840, forward), views sharded over the ranks in
+    contiguous blocks (no collective); views/s = 64 / max-over-ranks batch
+    time (CUDA events).  The scaling configuration of the north star."""
+    import torch
+    from paper_2605_18334_b200.engine import DeviceScene
+    from paper_2605_18334_b200.synthetic import ball_scene, orbit_views
+    from paper_2605_18334_b200.views import render_views, shard_views
+    scene = ball_scene(3_000_000, seed=0)
+    views = orbit_views(64, radius=4.0, elevation=1.2, width=1297, height=840, fov_x=0.9)
+    mine = [views[i] for i in shard_views(64, rank, world)]
+    ds = DeviceScene.from_host(scene)
+    out = torch.empty((max(len(mine), 1), 840, 1297, 3), dtype=torch.float32, device="cuda")
+    render_views(ds, mine, engine=[eng], out=out)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        render_views(ds, mine, engine=[eng], out=out)
+    e1.record()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / reps)
+    return {"metric": "config 4: 64-view forward batch, 3M skew Gaussians @1297x840", "value": 64000.0 / ms,
+            "unit": "views/s", "ms_per_batch": ms, "n_gpus": world, "scaling": "strong",
+            "views_per_rank": len(mine), "reps": reps,
+            "parallelism": f"views sharded x{world} (contiguous blocks, no collective)"}
+
+
+def spawn(args) -> int:
+    """`--gpus N` without a torchrun environment: launch N ranks (one per
+    GPU) through torch.distributed.run on 127.0.0.1 and pass the exit code
+    through; NCCL_DEBUG=INFO prints the communicator setup on stderr."""
+    import socket
+
+    import torch
+    n_dev = torch.cuda.device_count()
+    if n_dev < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} needs {args.gpus} GPUs; {n_dev} visible"}))
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def reference_arm(args, config):
+    """--impl reference: the reference's own CPU path (oracle/_ref, Cython +
+    OpenMP on every host core; the C oracle port when absent) on the full
+    config-2 frame, timed once end to end (about a minute on 16 cores),
+    after `warmup` runs of the bounded homothetic sample; the sample's
+    extrapolation is reported beside it as a cross-check."""
+    scene, view, dL = workload()
+    kind, run_sample, desc = cpu_sample_runner(scene, view, dL, args.cpu_k)
+    for _ in range(max(args.warmup, 1)):
+        run_sample()
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        run_sample()
+        ts.append(time.perf_counter() - t0)
+    t_sample = statistics.median(ts) * args.cpu_k
+    ref = _load_reference()
+    t0 = time.perf_counter()
+    if ref is not None:
+        rf, rb = ref
+        fr = rf(scene, view, 0.3, backend_name="cython")
+        rb(scene, view, fr, dL, backend_name="cython")
+    else:
+        from oracle import oracle as O
+        O.set_num_threads(cpu_cores())
+        fr = O.render_forward(scene, view, 0.3)
+        O.render_backward(scene, view, fr, dL)
+    t = time.perf_counter() - t0
+    v = 1.0 / t
+    return {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0,
+        "steps": 1, "warmup": max(args.warmup, 1), "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": kind,
+                         "sample": "one full config-2 frame (1M primitives, 1920x1080, forward + backward) "
+                                   "through the reference's render_forward / render_backward",
+                         "sample_cross_check": {"views_per_s": 1.0 / t_sample, "ms_per_frame": t_sample * 1e3,
+                                                "desc": desc + "; median of 3"}},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -210,6 +303,8 @@ def main():
     ap.add_argument("--cpu-k", type=int, default=16, help="homothetic CPU sample factor")
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-view-batch", action="store_true",
+                    help="skip the config-4 view-batch key (3M scene, 64 views sharded over the ranks)")
     ap.add_argument("--lanes", type=int, default=1,
                     help="config 4: engines on their own streams (views overlap); measured slower at 2-4 "
                          "(668 vs 720 views/s): the cooperative depth sort needs every SM free")
@@ -217,6 +312,8 @@ def main():
                     help="BASELINE.json config: 2 (default, the headline), 3 (50%% skew-free), "
                          "4 (3M, 64-view forward batch sharded over ranks), 5 (2M view-parallel training)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args)
     if args.config in (4, 5):
         import bench_configs
         return bench_configs.main(args)
@@ -235,27 +332,8 @@ def main():
               "l2": "inputs larger than L2 (scene 304 MB, instance lists ~110 MB per frame)"}
 
     if args.impl == "reference":
-        if rank != 0:
-            return
-        scene, view, dL = workload()
-        steps = []
-        kind, run, desc = cpu_sample_runner(scene, view, dL, args.cpu_k)
-        for _ in range(args.warmup):
-            run()
-        for _ in range(args.steps):
-            t0 = time.perf_counter()
-            run()
-            steps.append(time.perf_counter() - t0)
-        t = statistics.median(steps) * args.cpu_k
-        v = 1.0 / t
-        print(json.dumps({
-            "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": config,
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": kind,
-                             "sample": desc + f"; median of {args.steps} steps"},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        if rank == 0:
+            print(json.dumps(reference_arm(args, config)))
         return
 
     import torch
@@ -272,12 +350,14 @@ def main():
     ds = DeviceScene.from_host(scene)
     dL = torch.from_numpy(dL_host).cuda().float()
 
+    g_hold = []
+
     def step(sync=False):
         # no host round trip inside the frame (the instance buffers are sized
         # by the first, synchronised frame; eng.instances() checks after the run)
         # the forward's exact path (flagged pixels) overlaps the backward's main kernel
         f = eng.forward(ds, view, 0.3, sync=sync, defer_exact=True)
-        eng.backward(ds, view, 0.3, f.final_T, f.last_idx, dL, rebin=False)
+        g_hold[:] = [eng.backward(ds, view, 0.3, f.final_T, f.last_idx, dL, rebin=False)]
         return f
 
     def barrier():
@@ -297,8 +377,11 @@ def main():
     for i in range(max(args.warmup, 3)):
         f = step(sync=(i == 0))
     barrier()
+    g_last = g_hold[0]
     m = eng.instances()
     pairs = tile_pairs(f, eng.ranges, WIDTH, HEIGHT)
+    blended = int(f.n_contrib.sum().item())            # pixel-instance pairs that blend
+    redo_px = eng.redo_pixels()
 
     # per-stage CUDA events on separate (untimed) frames: event records inside
     # the timed loop would cost ~2 % of the frame
@@ -419,7 +502,11 @@ def main():
     r_mufu = n_sm * per_clk["ex2"] * f_max
     dom = max(("blend_fwd", "blend_bwd"), key=lambda k: stage_ms.get(k, 0.0))
     t_dom = stage_ms[dom] * 1e-3
-    achieved = FP32_PER_PAIR[dom] * pairs / t_dom
+    # algorithmic work: the FP32 arithmetic of the pixel-instance pairs that
+    # contribute (every blended pair: the per-pair count of SURVEY.md §8(d)),
+    # the minimum any implementation does; the tile-synchronous model
+    # (every pair the reference's loop touches) is kept as model_frac
+    achieved = FP32_PER_PAIR[dom] * blended / t_dom
     kname = {"blend_fwd": "k_blend_forward", "blend_bwd": "k_blend_backward"}[dom]
     try:  # DRAM bytes and issue-slot utilisation of the kernel from the committed ncu --set full capture
         ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
@@ -431,18 +518,23 @@ def main():
                 "frac": achieved / r_fp32, "traffic": traffic, "ncu_issue_slots_busy": issue_busy,
                 "traffic_note": "DRAM bytes per launch (profiles/ncu_traffic.json); the blend kernels are "
                                 "issue-bound, DRAM ~1 % busy",
-                "algorithmic": f"{FP32_PER_PAIR[dom]} FP32 instr/pair x {pairs} tile-synchronous "
-                               f"pixel-instance pairs per launch (SURVEY.md §8(d))",
-                "mufu_frac": MUFU_PER_PAIR[dom] * pairs / t_dom / r_mufu,
-                "frac_note": "frac > 1 is possible: the SURVEY model charges every tile-synchronous pair, "
-                             "while the kernels cull pairs per 8x4-pixel warp block by an exact ellipse test "
-                             "and the backward visits only (warp, instance) pairs the forward blended; "
-                             "profiles/ has the measured issue-slot utilisation",
+                "algorithmic": f"{FP32_PER_PAIR[dom]} FP32 instr/pair x {blended} blended pixel-instance pairs "
+                               f"per launch (sum of n_contrib; SURVEY.md §8(d) per-pair count)",
+                "model_frac": FP32_PER_PAIR[dom] * pairs / t_dom / r_fp32,
+                "model_note": f"SURVEY.md §8(d) model: {FP32_PER_PAIR[dom]} x {pairs} tile-synchronous pairs "
+                              "(every pair the reference's loop visits); the kernels cull per 8x8 warp block, so "
+                              "this can exceed 1",
+                "mufu_frac": MUFU_PER_PAIR[dom] * blended / t_dom / r_mufu,
                 "peak_basis": f"{n_sm} SMs x {per_clk['ffma']:.1f} FFMA lanes/clk x sm_max {f_max/1e6:.0f} MHz, "
                               f"{peak_src}; no dense contraction on this path, tensor cores unused"}
     hbm = float(peaks["hbm_gbs"])
-    stage_bytes = {"preprocess_fwd": n * (304 + 64 + 29),
-                   "preprocess_bwd": n * (304 + 48 + 65 * 4)}
+    # preprocess_bwd: the active-only kernel reads every primitive's 48 B of
+    # screen sums and, for the primitives with a non-zero one, 304 B of
+    # parameters + writes 284 B of gradients (the zero-fill of the others is a
+    # memset on a side stream under the blend backward)
+    n_active = int((g_last.screen.abs().sum(dim=1) > 0).sum().item())
+    stage_bytes = {"preprocess_fwd": n * (304 + 64 + 64 + 29),
+                   "preprocess_bwd": n * 48 + n_active * (304 + 284)}
     stage_roofline = {}
     for k_, b in stage_bytes.items():
         if k_ in stage_ms:
@@ -468,7 +560,16 @@ def main():
         "frame_floor_ms": t_floor * 1e3, "clocks": clk, "e2e": e2e,
         "gpu_launches": LAUNCHES_PER_FRAME * args.steps,
         "gpu_launches_note": LAUNCHES_NOTE,
+        "exact_path": {"pixels": redo_px, "of": WIDTH * HEIGHT,
+                       "note": "pixels whose fp32 decisions the error bounds could not certify, recomputed on "
+                               "the fp64 exact path (blend.cu); every decision equals the reference's"},
+        "blended_pairs": blended,
     }
+    if world > 1:
+        result["nccl"] = {"backend": dist.get_backend(), "nranks": world,
+                          "version": ".".join(str(x) for x in torch.cuda.nccl.version())}
+    if not args.no_view_batch:
+        result["view_batch"] = view_batch(eng, rank, world, local, barrier, max_over_ranks)
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(scene, view, dL_host, args.cpu_k, args.cpu_reps)
     if rank == 0:
@@ -478,4 +579,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main() or 0)

@@ -287,6 +287,9 @@ int ssg_preprocess_backward(const ssg_scene *scene, const ssg_camera *cam,
  * identical either way. */
 #define SSG_PREP_BWD_ACTIVE_ONLY 1
 int ssg_zero_prim_grads(int64_t n, int32_t sh_coeffs, const ssg_grad_buffers *grads, void *stream);
+/* zeroes grads->screen (n,12): what ssg_blend_backward_ex does unless
+ * SSG_BLEND_NO_ZERO, for callers that split the halves across streams */
+int ssg_zero_screen_grads(int64_t n, const ssg_grad_buffers *grads, void *stream);
 int ssg_preprocess_backward_ex(const ssg_scene *scene, const ssg_camera *cam,
                                const ssg_grad_buffers *grads, int32_t flags, void *stream);
 /* the reference's blend-backward plugin contract (raster/_core.pyx:315-343,

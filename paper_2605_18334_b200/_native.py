@@ -33,7 +33,8 @@ EXPORTS = ("ssg_abi_version", "ssg_last_error", "ssg_grid_dims", "ssg_bin_temp_b
            "ssg_loss_scratch_floats", "ssg_image_loss", "ssg_regularize", "ssg_interval_stats_add",
            "ssg_densify_temp_bytes", "ssg_densify_plan", "ssg_densify_apply", "ssg_ply_unpack",
            "ssg_quantize_u8", "ssg_blend_det_temp_bytes", "ssg_blend_backward_det", "ssg_erf_probe",
-           "ssg_pack_splats", "ssg_blend_forward_ex", "ssg_blend_backward_ex")
+           "ssg_pack_splats", "ssg_blend_forward_ex", "ssg_blend_backward_ex",
+           "ssg_zero_screen_grads")
 
 _vp = ctypes.c_void_p
 
@@ -155,6 +156,7 @@ def lib():
     L.ssg_pack_splats.argtypes = [ctypes.c_int64] + [_vp] * 8
     L.ssg_preprocess_backward.argtypes = [P(SsgScene), P(SsgCamera), P(SsgGradBuffers), _vp]
     L.ssg_zero_prim_grads.argtypes = [ctypes.c_int64, ctypes.c_int32, P(SsgGradBuffers), _vp]
+    L.ssg_zero_screen_grads.argtypes = [ctypes.c_int64, P(SsgGradBuffers), _vp]
     L.ssg_preprocess_backward_ex.argtypes = [P(SsgScene), P(SsgCamera), P(SsgGradBuffers), ctypes.c_int32, _vp]
     L.ssg_blend_backward_slots.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                            P(ctypes.c_float), _vp, _vp, P(SsgBinBuffers), P(SsgFrameBuffers),

@@ -437,6 +437,14 @@ extern "C" int ssg_zero_prim_grads(int64_t n, int32_t sh_coeffs, const ssg_grad_
     return SSG_OK;
 }
 
+extern "C" int ssg_zero_screen_grads(int64_t n, const ssg_grad_buffers *grads, void *stream) {
+    using namespace ssg;
+    if (!grads || !grads->screen || n < 0) return SSG_ERR_INVALID_ARGUMENT;
+    const cudaError_t e = cudaMemsetAsync(grads->screen, 0, sizeof(float) * 12 * (size_t)n, (cudaStream_t)stream);
+    if (e != cudaSuccess) { set_error("memset screen grads", e); return SSG_ERR_CUDA; }
+    return SSG_OK;
+}
+
 extern "C" int ssg_preprocess_backward_ex(const ssg_scene *scene, const ssg_camera *cam,
                                           const ssg_grad_buffers *grads, int32_t flags, void *stream) {
     using namespace ssg;

@@ -522,7 +522,7 @@ class Engine:
             else:
                 # exact half on the exact stream (after the forward's exact
                 # half, which is already queued there), main half here
-                self.g_screen[:max(ds.n, 1)].zero_()
+                N.check(self.lib.ssg_zero_screen_grads(ds.n, ctypes.byref(gs), st), "ssg_zero_screen_grads")
                 ex = self._exact_stream()
                 ev = torch.cuda.Event()
                 ev.record(main)
