@@ -47,10 +47,13 @@ constexpr int kBlocks = 8;           // 8x4-pixel blocks per tile (the redo mask
 constexpr float kNearT = 1.05e-4f;   // candidate transmittance below which the stop test needs its bound
 constexpr int kCand = 256;           // redo: candidate instances per segment (per warp)
 constexpr int kRedoWarps = 4;        // redo: warps per CTA
+constexpr int kDoneNaN = 0x7fc00001;   // row coordinate of a pixel that is outside / stopped
+constexpr int kUnsureNaN = 0x7fc00002; // ... of a pixel on the exact path
 
 // Shared-memory image of one instance:
 //   A = (mx_local, my_local, conic_a, conic_b)
-//   B = (conic_c, far_thr, skew_x, skew_y)
+//   B = (conic_c, hw, skew_x, skew_y), hw = -far_thr / 2: a pair is live when
+//       its exponent lies in [far_thr, 0], i.e. |power + hw| <= hw (one compare)
 //   C = (o_sum, o_diff, r, g)
 //   D = (b, sband, g0, g1): the pair's relative alpha error is <= g0 + g1 |power|
 //       (alpha_band); sband = (1/255) (g0 + 6.3 g1): fp32 alpha - 1/255 >= sband
@@ -100,7 +103,7 @@ __device__ __forceinline__ Staged stage_values(const ssg_splat *splat, uint32_t 
             v.X = make_float4(0.0f, 0.0f, 0.0f, INFINITY);          // degenerate: always evaluate
     }
     v.A = make_float4(mx, my, a, b);
-    v.B = make_float4(c, thr, q1.w, q2.x);
+    v.B = make_float4(c, -0.5f * thr, q1.w, q2.x);
     v.C = make_float4(0.5f * (q2.y + q2.z), 0.5f * (q2.y - q2.z), q2.w, q3.x);
     v.D = make_float4(q3.y, SSG_ALPHA_SKIP * band, q3.z, q3.w);
     return v;
@@ -305,28 +308,33 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
     const bool in0 = px < W && py < H, in1 = px < W && py + 4 < H;
     const int start = ranges[2 * tile], end = ranges[2 * tile + 1];
     const float fx = (float)lx + 0.5f;
-    const float2 fy = make_float2((float)ly + 0.5f, (float)ly + 4.5f);
     const float fwx0 = (float)wx0, fwy0 = (float)wy0;
     const double ox = (double)(txi * 16), oy = (double)(tyi * 16);
 
     float2 T = f2(1.0f), dT = f2(0.0f);          // dT: bound on |T - T_reference|
     float2 C0 = f2(0.0f), C1 = f2(0.0f), C2 = f2(0.0f);
     int nc0 = 0, nc1 = 0, li0 = -1, li1 = -1;
-    // bit 0: stopped / outside, bit 1: met a decision its bounds cannot certify
-    // (all_exact: every pixel takes the exact path -- a test mode)
-    int done0 = !in0 ? 1 : (all_exact ? 2 : 0), done1 = !in1 ? 1 : (all_exact ? 2 : 0);
+    // A pixel that is done (outside, stopped, or on the exact path) gets a NaN
+    // row coordinate: its exponent is NaN and every later test fails, so the
+    // hot loop carries no per-pixel done state.  un*: met a decision its
+    // bounds cannot certify (all_exact: every pixel does -- a test mode).
+    float2 fy = make_float2((float)ly + 0.5f, (float)ly + 4.5f);
+    if (!in0) fy.x = __int_as_float(kDoneNaN);
+    else if (all_exact) fy.x = __int_as_float(kUnsureNaN);
+    if (!in1) fy.y = __int_as_float(kDoneNaN);
+    else if (all_exact) fy.y = __int_as_float(kUnsureNaN);
     const uint32_t aA = smem_addr(s.A), aB = smem_addr(s.B), aC = smem_addr(s.C);
     const uint32_t aX = smem_addr(s.X), aD = smem_addr(s.D);
     int kdone = start;    // instances [start, kdone) walked by this warp (mask words written)
 
     for (int base = start; base < end; base += kBatch) {
-        if (__syncthreads_count(done0 && done1) == kThreads) break;
+        if (__syncthreads_count(isnan(fy.x) && isnan(fy.y)) == kThreads) break;
         for (int t = threadIdx.x; t < kBatch && base + t < end; t += kThreads)
             stage_splat(splat, inst_prim[base + t], ox, oy, s, t);
         __syncthreads();
         const int cnt = min(kBatch, end - base);
         for (int c0 = 0; c0 < cnt; c0 += 32) {
-            if (__all_sync(0xffffffffu, done0 && done1)) break;
+            if (__all_sync(0xffffffffu, isnan(fy.x) && isnan(fy.y))) break;
             kdone = base + c0 + 32;
             const int i = c0 + lane;
             bool hit = false;
@@ -346,8 +354,8 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
                 const float4 B = lds128(aB + 16 * j);
                 Pair2 q;
                 pair_power2(fx, fy, A, B, q);
-                const bool live0 = !done0 & (q.power.x >= B.y) & (q.power.x <= 0.0f);
-                const bool live1 = !done1 & (q.power.y >= B.y) & (q.power.y <= 0.0f);
+                const float2 pc = add2(q.power, f2(B.y));
+                const bool live0 = fabsf(pc.x) <= B.y, live1 = fabsf(pc.y) <= B.y;
                 if (!__any_sync(0xffffffffu, live0 | live1)) continue;
                 const float4 C = lds128(aC + 16 * j);
                 const float4 D = lds128(aD + 16 * j);
@@ -364,8 +372,9 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
                 const float2 test_T = mul2(T, oma);                                                // :143
                 const float2 nthr = add2(f2(kNearT), dT);
                 const bool near0 = pass0 & (test_T.x < nthr.x), near1 = pass1 & (test_T.y < nthr.y);
-                bool stop0 = false, stop1 = false;
-                if (__any_sync(0xffffffffu, near0 | near1)) {
+                bool bl0 = pass0, bl1 = pass1;
+                if (__any_sync(0xffffffffu, near0 | near1 | bad0 | bad1)) {
+                    // rare: a candidate stop, or an uncertain decision
                     // |T (1 - alpha) - T_ref (1 - alpha_ref)| <= dT (1 - alpha) + T alpha gp
                     //   + 2 roundings per blend so far (eps / 2 each, relative)
                     const float e0 = fmaf(dT.x, oma.x, T.x * alpha.x * gp.x) +
@@ -374,19 +383,25 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
                                      (float)(nc1 + __popc(lb1) + 2) * 6e-8f * test_T.y;
                     bad0 |= near0 & (fabsf(test_T.x - SSG_T_STOP) <= e0);
                     bad1 |= near1 & (fabsf(test_T.y - SSG_T_STOP) <= e1);
-                    stop0 = near0 & (test_T.x < SSG_T_STOP);                                    // :144-147
-                    stop1 = near1 & (test_T.y < SSG_T_STOP);
+                    const bool stop0 = near0 & (test_T.x < SSG_T_STOP);                          // :144-147
+                    const bool stop1 = near1 & (test_T.y < SSG_T_STOP);
+                    if (stop0 | bad0) {                                                            // :148-154
+                        bl0 = false;
+                        fy.x = __int_as_float(bad0 ? kUnsureNaN : kDoneNaN);
+                    }
+                    if (stop1 | bad1) {
+                        bl1 = false;
+                        fy.y = __int_as_float(bad1 ? kUnsureNaN : kDoneNaN);
+                    }
                 }
-                const bool bl0 = pass0 & !stop0 & !bad0, bl1 = pass1 & !stop1 & !bad1;       // :148-154
-                done0 |= (int)stop0 | ((int)bad0 << 1);
-                done1 |= (int)stop1 | ((int)bad1 << 1);
-                const float2 w = sel2(bl0, bl1, mul2(alpha, T), f2(0.0f));
+                const float2 bm = make_float2(bl0 ? 1.0f : 0.0f, bl1 ? 1.0f : 0.0f);
+                const float2 w = mul2(mul2(alpha, T), bm);
                 C0 = fma2(w, f2(C.z), C0);
                 C1 = fma2(w, f2(C.w), C1);
                 C2 = fma2(w, f2(D.x), C2);
-                const float2 omb = sel2(bl0, bl1, oma, f2(1.0f));
+                const float2 omb = fma2(make_float2(-alpha.x, -alpha.y), bm, f2(1.0f));   // 1 - alpha or 1
                 dT = fma2(w, gp, mul2(dT, omb));
-                T = sel2(bl0, bl1, test_T, T);
+                T = mul2(T, omb);
                 lb0 |= bl0 ? lowb : 0u;
                 lb1 |= bl1 ? lowb : 0u;
             }
@@ -412,7 +427,7 @@ k_blend_forward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float b
             blend_mask[mask_word(start, tile, c, warp)] = 0u;
     // the redo mask is kept per 8x4 block: rows ly (block 4 (warp >> 1) +
     // (warp & 1)) and ly + 4 (two blocks further)
-    const bool un0 = (done0 & 2) && in0, un1 = (done1 & 2) && in1;
+    const bool un0 = in0 && __float_as_int(fy.x) == kUnsureNaN, un1 = in1 && __float_as_int(fy.y) == kUnsureNaN;
     const uint32_t r0 = __ballot_sync(0xffffffffu, un0), r1 = __ballot_sync(0xffffffffu, un1);
     if (lane == 0) {
         const int b0 = (warp >> 1) * 4 + (warp & 1);
@@ -717,6 +732,17 @@ __device__ __forceinline__ float warp_reduce_transposed12(float (&v)[12], int la
     return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
+// one fp32 reduction into global memory (RED, no return value): the
+// destination rows are global, so no generic-address dispatch
+__device__ __forceinline__ void red_add_global(float *p, float v) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ float *lds_ptr(uint32_t a) {
+    uint64_t v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+    return reinterpret_cast<float *>(v);
+}
+
 // d_z * SQRT1_2 of _core.pyx:293-302 (d_z = DA G (2/sqrt(pi)) e^-z^2 (o + (o1-o2)E/2))
 constexpr float kDzScale = SSG_TWO_OVER_SQRT_PI * SSG_SQRT1_2;
 
@@ -799,6 +825,9 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
     // lane 8g + 2c (c < 3) holds component 3g + c after the reduction
     const bool holder = (lane & 1) == 0 && ((lane >> 1) & 3) < 3;
     const int my_comp = 3 * (lane >> 3) + ((lane >> 1) & 3);
+    // this lane's destination pointer slot: sRow[j] + my_comp, read as one
+    // 64-bit shared load per visit (the pointer array's shared-window address)
+    const uint32_t aRow = smem_addr(sRow);
     float *part = kMode != 0 ? s_part + (size_t)warp * kBatch * 12 : nullptr;
 
     // batches aligned to the forward's chunk grid (start + 256 b), top down
@@ -848,8 +877,8 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                 const float4 B = lds128(aB + 16 * j);
                 Pair2 q;
                 pair_power2(fx, fy, A, B, q);
-                const bool live0 = (k <= li0) & (q.power.x >= B.y) & (q.power.x <= 0.0f);   // :263-264, :265-269
-                const bool live1 = (k <= li1) & (q.power.y >= B.y) & (q.power.y <= 0.0f);
+                const float2 pc = add2(q.power, f2(B.y));                                      // :263-269
+                const bool live0 = (k <= li0) & (fabsf(pc.x) <= B.y), live1 = (k <= li1) & (fabsf(pc.y) <= B.y);
                 if (!blend_mask && !__any_sync(0xffffffffu, live0 | live1)) continue;
                 const float4 C = lds128(aC + 16 * j);
                 const float4 D = lds128(aD + 16 * j);
@@ -910,7 +939,7 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                 R2 = fma2(ae, e2, R2);
                 const float v = warp_reduce_transposed12(g, lane);
                 if (holder) {
-                    if (kMode == 0) atomicAdd(sRow[j] + my_comp, v);
+                    if (kMode == 0) red_add_global(lds_ptr(aRow + 8 * j) + my_comp, v);
                     else part[j * 12 + my_comp] = v;
                 }
             }
