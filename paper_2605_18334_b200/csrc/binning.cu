@@ -11,7 +11,7 @@
 // The ranges fall out of step 3 as the exclusive scan of the per-tile counts:
 // [start, start + count), empty tiles at the insertion point, i.e. exactly
 // np.searchsorted(..., "left"/"right") (tiles.py:76-78).
-#include "depth_sort.cuh"
+#include "onesweep.cuh"
 #include "ssg_common.cuh"
 
 namespace ssg {
@@ -26,7 +26,7 @@ static size_t cs_temp_bytes(int64_t n, int64_t capacity, int32_t width, int32_t 
 
 static BinTemp bin_temp(int64_t n, int64_t capacity, int32_t width, int32_t height) {
     BinTemp b;
-    b.sort_depth = dsort::temp_bytes(n > 0 ? n : 1);
+    b.sort_depth = osort::temp_bytes(n > 0 ? n : 1);
     b.sort_tile = width < 1 ? 0 : cs_temp_bytes(n, capacity, width, height);
     b.total = b.sort_depth > b.sort_tile ? b.sort_depth : b.sort_tile;
     return b;
@@ -563,7 +563,7 @@ extern "C" int ssg_bin_prepare(int64_t n, const ssg_prim_buffers *prim, const ss
     const BinTemp L = bin_temp(n, bins->capacity, 0, 0);
     if (bins->temp_bytes < L.total) return SSG_ERR_CAPACITY;
     // 1+2. stable sort of the ids by depth key, counts in depth order, scan
-    cudaError_t e = dsort::sort_and_scan(prim->depth_key, bins->depth_order, prim->tile_count, bins->rank_offset,
+    cudaError_t e = osort::sort_and_scan(prim->depth_key, bins->depth_order, prim->tile_count, bins->rank_offset,
                                          bins->n_instances, n, bins->temp,
                                          (cudaStream_t)stream);
     if (e != cudaSuccess) { set_error("depth sort", e); return SSG_ERR_CUDA; }
@@ -633,7 +633,7 @@ extern "C" int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t heigh
 // ---- test hooks (tests/ only): the depth sort in isolation ---------------
 extern "C" size_t ssg_test_sort_temp_bytes(int64_t n, int key_bytes) {
     using namespace ssg;
-    return key_bytes == 8 ? dsort::temp_bytes(n) : 0;
+    return key_bytes == 8 ? osort::temp_bytes(n) : 0;
 }
 
 // stable sort of u64 keys (not modified): vals <- ids in sorted order
@@ -641,7 +641,7 @@ extern "C" int ssg_test_sort(void *keys, uint32_t *vals, int key_bytes, int iota
                              void *temp, void *stream) {
     using namespace ssg;
     if (key_bytes != 8 || !iota || npass != 8) return SSG_ERR_INVALID_ARGUMENT;
-    cudaError_t e = dsort::sort_and_scan((const uint64_t *)keys, vals, nullptr, nullptr, nullptr, n, temp,
+    cudaError_t e = osort::sort_and_scan((const uint64_t *)keys, vals, nullptr, nullptr, nullptr, n, temp,
                                          (cudaStream_t)stream);
     if (e != cudaSuccess) { set_error("test sort", e); return SSG_ERR_CUDA; }
     return SSG_OK;

@@ -94,6 +94,7 @@ struct Args {
     uint64_t *tile_sums;          // [ntiles]
     uint64_t *keys_a, *keys_b;    // ping-pong keys
     uint32_t *vals_a;             // ping-pong values (the other buffer is order_out)
+    const uint32_t *gate;         // optional: run only when *gate != 0 (the onesweep's fallback)
 };
 
 struct Smem {
@@ -190,6 +191,7 @@ static __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_depth_sort
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem &s = *reinterpret_cast<Smem *>(smem_raw);
     cg::grid_group grid = cg::this_grid();
+    if (a.gate && *((volatile const uint32_t *)a.gate) == 0) return;   // every CTA sees the same flag
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int64_t n = a.n, ntiles = num_tiles(n);
     const uint32_t lt = radix::lanemask_lt();
@@ -501,9 +503,11 @@ static __global__ void __launch_bounds__(kThreads, 1024 / kThreads) k_depth_sort
 }
 
 // Host side: sort (and, with count != nullptr, scan the counts in depth
-// order).  keys are not modified.
+// order).  keys are not modified.  With a gate, the launch returns at once
+// unless *gate != 0 (the exact fallback of onesweep.cuh).
 static inline cudaError_t sort_and_scan(const uint64_t *keys, uint32_t *order, const uint32_t *count, uint64_t *rank_offset,
-                                 int64_t *n_instances, int64_t n, void *temp, cudaStream_t st) {
+                                 int64_t *n_instances, int64_t n, void *temp, cudaStream_t st,
+                                 const uint32_t *gate = nullptr) {
     if (n <= 0) return cudaSuccess;
     char *tp = (char *)temp;
     const int64_t nt = num_tiles(n);
@@ -514,6 +518,7 @@ static inline cudaError_t sort_and_scan(const uint64_t *keys, uint32_t *order, c
     a.rank_offset = rank_offset;
     a.n_instances = n_instances;
     a.n = n;
+    a.gate = gate;
     a.ctl = (Ctl *)tp;
     tp += radix::align256(sizeof(Ctl));
     a.tile_counts = (uint32_t *)tp;

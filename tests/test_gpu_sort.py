@@ -72,3 +72,35 @@ def test_u64_fixup_short_runs_and_long_run_fallback():
     keys2[0] = base + np.uint64(2**40)
     k, v = _sort(keys2, 8, iota=True)
     np.testing.assert_array_equal(v, np.argsort(keys2, kind="stable").astype(np.uint32))
+
+
+# ---- the onesweep path (>= 2M keys: one kernel per pass, decoupled look-back)
+@pytest.mark.parametrize("n", [2_000_000, 2_500_001, 6_000_000])
+def test_onesweep_depth_keys_with_ties_and_invalid(n):
+    rng = np.random.default_rng(n + 3)
+    depth = rng.choice(np.linspace(2.0, 12.0, n // 4), n)
+    keys = depth.view(np.uint64).copy()
+    keys[rng.uniform(0, 1, n) < 0.05] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    k, v = _sort(keys, 8, iota=True)
+    # no-instance keys sort last, the rest stably by key
+    want = np.argsort(keys, kind="stable").astype(np.uint32)
+    np.testing.assert_array_equal(v, want)
+
+
+def test_onesweep_fixup_runs_and_exact_fallback():
+    rng = np.random.default_rng(19)
+    n = 2_200_000
+    base = np.uint64(0xC010000000000000)
+    # a 46-bit spread: the 31-bit window leaves 15 low bits to the fix-up, and
+    # 2.2M keys over 2^14 window values make many short inverted runs
+    keys = base + (rng.integers(0, 2**14, n).astype(np.uint64) << np.uint64(32)) + \
+        rng.integers(0, 2**14, n).astype(np.uint64)
+    k, v = _sort(keys, 8, iota=True)
+    np.testing.assert_array_equal(v, np.argsort(keys, kind="stable").astype(np.uint32))
+    # a long inverted run: the gated cooperative sort redoes the whole sort
+    # (at 6M keys its CTAs sweep several tiles each)
+    for m in (n, 6_000_000):
+        keys2 = base + rng.integers(0, 2**9, m).astype(np.uint64)
+        keys2[0] = base + np.uint64(2**44)
+        k, v = _sort(keys2, 8, iota=True)
+        np.testing.assert_array_equal(v, np.argsort(keys2, kind="stable").astype(np.uint32))
