@@ -98,7 +98,7 @@ typedef struct ssg_splat64 {
     double conic_a, conic_b, conic_c;
     double skew_x, skew_y;
     double o1, o2;
-    double pad;
+    double comp;                /* dilation compensation (projection.py:201); 0 from ssg_pack_splats */
 } ssg_splat64;
 
 /* Per-primitive buffers written by ssg_preprocess_forward. */
@@ -312,7 +312,8 @@ int ssg_image_loss(const float *rendered, const float *target, int32_t width, in
                    float lambda_ssim, float *scratch, float *dL_dpixels, double *sums, void *stream);
 /* optimize/losses.py:116-136 scene_regularizers folded into the gradients:
  * d_beta = d_eta + 2 lambda_beta beta, d_logits += the opacity-gap term,
- * sums[2] = the penalty value */
+ * sums[2] = the penalty value.  d_eta, d_beta and d_logits all NULL: the
+ * value only (losses.py:146-149 tests loss + penalty for finiteness) */
 int ssg_regularize(int64_t n, const float *beta, const float *opacity_logits, const float *d_eta,
                    float lambda_beta, float lambda_opacity, float *d_beta, float *d_logits, double *sums,
                    void *stream);

@@ -19,8 +19,11 @@ OBJ_DIR = os.path.join(HERE, "csrc", "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
-# per-file extra flags: K1 must not contract (tile lists are bit-exact)
-EXTRA = {"preprocess_fwd.cu": ["--fmad=false"], "densify.cu": ["--fmad=false"]}
+# per-file extra flags: K1 must not contract (tile lists are bit-exact); the
+# backward projection recomputes K1's colour clamp and validity, so it rounds
+# the same way
+EXTRA = {"preprocess_fwd.cu": ["--fmad=false"], "preprocess_bwd.cu": ["--fmad=false"],
+         "densify.cu": ["--fmad=false"]}
 SOURCES = ["api.cu", "preprocess_fwd.cu", "binning.cu", "blend.cu", "preprocess_bwd.cu", "adam.cu", "train.cu", "densify.cu", "ply.cu", "serve.cu"]
 HEADERS = ["ssg_common.cuh", "radix_sort.cuh", "depth_sort.cuh", "onesweep.cuh", os.path.join("..", "..", "include", "ssg_b200.h")]
 

@@ -88,7 +88,7 @@ k_preprocess_forward(ssg_scene sc, ssg_camera cam, ssg_prim_buffers out, int ntx
         e.skew_y = P.skew[1];
         e.o1 = P.sig[0] * P.comp;   // projection.py:209-210
         e.o2 = P.sig[1] * P.comp;
-        e.pad = 0.0;
+        e.comp = P.comp;
         s.band0 = alpha_band(e.conic_a, e.conic_b, e.conic_c, e.skew_x, e.skew_y, e.o1, e.o2, &s.band1);
         // 64-byte records as four 16-byte stores each
         const int4 *src = reinterpret_cast<const int4 *>(&s);
@@ -159,7 +159,7 @@ __global__ void k_pack_splats(int64_t n, const double *__restrict__ mean2d, cons
     e.skew_y = skew2d[2 * i + 1];
     e.o1 = opair[2 * i];
     e.o2 = opair[2 * i + 1];
-    e.pad = 0.0;
+    e.comp = 0.0;
     ssg_splat s;
     s.mean_x = mean2d[2 * i];
     s.mean_y = mean2d[2 * i + 1];

@@ -239,7 +239,7 @@ __global__ void k_regularize(int64_t n, const float *__restrict__ beta, const fl
     if (i < n) {
         for (int j = 0; j < 3; j++) {
             const float b = beta[3 * i + j];
-            d_beta[3 * i + j] = d_eta[3 * i + j] + (lb > 0.f ? 2.f * lb * b : 0.f);
+            if (d_beta) d_beta[3 * i + j] = d_eta[3 * i + j] + (lb > 0.f ? 2.f * lb * b : 0.f);
             if (lb > 0.f) val += (double)lb * (double)b * (double)b;
         }
         if (lo > 0.f) {
@@ -252,8 +252,10 @@ __global__ void k_regularize(int64_t n, const float *__restrict__ beta, const fl
             const double gap = sg[0] - sg[1];
             val += (double)lo * fabs(gap);
             const double sgn = gap > 0 ? 1.0 : (gap < 0 ? -1.0 : 0.0);
-            d_logits[2 * i] += (float)(lo * sgn * sg[0] * (1.0 - sg[0]));
-            d_logits[2 * i + 1] += (float)(-lo * sgn * sg[1] * (1.0 - sg[1]));
+            if (d_logits) {
+                d_logits[2 * i] += (float)(lo * sgn * sg[0] * (1.0 - sg[0]));
+                d_logits[2 * i + 1] += (float)(-lo * sgn * sg[1] * (1.0 - sg[1]));
+            }
         }
     }
     const double t = block_sum(val, s_red);
@@ -319,7 +321,11 @@ extern "C" int ssg_regularize(int64_t n, const float *beta, const float *opacity
                               float lambda_beta, float lambda_opacity, float *d_beta, float *d_logits,
                               double *sums, void *stream) {
     using namespace ssg;
-    if (n < 0 || (n > 0 && (!beta || !opacity_logits || !d_eta || !d_beta || !d_logits)) || !sums)
+    // d_eta, d_beta and d_logits all NULL = the penalty value only (the
+    // finite-loss test of a step runs before its backward)
+    const bool value_only = !d_eta && !d_beta && !d_logits;
+    if (n < 0 || (n > 0 && (!beta || !opacity_logits || (!value_only && (!d_eta || !d_beta || !d_logits)))) ||
+        !sums)
         return SSG_ERR_INVALID_ARGUMENT;
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(sums + 2, 0, sizeof(double), st);

@@ -362,6 +362,21 @@ class Engine:
                     "ssg_preprocess_forward")
         return self._bin(ds.n, W, H, sync)
 
+    def project(self, ds: DeviceScene, view: CameraView, s: float = 0.3) -> torch.Tensor:
+        """Projection only (projection.py:151-235): the screen radii (n,)
+        fp64 of `view` -- what the reference's densify cadence reads for its
+        max_radii (trainer.py:139-141)."""
+        cam = camera_struct(view, s)
+        if int(cam.width) > 65535 or int(cam.height) > 65535:
+            raise ValueError("image dimension overflow")
+        self._ensure_prim(ds.n)
+        sc = ds.struct()
+        N.check(self.lib.ssg_preprocess_forward(ctypes.byref(sc), ctypes.byref(cam),
+                                                ctypes.byref(self._prim_struct()), self._stream()),
+                "ssg_preprocess_forward")
+        self._bin_gen += 1  # the splat records no longer match the last binning
+        return self.radius[:ds.n]
+
     def bin_arrays(self, mean2d, radius, depth, valid, W: int, H: int) -> int:
         """Binning of caller-provided screen arrays (device tensors, fp64/uint8)."""
         n = int(mean2d.shape[0])

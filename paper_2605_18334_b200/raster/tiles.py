@@ -61,17 +61,13 @@ def bin_arrays(mean2d, radius, depth, valid, width: int, height: int) -> TileGri
 
 
 def bin_and_sort(splats, width: int, height: int) -> TileGrid:
-    """List-of-splats variant (tiles.py:82-96); None entries are culled."""
+    """List-of-splats variant (tiles.py:82-96): None entries are culled (an
+    invalid row), the others binned by their mean, radius and depth."""
     n = len(splats)
-    mean2d = np.zeros((n, 2))
-    radius = np.zeros(n)
-    depth = np.zeros(n)
+    live = [i for i, sp in enumerate(splats) if sp is not None]
+    mean2d, radius, depth = np.zeros((n, 2)), np.zeros(n), np.zeros(n)
     valid = np.zeros(n, dtype=bool)
-    for i, sp in enumerate(splats):
-        if sp is None:
-            continue
-        mean2d[i] = sp.mean2d
-        radius[i] = sp.radius
-        depth[i] = sp.depth
-        valid[i] = True
+    valid[live] = True
+    for i in live:
+        mean2d[i], radius[i], depth[i] = splats[i].mean2d, splats[i].radius, splats[i].depth
     return bin_arrays(mean2d, radius, depth, valid, width, height)

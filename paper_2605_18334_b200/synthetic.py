@@ -17,7 +17,7 @@ import math
 import numpy as np
 
 from .camera import OPENCV, CameraView, look_at
-from .scene import Scene
+from .scene import Scene, SkewGaussian
 
 
 def fp32_round(scene: Scene) -> Scene:
@@ -124,3 +124,25 @@ def homothetic_sample(scene: Scene, view: CameraView, k: int, seed: int = 99):
     h = max(int(round(view.height / g)), 16)
     v = CameraView(view.c2w, view.convention, w, h, view.fov_x)
     return fp32_round(sub), v
+
+
+# ---- the reference's blob fixture (synthetic.py:22-47), for the trainer tests
+BLOB_BACKGROUND = (0.05, 0.05, 0.08)
+
+
+def _blob(position, color, scale, opacity=0.92) -> SkewGaussian:
+    logit = math.log(opacity / (1.0 - opacity))
+    sh = np.zeros((1, 3))
+    sh[0] = (np.asarray(color, dtype=np.float64) - 0.5) / 0.28209479177387814
+    return SkewGaussian(mu=np.asarray(position, dtype=np.float64),
+                        log_scale=np.log(np.asarray(scale, dtype=np.float64)),
+                        rot=np.array([1.0, 0.0, 0.0, 0.0]), sh=sh, opacity_logits=np.array([logit, logit]),
+                        beta=np.zeros(3), dir=np.zeros(3))
+
+
+def blob_scene() -> Scene:
+    """Three coloured, slightly anisotropic blobs (synthetic.py:39-46)."""
+    prims = [_blob((-0.7, 0.0, 0.2), (0.85, 0.15, 0.10), (0.42, 0.30, 0.34)),
+             _blob((0.6, 0.35, -0.1), (0.12, 0.75, 0.20), (0.30, 0.44, 0.30)),
+             _blob((0.1, -0.5, -0.3), (0.15, 0.25, 0.88), (0.36, 0.30, 0.42))]
+    return Scene.from_primitives(prims, background=BLOB_BACKGROUND, sh_degree=0)

@@ -158,6 +158,8 @@ class IntervalStats:
         """`skip`: optional device int32 flag; nonzero = this step adds nothing
         (the caller then takes the `views` back, see Trainer)."""
         n = self.uv_sum.numel()
+        if grads.g_uv.numel() != n:  # trainer.py:146 starts a new interval after densify
+            raise ValueError(f"IntervalStats covers {n} primitives, gradients {grads.g_uv.numel()}")
         N.check(N.lib().ssg_interval_stats_add_ex(n, grads.g_uv.data_ptr(), grads.g_z.data_ptr(),
                                                   grads.d_mu.data_ptr(), self.uv_sum.data_ptr(),
                                                   self.z_max.data_ptr(), self.mu_sum.data_ptr(),
@@ -307,7 +309,7 @@ class Trainer:
         n = ds.n
         if self.d_beta is None or self.d_beta.shape[0] < n:
             self.d_beta = torch.empty((max(n, 1), 3), dtype=torch.float32, device=eng.device)
-        lossfn.sums[2].zero_()
+        self._penalty(lossfn)
         v = lossfn.value_tensor()
         # the step's fate on the device: 2 overflow > 1 non-finite > 0 run
         over = eng.n_inst_dev[1] > eng.capacity
@@ -334,6 +336,14 @@ class Trainer:
         self._pending = (ev, (view, target, iteration, stats, s, group), loss)
         return loss, f
 
+    def _penalty(self, lossfn):
+        """sums[2] = the regularizer value (value-only ssg_regularize), so
+        the finite-loss test sees loss + penalty as fit2d.py:69-71 does."""
+        ds, cfg = self.ds, self.cfg
+        N.check(N.lib().ssg_regularize(ds.n, ds.beta.data_ptr(), ds.opacity_logits.data_ptr(), None,
+                                       cfg.lambda_beta_reg, cfg.lambda_opacity_reg, None, None,
+                                       lossfn.sums.data_ptr(), _stream(self.eng.device)), "ssg_regularize")
+
     def _step_sync(self, view, target: torch.Tensor, iteration: int, stats: IntervalStats | None,
                    s: float, group, check_finite: bool):
         eng, ds, cfg = self.eng, self.ds, self.cfg
@@ -345,14 +355,14 @@ class Trainer:
             self.d_beta = torch.empty((max(n, 1), 3), dtype=torch.float32, device=eng.device)
         # the regularizer value is part of the loss (losses.py:146-149); its
         # gradients are folded in after the backward and the statistics
-        lossfn.sums[2].zero_()
+        self._penalty(lossfn)
         v = lossfn.value_tensor()
         try:  # one read-back for the instance-count check and the loss value
             _, (loss,) = eng.instances(v)
         except N.NativeError:  # the scene outgrew the instance buffers: redo synchronised
             f = eng.forward(ds, view, s, sync=True)
             dL = lossfn(f.color, target)
-            lossfn.sums[2].zero_()
+            self._penalty(lossfn)
             v = lossfn.value_tensor()
             loss = float(v)
         if check_finite:

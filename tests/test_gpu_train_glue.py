@@ -93,6 +93,12 @@ def test_regularizers_match_reference():
                                    cfg.lambda_opacity_reg, d_beta.data_ptr(), d_logits.data_ptr(), sums.data_ptr(),
                                    torch.cuda.current_stream().cuda_stream), "ssg_regularize")
     assert abs(float(sums[2]) - want_v) <= 1e-6 * max(1.0, abs(want_v))
+    full = float(sums[2])
+    # value-only pass (the finite-loss test runs it before the backward)
+    N.check(N.lib().ssg_regularize(n, beta.data_ptr(), logits.data_ptr(), None, cfg.lambda_beta_reg,
+                                   cfg.lambda_opacity_reg, None, None, sums.data_ptr(),
+                                   torch.cuda.current_stream().cuda_stream), "ssg_regularize")
+    assert float(sums[2]) == full
     np.testing.assert_allclose(d_beta.double().cpu().numpy(), want_db, rtol=1e-6, atol=1e-9)
     np.testing.assert_allclose(d_logits.double().cpu().numpy(), want_dl, rtol=1e-5, atol=1e-9)
 
@@ -114,6 +120,36 @@ def test_interval_stats_match_reference():
     np.testing.assert_allclose(b.g_uv.cpu().numpy(), uv / 4, rtol=1e-12)
     np.testing.assert_array_equal(b.g_z.double().cpu().numpy(), zmax)
     np.testing.assert_allclose(b.d_mu.cpu().numpy(), mu / 4, rtol=1e-12)
+
+
+def test_interval_stats_rejects_a_resized_scene():
+    """trainer.py:146 starts new statistics after a densify; a stale
+    accumulator fails loudly instead of reading past the gradients."""
+    st = IntervalStats(10, torch.device("cuda"))
+    g = SimpleNamespace(g_uv=torch.zeros(12, device="cuda"), g_z=torch.zeros(12, device="cuda"),
+                        d_mu=torch.zeros((12, 3), device="cuda"))
+    with pytest.raises(ValueError, match="10 primitives"):
+        st.add(g)
+
+
+@pytest.mark.parametrize("pipelined", [False, True])
+def test_non_finite_penalty_skips_the_step(pipelined):
+    """fit2d.py:69-71 tests loss + regularizer: an infinite
+    beta penalty (here an infinite lambda) skips the update."""
+    rng = np.random.default_rng(5)
+    scene = fp32_round(random_scene(rng, 60, sh_degree=1))
+    view = random_view(rng, 32, 32)
+    eng = Engine()
+    ds = DeviceScene.from_host(scene)
+    cfg = TrainConfig(lambda_beta_reg=float("inf"))
+    tr = Trainer(eng, ds, DeviceAdam(ds, cfg), pipelined=pipelined)
+    mu0 = ds.mu.clone()
+    target = torch.rand((32, 32, 3), device="cuda")
+    loss, _ = tr.step(view, target, 0)
+    if pipelined:
+        tr.flush()
+    assert not np.isfinite(float(loss))
+    assert torch.equal(ds.mu, mu0)
 
 
 def test_training_step_matches_reference():
