@@ -25,7 +25,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
 EXTRA = {"preprocess_fwd.cu": ["--fmad=false"], "preprocess_bwd.cu": ["--fmad=false"],
          "densify.cu": ["--fmad=false"]}
 SOURCES = ["api.cu", "preprocess_fwd.cu", "binning.cu", "blend.cu", "preprocess_bwd.cu", "adam.cu", "train.cu", "densify.cu", "ply.cu", "serve.cu"]
-HEADERS = ["ssg_common.cuh", "radix_sort.cuh", "depth_sort.cuh", "onesweep.cuh", os.path.join("..", "..", "include", "ssg_b200.h")]
+HEADERS = ["ssg_common.cuh", "radix_sort.cuh", "depth_sort.cuh", "onesweep.cuh", "bucket_sort.cuh", os.path.join("..", "..", "include", "ssg_b200.h")]
 
 
 def _newest_input_mtime(src: str) -> float:

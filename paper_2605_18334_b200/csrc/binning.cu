@@ -11,7 +11,7 @@
 // The ranges fall out of step 3 as the exclusive scan of the per-tile counts:
 // [start, start + count), empty tiles at the insertion point, i.e. exactly
 // np.searchsorted(..., "left"/"right") (tiles.py:76-78).
-#include "onesweep.cuh"
+#include "bucket_sort.cuh"
 #include "ssg_common.cuh"
 
 namespace ssg {
@@ -24,9 +24,24 @@ struct BinTemp {
 
 static size_t cs_temp_bytes(int64_t n, int64_t capacity, int32_t width, int32_t height);
 
+// steps 1+2: the bucket sort (bucket_sort.cuh); SSG_DEPTH_SORT=1 selects the
+// onesweep radix sort instead (A/B builds)
+#ifndef SSG_DEPTH_SORT
+#define SSG_DEPTH_SORT 0
+#endif
+static inline size_t depth_sort_temp(int64_t n) {
+    return SSG_DEPTH_SORT == 1 ? osort::temp_bytes(n) : bsort::temp_bytes(n);
+}
+static inline cudaError_t depth_sort(const uint64_t *keys, uint32_t *order, const uint32_t *count,
+                                     uint64_t *rank_offset, int64_t *n_instances, int64_t n, void *temp,
+                                     cudaStream_t st) {
+    if (SSG_DEPTH_SORT == 1) return osort::sort_and_scan(keys, order, count, rank_offset, n_instances, n, temp, st);
+    return bsort::sort_and_scan(keys, order, count, rank_offset, n_instances, n, temp, st);
+}
+
 static BinTemp bin_temp(int64_t n, int64_t capacity, int32_t width, int32_t height) {
     BinTemp b;
-    b.sort_depth = osort::temp_bytes(n > 0 ? n : 1);
+    b.sort_depth = depth_sort_temp(n > 0 ? n : 1);
     b.sort_tile = width < 1 ? 0 : cs_temp_bytes(n, capacity, width, height);
     b.total = b.sort_depth > b.sort_tile ? b.sort_depth : b.sort_tile;
     return b;
@@ -563,9 +578,8 @@ extern "C" int ssg_bin_prepare(int64_t n, const ssg_prim_buffers *prim, const ss
     const BinTemp L = bin_temp(n, bins->capacity, 0, 0);
     if (bins->temp_bytes < L.total) return SSG_ERR_CAPACITY;
     // 1+2. stable sort of the ids by depth key, counts in depth order, scan
-    cudaError_t e = osort::sort_and_scan(prim->depth_key, bins->depth_order, prim->tile_count, bins->rank_offset,
-                                         bins->n_instances, n, bins->temp,
-                                         (cudaStream_t)stream);
+    cudaError_t e = depth_sort(prim->depth_key, bins->depth_order, prim->tile_count, bins->rank_offset,
+                               bins->n_instances, n, bins->temp, (cudaStream_t)stream);
     if (e != cudaSuccess) { set_error("depth sort", e); return SSG_ERR_CUDA; }
     return check_launch("ssg_bin_prepare");
 }
@@ -633,7 +647,7 @@ extern "C" int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t heigh
 // ---- test hooks (tests/ only): the depth sort in isolation ---------------
 extern "C" size_t ssg_test_sort_temp_bytes(int64_t n, int key_bytes) {
     using namespace ssg;
-    return key_bytes == 8 ? osort::temp_bytes(n) : 0;
+    return key_bytes == 8 ? depth_sort_temp(n) : 0;
 }
 
 // stable sort of u64 keys (not modified): vals <- ids in sorted order
@@ -641,8 +655,7 @@ extern "C" int ssg_test_sort(void *keys, uint32_t *vals, int key_bytes, int iota
                              void *temp, void *stream) {
     using namespace ssg;
     if (key_bytes != 8 || !iota || npass != 8) return SSG_ERR_INVALID_ARGUMENT;
-    cudaError_t e = osort::sort_and_scan((const uint64_t *)keys, vals, nullptr, nullptr, nullptr, n, temp,
-                                         (cudaStream_t)stream);
+    cudaError_t e = depth_sort((const uint64_t *)keys, vals, nullptr, nullptr, nullptr, n, temp, (cudaStream_t)stream);
     if (e != cudaSuccess) { set_error("test sort", e); return SSG_ERR_CUDA; }
     return SSG_OK;
 }

@@ -1,19 +1,15 @@
-"""Summarise an ncu --metrics gpu__time_duration.sum --csv launch list."""
+"""Print the last frame's kernels from an ncu --metrics gpu__time_duration.sum
+--csv launch list: python tools/launch_table.py launches.csv [frames]"""
 import csv
 import sys
-from collections import defaultdict
 
-rows = list(csv.reader(open(sys.argv[1])))
-for i, r in enumerate(rows):
-    if "Kernel Name" in r:
-        h, start = r, i
-        break
-ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
-d = defaultdict(list)
-for r in rows[start + 1:]:
-    v = float(r[vi].replace(",", ""))
-    v = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0) * v
-    d[r[ki].split("(")[0][-48:]].append(v)
-tot = sum(sum(v) for v in d.values())
-for k, v in sorted(d.items(), key=lambda x: -sum(x[1])):
-    print(f"{k:48s} n={len(v):4d} mean_us={sum(v)/len(v):9.1f} total_us={sum(v):10.1f} {100*sum(v)/tot:5.1f}%")
+rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 5]
+h, rows = rows[0], rows[1:]
+ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+frames = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+tot = 0.0
+for r in rows[len(rows) - len(rows) // frames:]:
+    us = float(r[vi].replace(",", "")) / 1000
+    tot += us
+    print(f"{us:8.1f} us  {r[ki][:90]}")
+print(f"{tot:8.1f} us  total")
