@@ -92,7 +92,6 @@ def config4(args, rank, world, local):
     barrier()
     clocks = B.ClockSampler(local)
     clocks.start()
-    eng.stage_events = {}
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_start = time.perf_counter()
@@ -104,7 +103,12 @@ def config4(args, rank, world, local):
     clocks.mark(t_start, time.perf_counter())
     clk = clocks.stop()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-    stage_ms = {k: statistics.mean(a.elapsed_time(b) for a, b in v) for k, v in eng.stage_events.items()}
+    # per-stage times from one separate, untimed batch (stage events would
+    # perturb the timed loop): totals over the batch / views
+    eng.stage_events = {}
+    render_views(ds, mine, engine=lanes, out=out)
+    torch.cuda.synchronize()
+    stage_ms = {k: sum(a.elapsed_time(b) for a, b in v) / max(len(mine), 1) for k, v in eng.stage_events.items()}
     eng.stage_events = None
 
     # e2e: the reference-facing call per view (render_forward with the scene in

@@ -45,6 +45,7 @@ typedef enum {
 
 #define SSG_TILE 16               /* raster/tiles.py:16 */
 #define SSG_MAX_IMAGE_DIM 65535   /* raster/forward.py:21 */
+#define SSG_MAX_BATCH_VIEWS 8     /* cameras per ssg_preprocess_forward_views call */
 
 /* Scene on the device (reference Scene, scene.py:99-121).  Geometry that
  * decides tile membership and depth order stays fp64 so the tile lists are
@@ -212,6 +213,15 @@ int ssg_pack_splats(int64_t n, const double *mean2d, const double *conic, const 
                     void *stream);
 int ssg_preprocess_forward(const ssg_scene *scene, const ssg_camera *cam,
                            const ssg_prim_buffers *out, void *stream);
+/* ssg_preprocess_forward for a batch of n_views (1..SSG_MAX_BATCH_VIEWS) cameras of
+ * one scene in one pass over the scene (each primitive read once per batch; the
+ * view-independent part of projection.py:151-235 -- scene.py:66-96 Sigma_world,
+ * the sigmoids, Sigma eta -- computed once): outs[v] receives exactly what
+ * ssg_preprocess_forward(scene, &cams[v], &outs[v]) writes.  outs[v].valid /
+ * .depth / .radius may be NULL (not written).  Replaces the per-view project_scene
+ * calls of the reference's trajectory loop (trajectory.py:12-31). */
+int ssg_preprocess_forward_views(const ssg_scene *scene, const ssg_camera *cams,
+                                 const ssg_prim_buffers *outs, int32_t n_views, void *stream);
 /* depth sort, counts in depth order, exclusive scan; writes bins->n_instances */
 int ssg_bin_prepare(int64_t n, const ssg_prim_buffers *prim, const ssg_bin_buffers *bins,
                     void *stream);

@@ -34,7 +34,7 @@ EXPORTS = ("ssg_abi_version", "ssg_last_error", "ssg_grid_dims", "ssg_bin_temp_b
            "ssg_densify_temp_bytes", "ssg_densify_plan", "ssg_densify_apply", "ssg_ply_unpack",
            "ssg_quantize_u8", "ssg_blend_det_temp_bytes", "ssg_blend_backward_det", "ssg_erf_probe",
            "ssg_pack_splats", "ssg_blend_forward_ex", "ssg_blend_backward_ex",
-           "ssg_zero_screen_grads")
+           "ssg_zero_screen_grads", "ssg_preprocess_forward_views")
 
 _vp = ctypes.c_void_p
 
@@ -105,7 +105,8 @@ class SsgAdamHparams(ctypes.Structure):
 
 SPLAT_BYTES = 64
 SPLAT64_BYTES = 64
-ABI_VERSION = 5
+ABI_VERSION = 6
+MAX_BATCH_VIEWS = 8  # SSG_MAX_BATCH_VIEWS
 
 _lib = None
 
@@ -131,6 +132,7 @@ def lib():
     L.ssg_bin_temp_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                      P(ctypes.c_size_t)]
     L.ssg_preprocess_forward.argtypes = [P(SsgScene), P(SsgCamera), P(SsgPrimBuffers), _vp]
+    L.ssg_preprocess_forward_views.argtypes = [P(SsgScene), P(SsgCamera), P(SsgPrimBuffers), ctypes.c_int32, _vp]
     L.ssg_bin_rects.argtypes = [ctypes.c_int64, _vp, _vp, _vp, _vp, ctypes.c_int32,
                                 ctypes.c_int32, P(SsgPrimBuffers), _vp]
     L.ssg_bin_prepare.argtypes = [ctypes.c_int64, P(SsgPrimBuffers), P(SsgBinBuffers), _vp]

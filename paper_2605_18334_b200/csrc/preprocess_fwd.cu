@@ -141,6 +141,221 @@ extern "C" int ssg_preprocess_forward(const ssg_scene *scene, const ssg_camera *
     return check_launch("k_preprocess_forward");
 }
 
+namespace ssg {
+// ------------------------------------------------------------ view batch
+// K1 over a batch of up to SSG_MAX_BATCH_VIEWS cameras of one scene (the
+// config-4 trajectory batch; the reference renders such batches one
+// render_forward at a time, trajectory.py:12-31).  One thread per primitive
+// reads the primitive's 304 bytes once for the whole batch instead of once
+// per view: the geometry into registers, the view-independent part of the
+// projection (world_geometry: rotation, Sigma_world, sigmoids, Sigma eta)
+// computed once, the SH row staged into shared memory by cp.async (the
+// block's rows are one contiguous range: fully coalesced 16-byte copies,
+// landing while view 0's geometry runs).  Per view it runs view_geometry
+// and the SH dot product with the same operation sequence as
+// k_preprocess_forward, so every output is bit-identical to the
+// single-view kernel's.  valid / depth / radius may be NULL per view
+// (introspection-only outputs a throughput batch skips).
+constexpr int kMvThreads = 128;
+
+// padded smem row stride (floats) of a 3K-float SH row: conflict-free
+// LDS.128 when 3K % 4 == 0 (an odd number of 16-byte units per row), an odd
+// stride for scalar rows
+__host__ __device__ constexpr int mv_sh_stride(int K3) {
+    return (K3 % 4 == 0) ? ((K3 / 4) % 2 == 0 ? K3 + 4 : K3) : K3;
+}
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+struct MvArgs {
+    ssg_camera cam[SSG_MAX_BATCH_VIEWS];
+    ssg_prim_buffers out[SSG_MAX_BATCH_VIEWS];
+    int ntx[SSG_MAX_BATCH_VIEWS], nty[SSG_MAX_BATCH_VIEWS];
+    int nv;
+};
+
+template <int DEG>
+__global__ void __launch_bounds__(kMvThreads)
+k_preprocess_forward_views(ssg_scene sc, const __grid_constant__ MvArgs a) {
+    constexpr int K = (DEG + 1) * (DEG + 1), K3 = 3 * K, S = mv_sh_stride(K3);
+    extern __shared__ __align__(16) float s_sh[];  // [kMvThreads][S]
+    const int64_t base = (int64_t)blockIdx.x * kMvThreads;
+    const int rows = (int)(sc.n - base < kMvThreads ? sc.n - base : kMvThreads);
+    const int tid = threadIdx.x;
+    // stage the block's SH rows (one contiguous range of rows * K3 floats)
+    if constexpr (K3 % 4 == 0) {
+        const float *src = sc.sh + base * K3;
+        for (int e = tid; e < rows * (K3 / 4); e += kMvThreads) {
+            const int r = e / (K3 / 4), c = e - r * (K3 / 4);
+            cp_async16(s_sh + r * S + 4 * c, src + 4 * (int64_t)e);
+        }
+    } else {
+        const float *src = sc.sh + base * K3;
+        for (int e = tid; e < rows * K3; e += kMvThreads) {
+            const int r = e / K3, c = e - r * K3;
+            cp_async4(s_sh + r * S + c, src + e);
+        }
+    }
+    const int64_t i = base + tid;
+    const bool live = tid < rows;
+    double mu[3] = {0.0, 0.0, 0.0};
+    Proj P;
+    if (live) {
+        double ls[3], q4[4], eta[3];
+        float logit[2];
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+            mu[j] = sc.mu[3 * i + j];
+            ls[j] = sc.log_scale[3 * i + j];
+            eta[j] = (double)sc.beta[3 * i + j] + (double)sc.dir[3 * i + j];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) q4[j] = sc.rot[4 * i + j];
+        logit[0] = sc.opacity_logits[2 * i];
+        logit[1] = sc.opacity_logits[2 * i + 1];
+        world_geometry(ls, q4, logit, eta, P);
+    }
+    bool staged = false;
+    for (int v = 0; v < a.nv; v++) {
+        const ssg_camera &cam = a.cam[v];
+        const ssg_prim_buffers &out = a.out[v];
+        bool fb = false;
+        if (live) view_geometry(cam, mu, P);
+        if (!staged) {  // block-uniform: the SH rows have landed
+            cp_async_wait_all();
+            __syncthreads();
+            staged = true;
+        }
+        if (live) {
+            fb = P.fallback;
+            double dv0 = mu[0] - cam.campos[0], dv1 = mu[1] - cam.campos[1], dv2 = mu[2] - cam.campos[2];
+            double dn = sqrt(dv0 * dv0 + dv1 * dv1 + dv2 * dv2);
+            double dns = dn > 1e-12 ? dn : 1.0;
+            float basis[16];
+            sh_basis_f(DEG, (float)(dv0 / dns), (float)(dv1 / dns), (float)(dv2 / dns), basis);
+            float col[3] = {0.0f, 0.0f, 0.0f};
+            const float *row = s_sh + tid * S;
+            if constexpr (K3 % 4 == 0) {
+#pragma unroll
+                for (int q = 0; q < K3 / 4; q++) {
+                    const float4 v4 = *reinterpret_cast<const float4 *>(row + 4 * q);
+                    const float e[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+                    for (int u = 0; u < 4; u++)
+                        col[(4 * q + u) % 3] = fmaf(basis[(4 * q + u) / 3], e[u], col[(4 * q + u) % 3]);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < K; k++)
+#pragma unroll
+                    for (int c = 0; c < 3; c++) col[c] = fmaf(basis[k], row[3 * k + c], col[c]);
+            }
+            ssg_splat s;
+            s.mean_x = P.mean2d[0];
+            s.mean_y = P.mean2d[1];
+            s.conic_a = (float)P.inv_dil[0];
+            s.conic_b = (float)P.inv_dil[1];
+            s.conic_c = (float)P.inv_dil[3];
+            s.skew_x = (float)P.skew[0];
+            s.skew_y = (float)P.skew[1];
+            s.o1 = (float)(P.sig[0] * P.comp);
+            s.o2 = (float)(P.sig[1] * P.comp);
+            s.r = fmaxf(col[0] + 0.5f, 0.0f);
+            s.g = fmaxf(col[1] + 0.5f, 0.0f);
+            s.b = fmaxf(col[2] + 0.5f, 0.0f);
+            ssg_splat64 e;
+            e.conic_a = P.inv_dil[0];
+            e.conic_b = P.inv_dil[1];
+            e.conic_c = P.inv_dil[3];
+            e.skew_x = P.skew[0];
+            e.skew_y = P.skew[1];
+            e.o1 = P.sig[0] * P.comp;
+            e.o2 = P.sig[1] * P.comp;
+            e.comp = P.comp;
+            s.band0 = alpha_band(e.conic_a, e.conic_b, e.conic_c, e.skew_x, e.skew_y, e.o1, e.o2, &s.band1);
+            const int4 *src = reinterpret_cast<const int4 *>(&s);
+            int4 *dst = reinterpret_cast<int4 *>(out.splat + i);
+#pragma unroll
+            for (int j = 0; j < 4; j++) dst[j] = src[j];
+            const int4 *src64 = reinterpret_cast<const int4 *>(&e);
+            int4 *dst64 = reinterpret_cast<int4 *>(out.splat64 + i);
+#pragma unroll
+            for (int j = 0; j < 4; j++) dst64[j] = src64[j];
+            uint64_t rect;
+            out.tile_count[i] = tile_rect(P.mean2d[0], P.mean2d[1], P.radius, P.valid, a.ntx[v], a.nty[v], rect);
+            out.tile_rect[i] = rect;
+            if (out.valid) out.valid[i] = (uint8_t)P.valid;
+            if (out.depth) out.depth[i] = P.t[2];
+            if (out.radius) out.radius[i] = P.radius;
+            out.depth_key[i] = P.valid ? (uint64_t)__double_as_longlong(P.t[2]) : ~0ull;
+        }
+        const unsigned ballot = __ballot_sync(0xffffffffu, fb);
+        if ((tid & 31) == 0 && ballot) atomicAdd(out.n_skew_fallback, __popc(ballot));
+    }
+}
+
+template <int DEG>
+static int launch_views(const ssg_scene &sc, const MvArgs &a, cudaStream_t st) {
+    constexpr int K3 = 3 * (DEG + 1) * (DEG + 1);
+    const size_t smem = sizeof(float) * (size_t)kMvThreads * mv_sh_stride(K3);
+    static bool attr_dev[64] = {false};  // function attributes are per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !attr_dev[dev]) {
+        cudaFuncSetAttribute(k_preprocess_forward_views<DEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attr_dev[dev] = true;
+    }
+    const unsigned blocks = (unsigned)((sc.n + kMvThreads - 1) / kMvThreads);
+    k_preprocess_forward_views<DEG><<<blocks, kMvThreads, smem, st>>>(sc, a);
+    return check_launch("k_preprocess_forward_views");
+}
+
+}  // namespace ssg
+
+extern "C" int ssg_preprocess_forward_views(const ssg_scene *scene, const ssg_camera *cams,
+                                            const ssg_prim_buffers *outs, int32_t n_views, void *stream) {
+    using namespace ssg;
+    if (!scene || !cams || !outs || n_views < 1 || n_views > SSG_MAX_BATCH_VIEWS) return SSG_ERR_INVALID_ARGUMENT;
+    if (scene->sh_degree < 0 || scene->sh_degree > 3 ||
+        scene->sh_coeffs != (scene->sh_degree + 1) * (scene->sh_degree + 1))
+        return SSG_ERR_INVALID_ARGUMENT;
+    MvArgs a;
+    a.nv = n_views;
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int v = 0; v < n_views; v++) {
+        const ssg_camera &c = cams[v];
+        if (c.width > SSG_MAX_IMAGE_DIM || c.height > SSG_MAX_IMAGE_DIM) return SSG_ERR_DIM_OVERFLOW;
+        if (c.width < 1 || c.height < 1) return SSG_ERR_INVALID_ARGUMENT;
+        const ssg_prim_buffers &o = outs[v];
+        if (!o.splat || !o.splat64 || !o.depth_key || !o.tile_count || !o.tile_rect || !o.n_skew_fallback)
+            return SSG_ERR_INVALID_ARGUMENT;
+        a.cam[v] = c;
+        a.out[v] = o;
+        a.ntx[v] = (c.width + SSG_TILE - 1) / SSG_TILE;
+        a.nty[v] = (c.height + SSG_TILE - 1) / SSG_TILE;
+        cudaError_t e = cudaMemsetAsync(o.n_skew_fallback, 0, sizeof(int32_t), st);
+        if (e != cudaSuccess) { set_error("memset fallback", e); return SSG_ERR_CUDA; }
+    }
+    if (scene->n == 0) return SSG_OK;
+    if (scene->sh_degree > 0 && ((uintptr_t)scene->sh & 15) != 0 && (3 * scene->sh_coeffs) % 4 == 0)
+        return SSG_ERR_INVALID_ARGUMENT;  // 16-byte cp.async needs aligned rows
+    switch (scene->sh_degree) {
+        case 0: return launch_views<0>(*scene, a, st);
+        case 1: return launch_views<1>(*scene, a, st);
+        case 2: return launch_views<2>(*scene, a, st);
+        default: return launch_views<3>(*scene, a, st);
+    }
+}
+
 // Screen records from caller fp64 arrays (the plugin slot's inputs,
 // raster/_core.pyx:169-177): the fp32 splat (+ its alpha band) and the fp64
 // twin the threshold path reads.

@@ -97,17 +97,64 @@ struct Proj {
     double comp, radius;
     double sig[2];
     double eta[3], w[3], u[2], v[2], r;
+    double pe;         // eta . Sigma eta (projection.py:103)
     bool fallback, clip0, clip1;
     double skew[2];
 };
 
-// projection.py:151-210 and _project_eta projection.py:97-123.
-// `mu`, `ls`, `q` fp64; `eta` = beta + dir (evaluated in fp64 from the fp32
-// inputs), logits fp32.
-__device__ __forceinline__ void project_geometry(const ssg_camera &cam, const double mu[3],
-                                                 const double ls[3], const double q4[4],
-                                                 const float logit[2], const double eta[3],
-                                                 Proj &P) {
+// The view-independent half of a primitive's projection: scene.py:66-96
+// (normalised quaternion, rotation, Sigma_world = R S S^T R^T), the
+// opacity sigmoids (kernel_math.py:158-165) and the camera-free part of
+// _project_eta (w = Sigma eta, p = eta . w; projection.py:101-103).  A view
+// batch computes it once per primitive (k_preprocess_forward_views); every
+// operation is the one project_geometry performs, so the bits agree.
+__device__ __forceinline__ void world_geometry(const double ls[3], const double q4[4], const float logit[2],
+                                               const double eta[3], Proj &P) {
+    double nrm = sqrt(q4[0] * q4[0] + q4[1] * q4[1] + q4[2] * q4[2] + q4[3] * q4[3]);
+    double w = q4[0] / nrm, x = q4[1] / nrm, y = q4[2] / nrm, z = q4[3] / nrm;
+    P.qn[0] = w; P.qn[1] = x; P.qn[2] = y; P.qn[3] = z; P.qnorm = nrm;
+    P.Rq[0] = 1 - 2 * (y * y + z * z);
+    P.Rq[1] = 2 * (x * y - w * z);
+    P.Rq[2] = 2 * (x * z + w * y);
+    P.Rq[3] = 2 * (x * y + w * z);
+    P.Rq[4] = 1 - 2 * (x * x + z * z);
+    P.Rq[5] = 2 * (y * z - w * x);
+    P.Rq[6] = 2 * (x * z - w * y);
+    P.Rq[7] = 2 * (y * z + w * x);
+    P.Rq[8] = 1 - 2 * (x * x + y * y);
+#pragma unroll
+    for (int j = 0; j < 3; j++) P.scale[j] = exp(ls[j]);
+    double M[9];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++) M[3 * a + b] = P.Rq[3 * a + b] * P.scale[b];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++)
+            P.Sig[3 * a + b] = M[3 * a] * M[3 * b] + M[3 * a + 1] * M[3 * b + 1] + M[3 * a + 2] * M[3 * b + 2];
+    // kernel_math.py:158-165
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+        double l = (double)logit[j];
+        double sgm;
+        if (l >= 0) sgm = 1.0 / (1.0 + exp(-l));
+        else { double ex = exp(l); sgm = ex / (1.0 + ex); }
+        P.sig[j] = sgm;
+    }
+    // _project_eta (projection.py:97-123), camera-free part
+#pragma unroll
+    for (int j = 0; j < 3; j++) P.eta[j] = eta[j];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+        P.w[a] = P.Sig[3 * a] * eta[0] + P.Sig[3 * a + 1] * eta[1] + P.Sig[3 * a + 2] * eta[2];
+    P.pe = eta[0] * P.w[0] + eta[1] * P.w[1] + eta[2] * P.w[2];
+}
+
+// The camera-dependent half (projection.py:151-210 and the rest of
+// _project_eta, projection.py:102, 104-121); needs world_geometry's fields.
+__device__ __forceinline__ void view_geometry(const ssg_camera &cam, const double mu[3], Proj &P) {
     const double *R = cam.R;
     // projection.py:160 -- numpy/BLAS bits: fma(m2,R2,fma(m1,R1,m0*R0)) + t
 #pragma unroll
@@ -134,31 +181,6 @@ __device__ __forceinline__ void project_geometry(const ssg_camera &cam, const do
         P.T[c] = __dadd_rn(__dmul_rn(P.J00, R[c]), __dmul_rn(P.J02, R[6 + c]));
         P.T[3 + c] = __dadd_rn(__dmul_rn(P.J11, R[3 + c]), __dmul_rn(P.J12, R[6 + c]));
     }
-    // scene.py:66-96
-    double nrm = sqrt(q4[0] * q4[0] + q4[1] * q4[1] + q4[2] * q4[2] + q4[3] * q4[3]);
-    double w = q4[0] / nrm, x = q4[1] / nrm, y = q4[2] / nrm, z = q4[3] / nrm;
-    P.qn[0] = w; P.qn[1] = x; P.qn[2] = y; P.qn[3] = z; P.qnorm = nrm;
-    P.Rq[0] = 1 - 2 * (y * y + z * z);
-    P.Rq[1] = 2 * (x * y - w * z);
-    P.Rq[2] = 2 * (x * z + w * y);
-    P.Rq[3] = 2 * (x * y + w * z);
-    P.Rq[4] = 1 - 2 * (x * x + z * z);
-    P.Rq[5] = 2 * (y * z - w * x);
-    P.Rq[6] = 2 * (x * z - w * y);
-    P.Rq[7] = 2 * (y * z + w * x);
-    P.Rq[8] = 1 - 2 * (x * x + y * y);
-#pragma unroll
-    for (int j = 0; j < 3; j++) P.scale[j] = exp(ls[j]);
-    double M[9];
-#pragma unroll
-    for (int a = 0; a < 3; a++)
-#pragma unroll
-        for (int b = 0; b < 3; b++) M[3 * a + b] = P.Rq[3 * a + b] * P.scale[b];
-#pragma unroll
-    for (int a = 0; a < 3; a++)
-#pragma unroll
-        for (int b = 0; b < 3; b++)
-            P.Sig[3 * a + b] = M[3 * a] * M[3 * b] + M[3 * a + 1] * M[3 * b + 1] + M[3 * a + 2] * M[3 * b + 2];
     double TS[6];
 #pragma unroll
     for (int a = 0; a < 2; a++)
@@ -188,24 +210,9 @@ __device__ __forceinline__ void project_geometry(const ssg_camera &cam, const do
     // projection.py:207 -- unclamped ratio, no contraction
     P.mean2d[0] = __dadd_rn(__dmul_rn(cam.fx, txz), cam.cx);
     P.mean2d[1] = __dadd_rn(__dmul_rn(cam.fy, tyz), cam.cy);
-    // kernel_math.py:158-165
-#pragma unroll
-    for (int j = 0; j < 2; j++) {
-        double l = (double)logit[j];
-        double sgm;
-        if (l >= 0) sgm = 1.0 / (1.0 + exp(-l));
-        else { double ex = exp(l); sgm = ex / (1.0 + ex); }
-        P.sig[j] = sgm;
-    }
-    // _project_eta (projection.py:97-123)
-#pragma unroll
-    for (int j = 0; j < 3; j++) P.eta[j] = eta[j];
-#pragma unroll
-    for (int a = 0; a < 3; a++)
-        P.w[a] = P.Sig[3 * a] * eta[0] + P.Sig[3 * a + 1] * eta[1] + P.Sig[3 * a + 2] * eta[2];
+    // _project_eta (projection.py:102, 104-121)
 #pragma unroll
     for (int a = 0; a < 2; a++) P.u[a] = P.T[3 * a] * P.w[0] + P.T[3 * a + 1] * P.w[1] + P.T[3 * a + 2] * P.w[2];
-    double p = eta[0] * P.w[0] + eta[1] * P.w[1] + eta[2] * P.w[2];
     bool ok = P.det_raw > 1e-300;
     double d = ok ? P.det_raw : 1.0;
     if (ok) {
@@ -218,7 +225,7 @@ __device__ __forceinline__ void project_geometry(const ssg_camera &cam, const do
     }
     P.v[0] = P.inv_raw[0] * P.u[0] + P.inv_raw[1] * P.u[1];
     P.v[1] = P.inv_raw[2] * P.u[0] + P.inv_raw[3] * P.u[1];
-    double qq = p - (P.u[0] * P.v[0] + P.u[1] * P.v[1]);
+    double qq = P.pe - (P.u[0] * P.v[0] + P.u[1] * P.v[1]);
     double radicand = 1.0 + qq;
     P.fallback = (!ok) || (radicand <= 0.0);
     P.r = sqrt(P.fallback ? 1.0 : radicand);
@@ -228,6 +235,17 @@ __device__ __forceinline__ void project_geometry(const ssg_camera &cam, const do
     P.clip1 = fabs(s1) > SSG_BETA_CLAMP;
     P.skew[0] = fmin(fmax(s0, -SSG_BETA_CLAMP), SSG_BETA_CLAMP);
     P.skew[1] = fmin(fmax(s1, -SSG_BETA_CLAMP), SSG_BETA_CLAMP);
+}
+
+// projection.py:151-210 and _project_eta projection.py:97-123.
+// `mu`, `ls`, `q` fp64; `eta` = beta + dir (evaluated in fp64 from the fp32
+// inputs), logits fp32.
+__device__ __forceinline__ void project_geometry(const ssg_camera &cam, const double mu[3],
+                                                 const double ls[3], const double q4[4],
+                                                 const float logit[2], const double eta[3],
+                                                 Proj &P) {
+    world_geometry(ls, q4, logit, eta, P);
+    view_geometry(cam, mu, P);
 }
 
 // ------------------------------------------------------------- tile rect

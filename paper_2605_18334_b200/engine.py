@@ -362,6 +362,75 @@ class Engine:
                     "ssg_preprocess_forward")
         return self._bin(ds.n, W, H, sync)
 
+    # ------------------------------------------------------- view batches
+    _SET_FIELDS = ("splat", "splat64", "depth_key", "tile_count", "tile_rect", "n_fallback")
+
+    def _view_sets(self, k: int) -> list:
+        """k per-view screen-record sets for ssg_preprocess_forward_views
+        (valid / depth / radius are not written by a batch).  Sized like the
+        primary buffers (_prim_n rows), so whichever set is bound satisfies
+        _ensure_prim's invariant."""
+        key = (self._prim_n, k)
+        if getattr(self, "_vsets_key", None) != key:
+            nn = self._prim_n
+            self._vsets = [dict(splat=self._empty((nn, N.SPLAT_BYTES // 8), torch.float64),
+                                splat64=self._empty((nn, N.SPLAT64_BYTES // 8), torch.float64),
+                                depth_key=self._empty((nn,), torch.int64),
+                                tile_count=self._empty((nn,), torch.int32),
+                                tile_rect=self._empty((nn,), torch.int64),
+                                n_fallback=self._empty((1,), torch.int32)) for _ in range(k)]
+            self._vsets_key = key
+        return self._vsets
+
+    @staticmethod
+    def _set_struct(d: dict) -> N.SsgPrimBuffers:
+        p = N.SsgPrimBuffers()
+        p.splat, p.splat64, p.depth_key = _ptr(d["splat"]), _ptr(d["splat64"]), _ptr(d["depth_key"])
+        p.tile_count, p.tile_rect, p.n_skew_fallback = _ptr(d["tile_count"]), _ptr(d["tile_rect"]), _ptr(d["n_fallback"])
+        p.valid = p.depth = p.radius = None
+        return p
+
+    def forward_views(self, ds: DeviceScene, views, s: float = 0.3, out: torch.Tensor | None = None,
+                      sync_first: bool = True) -> torch.Tensor:
+        """Forward-render a batch of views of one scene (same image size)
+        into out[v] (f32 (V,H,W,3)).  The projection runs once per group of
+        up to MAX_BATCH_VIEWS views (ssg_preprocess_forward_views: one pass
+        over the scene, the view-independent projection part computed once),
+        then every view is binned and blended as forward() does.  Outputs
+        equal forward() per view bit for bit.  Only the first view reads M
+        back (sync_first); the caller checks instances() after the batch.
+        Afterwards the engine's screen records are the last view's (a
+        backward(rebin=False) of that view is valid)."""
+        views = list(views)
+        if not views:
+            return torch.empty((0, 0, 0, 3), dtype=torch.float32, device=self.device)
+        W, H = int(views[0].width), int(views[0].height)
+        if any(int(v.width) != W or int(v.height) != H for v in views):
+            raise ValueError("forward_views needs views of one image size")
+        if W > 65535 or H > 65535:
+            raise ValueError("image dimension overflow")
+        if out is None:
+            out = torch.empty((len(views), H, W, 3), dtype=torch.float32, device=self.device)
+        self.finish_exact()
+        self._ensure_prim(ds.n)
+        sc = ds.struct()
+        B = N.MAX_BATCH_VIEWS
+        for b0 in range(0, len(views), B):
+            chunk = views[b0:b0 + B]
+            k = len(chunk)
+            cams = [camera_struct(v, s) for v in chunk]
+            sets = self._view_sets(k)
+            cam_arr = (N.SsgCamera * k)(*cams)
+            out_arr = (N.SsgPrimBuffers * k)(*[self._set_struct(d) for d in sets[:k]])
+            with self._mark("preprocess_fwd_views"):
+                N.check(self.lib.ssg_preprocess_forward_views(ctypes.byref(sc), cam_arr, out_arr, k, self._stream()),
+                        "ssg_preprocess_forward_views")
+            for j, v in enumerate(chunk):
+                for f in self._SET_FIELDS:
+                    setattr(self, f, sets[j][f])
+                self.forward(ds, v, s, color_out=out[b0 + j], sync=sync_first and b0 + j == 0, _cam=cams[j])
+        return out
+
     def project(self, ds: DeviceScene, view: CameraView, s: float = 0.3) -> torch.Tensor:
         """Projection only (projection.py:151-235): the screen radii (n,)
         fp64 of `view` -- what the reference's densify cadence reads for its
@@ -401,7 +470,7 @@ class Engine:
 
     def forward(self, ds: DeviceScene, view: CameraView, s: float = 0.3,
                 color_out: torch.Tensor | None = None, sync: bool = True,
-                defer_exact: bool = False) -> DeviceFrame:
+                defer_exact: bool = False, _cam: N.SsgCamera | None = None) -> DeviceFrame:
         """Project, bin and blend one view.  `color_out` (contiguous f32
         (H,W,3) on this device) receives the image instead of the engine's
         own colour buffer (view batches write straight into their slice).
@@ -411,9 +480,14 @@ class Engine:
         second stream; the frame is complete only after finish_exact() (a
         following backward() overlaps it with its main kernel)."""
         self.finish_exact()
-        cam = camera_struct(view, s)
-        W, H = int(cam.width), int(cam.height)
-        m = self.project_and_bin(ds, cam, sync)
+        if _cam is None:
+            cam = camera_struct(view, s)
+            W, H = int(cam.width), int(cam.height)
+            m = self.project_and_bin(ds, cam, sync)
+        else:  # forward_views: the bound screen records are this view's
+            cam = _cam
+            W, H = int(cam.width), int(cam.height)
+            m = self._bin(ds.n, W, H, sync)
         self._ensure_frame(W, H)
         if color_out is not None and (tuple(color_out.shape) != (H, W, 3) or color_out.dtype != torch.float32
                                       or not color_out.is_contiguous() or color_out.device != self.device):

@@ -5,7 +5,9 @@ The reference renders trajectories one view at a time
 batch of views of one device-resident scene is rendered back to back on one
 GPU, each view writing straight into its slice of a (V,H,W,3) output, and
 `shard_views` splits a batch across ranks (contiguous blocks, views are
-independent, so no collective is needed -- SURVEY.md §8(e)).
+independent, so no collective is needed -- SURVEY.md §8(e)).  On one
+engine the projection of each group of up to 8 views is one pass over the
+scene (Engine.forward_views / ssg_preprocess_forward_views).
 """
 
 from __future__ import annotations
@@ -45,8 +47,8 @@ def render_views(ds: DeviceScene, views, s: float = 0.3, engine=None,
     # so the batch runs without host round trips; one check per engine at the
     # end (an overflowing frame makes the batch re-render synchronised)
     if len(engines) == 1:
-        for i, v in enumerate(views):
-            eng.forward(ds, v, s, color_out=out[i], sync=(i == 0))
+        # one pass over the scene projects up to MAX_BATCH_VIEWS views
+        eng.forward_views(ds, views, s, out=out, sync_first=True)
     else:
         main = torch.cuda.current_stream(eng.device)
         start = torch.cuda.Event()
