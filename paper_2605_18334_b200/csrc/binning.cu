@@ -142,11 +142,34 @@ __device__ __forceinline__ uint32_t warp_exclusive_scan(uint32_t *a, int len, in
     return carry;
 }
 
+// Lanes holding the same bucket b (NB low bits), from NB ballots.  Not
+// __match_any_sync: MATCH.ANY issues on the ADU pipe, which saturates at a
+// small fraction of the issue rate on sm_100 (ncu: adu 59 % of cycles in
+// this kernel with it, profiles/r2_binning.md).  Lanes with v == false
+// belong to no set.
+template <int NB>
+__device__ __forceinline__ uint32_t lane_peers(uint32_t b, bool v) {
+    uint32_t m = __ballot_sync(0xffffffffu, v);
+#pragma unroll
+    for (int k = 0; k < NB; k++) {
+        const uint32_t bb = __ballot_sync(0xffffffffu, (b >> k) & 1u);
+        m &= ((b >> k) & 1u) ? bb : ~bb;
+    }
+    return m;
+}
+
+// bits of the largest bucket index (buckets < 4096 per level)
+static inline int bucket_bits(int nb) {
+    int k = 1;
+    while ((1 << k) < nb) k++;
+    return k;
+}
+
 // Ordered walk of one warp's items [i0, i1): each item covers buckets
 // [b0, b1) and carries a payload.  Items are expanded 32 instances per step
 // (item-major, bucket-minor: the output order); equal buckets inside a step
-// are ranked by lane (match_any), across steps by the warp's cursors scur[].
-template <typename P, typename Load, typename Emit>
+// are ranked by lane (lane_peers), across steps by the warp's cursors scur[].
+template <int NB, typename P, typename Load, typename Emit>
 __device__ __forceinline__ void cs_walk(int64_t i0, int64_t i1, int lane, uint32_t *scur, Load &&load, Emit &&emit) {
     const uint32_t lt = radix::lanemask_lt();
     for (int64_t a = i0; a < i1; a += 32) {
@@ -180,7 +203,7 @@ __device__ __forceinline__ void cs_walk(int64_t i0, int64_t i1, int lane, uint32
             }
             const bool v = g < tot;
             const int b = bj + (int)(g - pj);
-            const uint32_t peers = __match_any_sync(0xffffffffu, v ? (uint32_t)b : 0xffffffffu);
+            const uint32_t peers = lane_peers<NB>((uint32_t)b, v);
             const uint32_t base = v ? scur[b] : 0u;
             __syncwarp();
             if (v && (peers & lt) == 0) scur[b] = base + (uint32_t)__popc(peers);
@@ -317,6 +340,7 @@ __global__ void __launch_bounds__(1024) k_cs1_rowstart(const uint32_t *__restric
 }
 
 // level 1, scatter: row segments (prim | x0 << 32 | x1 << 48) into per-row lists
+template <int NB>
 __global__ void __launch_bounds__(32 * kCsWarps) k_cs1_scatter(const uint32_t *__restrict__ order,
                                                                const uint32_t *__restrict__ count,
                                                                const uint64_t *__restrict__ rect, int64_t n,
@@ -342,7 +366,7 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs1_scatter(const uint32_t *_
         [&](int y) { return row_start[y] + cnt1[(size_t)y * nch1 + c]; });
     const bool staged = total <= (uint32_t)kCsStage;
     const int64_t r1 = min(n, (c + 1) * kCsC1);
-    cs_walk<uint64_t>(
+    cs_walk<NB, uint64_t>(
         c * kCsC1, r1, lane, scur,
         [&](int64_t r, int &b0, int &b1, uint64_t &pay) {
             const uint32_t p = order[r];
@@ -462,6 +486,7 @@ __global__ void __launch_bounds__(1024) k_cs2_tilestart(const uint32_t *__restri
 }
 
 // level 2, scatter: per-tile instance lists (inst_prim, inst_tile)
+template <int NB>
 __global__ void __launch_bounds__(32 * kCsWarps) k_cs2_scatter(const uint64_t *__restrict__ rowlist,
                                                                const uint32_t *__restrict__ row_start,
                                                                const uint32_t *__restrict__ chunk_base,
@@ -493,7 +518,7 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_cs2_scatter(const uint64_t *_
             [&](int x) { return tile_start[trow + x] + blk[(size_t)x * nk + k]; });
         const bool staged = total <= (uint32_t)kCsStage;
         const uint32_t i0 = row_start[y] + k * kCsC2, i1 = min(min(row_start[y + 1], i0 + kCsC2), cap);
-        cs_walk<uint32_t>(
+        cs_walk<NB, uint32_t>(
             i0, i1, lane, scur,
             [&](int64_t i, int &b0, int &b1, uint32_t &pay) {
                 const uint64_t seg = rowlist[i];
@@ -584,6 +609,11 @@ extern "C" int ssg_bin_prepare(int64_t n, const ssg_prim_buffers *prim, const ss
     return check_launch("ssg_bin_prepare");
 }
 
+#define CS_KERNELS(K)                                                                                       \
+    (const void *)K<1>, (const void *)K<2>, (const void *)K<3>, (const void *)K<4>, (const void *)K<5>,         \
+        (const void *)K<6>, (const void *)K<7>, (const void *)K<8>, (const void *)K<9>, (const void *)K<10>,    \
+        (const void *)K<11>, (const void *)K<12>
+
 extern "C" int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t height,
                               const ssg_prim_buffers *prim, const ssg_bin_buffers *bins, void *stream) {
     using namespace ssg;
@@ -615,10 +645,11 @@ extern "C" int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t heigh
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SSG_ERR_CUDA;
     if (!attr_dev[dev]) {
         const int mx = (int)(kCsWarps * cs_warp_smem<uint64_t>(4096));
-        cudaError_t e = cudaFuncSetAttribute(k_cs1_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(k_cs2_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(k_cs1_count, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(k_cs2_count, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        const void *fs[] = {CS_KERNELS(k_cs1_scatter), CS_KERNELS(k_cs2_scatter), (const void *)k_cs1_count,
+                            (const void *)k_cs2_count};
+        cudaError_t e = cudaSuccess;
+        for (const void *f : fs)
+            if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         if (e != cudaSuccess) { set_error("cudaFuncSetAttribute(binning)", e); return SSG_ERR_CUDA; }
         attr_dev[dev] = true;
     }
@@ -632,15 +663,34 @@ extern "C" int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t heigh
     const uint32_t cap = (uint32_t)(bins->capacity > 0 ? bins->capacity : 0);
     k_cs1_rowstart<<<1, 1024, 0, st>>>(row_total, nty, (uint32_t)L.max_ch2, row_start, chunk_base, ctl);
     if (n > 0)
-        k_cs1_scatter<<<g1, 32 * kCsWarps, sm1, st>>>(bins->depth_order, prim->tile_count, prim->tile_rect, n,
-                                                      L.nch1, nty, cnt1, row_total, row_start, rowlist, cap);
+        switch (bucket_bits(nty)) {
+#define SSG_CS1(B)                                                                                              \
+    case B:                                                                                                     \
+        k_cs1_scatter<B><<<g1, 32 * kCsWarps, sm1, st>>>(bins->depth_order, prim->tile_count, prim->tile_rect, \
+                                                         n, L.nch1, nty, cnt1, row_total, row_start, rowlist, cap); \
+        break;
+            SSG_CS1(1) SSG_CS1(2) SSG_CS1(3) SSG_CS1(4) SSG_CS1(5) SSG_CS1(6) SSG_CS1(7) SSG_CS1(8) SSG_CS1(9)
+            SSG_CS1(10) SSG_CS1(11) SSG_CS1(12)
+#undef SSG_CS1
+            default: return SSG_ERR_INVALID_ARGUMENT;
+        }
     // level 2: per-tile lists of each row
     k_cs2_count<<<g2, 32 * kCsWarps, smc2, st>>>(rowlist, row_start, chunk_base, ctl, ntx, nty, cnt2, cap);
     k_cs2_tilescan<<<(unsigned)(((int64_t)n_tiles * 32 + 255) / 256), 256, 0, st>>>(cnt2, chunk_base, ntx, nty,
                                                                                     tile_total);
     k_cs2_tilestart<<<1, 1024, 0, st>>>(tile_total, n_tiles, cap, tile_start, bins->ranges);
-    k_cs2_scatter<<<g2, 32 * kCsWarps, sm2, st>>>(rowlist, row_start, chunk_base, ctl, cnt2, tile_total, tile_start,
-                                                  ntx, nty, bins->inst_prim, bins->inst_tile, cap);
+    switch (bucket_bits(ntx)) {
+#define SSG_CS2(B)                                                                                              \
+    case B:                                                                                                     \
+        k_cs2_scatter<B><<<g2, 32 * kCsWarps, sm2, st>>>(rowlist, row_start, chunk_base, ctl, cnt2, tile_total, \
+                                                         tile_start, ntx, nty, bins->inst_prim, bins->inst_tile,  \
+                                                         cap);                                                   \
+        break;
+        SSG_CS2(1) SSG_CS2(2) SSG_CS2(3) SSG_CS2(4) SSG_CS2(5) SSG_CS2(6) SSG_CS2(7) SSG_CS2(8) SSG_CS2(9)
+        SSG_CS2(10) SSG_CS2(11) SSG_CS2(12)
+#undef SSG_CS2
+        default: return SSG_ERR_INVALID_ARGUMENT;
+    }
     return check_launch("ssg_bin_finish");
 }
 
