@@ -308,6 +308,9 @@ def main():
     ap.add_argument("--lanes", type=int, default=1,
                     help="config 4: engines on their own streams (views overlap); measured slower at 2-4 "
                          "(668 vs 720 views/s): the cooperative depth sort needs every SM free")
+    ap.add_argument("--buckets", type=int, default=None,
+                    help="config 5: primitive ranges of the overlapped gradient all-reduce (default 4 at N > 1, "
+                         "1 at N = 1)")
     ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=2,
                     help="BASELINE.json config: 2 (default, the headline), 3 (50%% skew-free), "
                          "4 (3M, 64-view forward batch sharded over ranks), 5 (2M view-parallel training)")

@@ -229,7 +229,8 @@ def config5(args, rank, world, local):
     adam = DeviceAdam(ds)
     # pipelined steps: no host read-back inside a step (the finite-loss branch
     # and the instance check are a device flag, resolved at the next step)
-    tr = Trainer(eng, ds, adam, pipelined=True)
+    buckets = args.buckets if getattr(args, "buckets", None) else (4 if world > 1 else 1)
+    tr = Trainer(eng, ds, adam, pipelined=True, buckets=buckets)
     step_no = [0]
 
     def step(target=None):
@@ -268,6 +269,32 @@ def config5(args, rank, world, local):
         float(loss.item())
         e2e_t.append(time.perf_counter() - t0)
     e2e_s = max_over_ranks(statistics.median(e2e_t))
+    # the post-blend tail (projection backward, all-reduce, statistics,
+    # regularizer, Adam) from separate untimed steps: what the bucketed
+    # all-reduce can hide its communication under
+    tr.tail_events = []
+    for _ in range(3):
+        step()
+    tr.flush()
+    torch.cuda.synchronize()
+    tail_ms = statistics.median(a.elapsed_time(b) for a, b in tr.tail_events)
+    tr.tail_events = None
+    grad_bytes = int(eng.g_flat.numel() * 4 + eng.g_z.numel() * 4)
+    busbw = 725e9  # 8-rank all-reduce bus bandwidth at 1 GiB, /opt/skills/guides/B200_PROFILING.md
+    model = {}
+    for nr in (2, 4, 8):
+        comm = grad_bytes * 2 * (nr - 1) / nr / busbw * 1e3
+        # ranges of equal size: range i's all-reduce overlaps the later ranges'
+        # projection backward and the earlier ranges' update, so the step
+        # grows by max(0, C - tail (B-1)/B) with B = 4
+        exp4 = max(0.0, comm - tail_ms * 3 / 4)
+        model[str(nr)] = {"comm_ms": comm, "exposed_ms_unbucketed": comm, "exposed_ms_4_buckets": exp4,
+                          "step_frac_unbucketed": comm / (ms + comm), "step_frac_4_buckets": exp4 / (ms + exp4)}
+    allreduce = {"bytes_per_rank": grad_bytes, "buckets": buckets, "tail_ms": tail_ms,
+                 "model_busbw_gbs": busbw / 1e9, "model": model,
+                 "note": "N = 1 measures the tail the communication can hide under; comm_ms = bytes x 2(N-1)/N / "
+                         "bus bandwidth (not measured here: one GPU per lease)" if world == 1 else
+                         "measured: ms_per_step includes the bucketed all-reduce"}
     result = {
         "metric": "config 5: view-parallel training step, 2M skew Gaussians @1297x840, views/s trained",
         "value": world * 1000.0 / ms, "unit": "views/s", "n_gpus": world, "steps": args.steps,
@@ -280,6 +307,7 @@ def config5(args, rank, world, local):
                                "finite check and instance check are a device flag resolved at the next step",
                    "parallelism": f"view-parallel x{world}, NCCL all-reduce SUM of {N5 * 65 * 4 / 1e6:.0f} MB "
                                   "packed gradients + MAX of g_z"},
+        "allreduce": allreduce,
         "clocks": clk,
         "e2e": {"value": world / e2e_s, "unit": "views/s", "h2d_bytes_per_step": H4 * W4 * 12,
                 "d2h_bytes_per_step": 4, "path": "training_step with the target image copied from pinned "

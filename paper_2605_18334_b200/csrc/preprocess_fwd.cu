@@ -157,6 +157,9 @@ namespace ssg {
 // single-view kernel's.  valid / depth / radius may be NULL per view
 // (introspection-only outputs a throughput batch skips).
 constexpr int kMvThreads = 128;
+#ifndef SSG_MV_MINB
+#define SSG_MV_MINB 1
+#endif
 
 // padded smem row stride (floats) of a 3K-float SH row: conflict-free
 // LDS.128 when 3K % 4 == 0 (an odd number of 16-byte units per row), an odd
@@ -183,7 +186,7 @@ struct MvArgs {
 };
 
 template <int DEG>
-__global__ void __launch_bounds__(kMvThreads)
+__global__ void __launch_bounds__(kMvThreads, SSG_MV_MINB)
 k_preprocess_forward_views(ssg_scene sc, const __grid_constant__ MvArgs a) {
     constexpr int K = (DEG + 1) * (DEG + 1), K3 = 3 * K, S = mv_sh_stride(K3);
     extern __shared__ __align__(16) float s_sh[];  // [kMvThreads][S]

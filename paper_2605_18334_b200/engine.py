@@ -90,6 +90,13 @@ class DeviceScene:
                    up(scene.opacity_logits, (n, 2), True), up(scene.beta, (n, 3), True),
                    up(scene.dir, (n, 3), True), scene.background, deg)
 
+    def rows(self, a: int, b: int) -> "DeviceScene":
+        """Primitives [a, b) as a scene of views into this one's storage
+        (row slices: the kernels see offset pointers)."""
+        return DeviceScene(self.mu[a:b], self.log_scale[a:b], self.rot[a:b], self.sh[a:b],
+                           self.opacity_logits[a:b], self.beta[a:b], self.dir[a:b], self.background,
+                           self.sh_degree)
+
     def struct(self) -> N.SsgScene:
         s = N.SsgScene()
         s.n, s.sh_degree, s.sh_coeffs = self.n, self.sh_degree, self.K
@@ -124,6 +131,22 @@ class DeviceGrads:
     d_eta: torch.Tensor       # d_beta == d_dir (projection.py:365-366)
     g_uv: torch.Tensor
     g_z: torch.Tensor
+
+    SUM_FIELDS = ("d_mu", "d_log_scale", "d_rot", "d_sh", "d_opacity_logits", "d_eta", "g_uv")
+
+    def rows(self, a: int, b: int) -> "DeviceGrads":
+        """Primitives [a, b): row slices of every field (flat stays whole)."""
+        return DeviceGrads(self.flat, self.screen[a:b], self.d_mu[a:b], self.d_log_scale[a:b], self.d_rot[a:b],
+                           self.d_sh[a:b], self.d_opacity_logits[a:b], self.d_eta[a:b], self.g_uv[a:b],
+                           self.g_z[a:b])
+
+    def struct(self, d_beta: torch.Tensor | None = None) -> N.SsgGradBuffers:
+        g = N.SsgGradBuffers()
+        g.screen, g.d_mu, g.d_log_scale = _ptr(self.screen), _ptr(self.d_mu), _ptr(self.d_log_scale)
+        g.d_rot, g.d_sh, g.d_opacity_logits = _ptr(self.d_rot), _ptr(self.d_sh), _ptr(self.d_opacity_logits)
+        g.d_eta, g.g_uv, g.g_z = _ptr(self.d_eta), _ptr(self.g_uv), _ptr(self.g_z)
+        g.d_beta = _ptr(d_beta)
+        return g
 
 
 class Engine:
@@ -544,13 +567,18 @@ class Engine:
 
     def backward(self, ds: DeviceScene, view: CameraView, s: float, final_T: torch.Tensor,
                  last_idx: torch.Tensor, dL: torch.Tensor, rebin: bool = True,
-                 expect_m: int | None = None, deterministic: bool | None = None) -> DeviceGrads:
+                 expect_m: int | None = None, deterministic: bool | None = None,
+                 projection: bool = True) -> DeviceGrads:
         """Blend backward + projection backward.  With rebin=True the
         projection and binning are recomputed first (raster/backward.py:49-53)
         and `expect_m` is checked against the new instance count.
         deterministic (default: self.deterministic): bitwise-repeatable
         gradients via ssg_blend_backward_det -- per-(primitive,
-        tile) sums combined in a fixed order, no atomics."""
+        tile) sums combined in a fixed order, no atomics.
+        projection=False stops after the screen-space gradients (and the
+        zero-fill of the parameter gradients): the caller runs
+        projection_backward itself, e.g. over primitive ranges whose
+        all-reduce overlaps the next range (train.Trainer buckets)."""
         cam = camera_struct(view, s)
         W, H = int(cam.width), int(cam.height)
         if rebin:
@@ -631,14 +659,28 @@ class Engine:
                 main.wait_event(done)
                 self._exact_pending = None
         main.wait_event(ev_zero)
-        sc = ds.struct()
-        with self._mark("preprocess_bwd"):
-            N.check(self.lib.ssg_preprocess_backward_ex(ctypes.byref(sc), ctypes.byref(cam), ctypes.byref(gs),
-                                                        N.SSG_PREP_BWD_ACTIVE_ONLY, st),
-                    "ssg_preprocess_backward_ex")
         n = ds.n
-        return DeviceGrads(self.g_flat, self.g_screen[:n], self.g_mu[:n], self.g_log_scale[:n], self.g_rot[:n],
-                           self.g_sh[:n], self.g_logits[:n], self.g_eta[:n], self.g_uv[:n], self.g_z[:n])
+        grads = DeviceGrads(self.g_flat, self.g_screen[:n], self.g_mu[:n], self.g_log_scale[:n], self.g_rot[:n],
+                            self.g_sh[:n], self.g_logits[:n], self.g_eta[:n], self.g_uv[:n], self.g_z[:n])
+        if projection:
+            with self._mark("preprocess_bwd"):
+                self.projection_backward(ds, cam, grads)
+        return grads
+
+    def projection_backward(self, ds: DeviceScene, cam: N.SsgCamera, grads: DeviceGrads,
+                            rows: tuple | None = None) -> None:
+        """projection_backward (projection.py:255-379) for primitives
+        [a, b) = rows (default: all), from the screen-space gradients of
+        `grads` into its parameter fields; only primitives with a non-zero
+        screen gradient are visited (the rest were zero-filled by
+        backward()).  Range bounds on 128-primitive multiples keep every
+        row 16-byte aligned."""
+        if rows is not None:
+            ds, grads = ds.rows(*rows), grads.rows(*rows)
+        sc, gs = ds.struct(), grads.struct()
+        N.check(self.lib.ssg_preprocess_backward_ex(ctypes.byref(sc), ctypes.byref(cam), ctypes.byref(gs),
+                                                    N.SSG_PREP_BWD_ACTIVE_ONLY, self._stream()),
+                "ssg_preprocess_backward_ex")
 
     def redo_pixels(self) -> int:
         """Pixels of the last forward decided on the exact fp64 path

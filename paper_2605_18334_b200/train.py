@@ -33,7 +33,7 @@ import torch
 import torch.distributed as dist
 
 from . import _native as N
-from .engine import DeviceGrads, DeviceScene, Engine
+from .engine import DeviceGrads, DeviceScene, Engine, camera_struct
 
 SUM_FIELDS = ("d_mu", "d_log_scale", "d_rot", "d_sh", "d_opacity_logits", "d_eta", "g_uv")
 
@@ -110,6 +110,79 @@ def allreduce_gradients(grads: DeviceGrads, group=None) -> None:
     dist.all_reduce(grads.g_z, op=dist.ReduceOp.MAX, group=group)
 
 
+def bucket_bounds(n: int, buckets: int, align: int = 128) -> list:
+    """[a, b) primitive ranges covering [0, n): `buckets` near-equal parts
+    with inner bounds on `align` multiples (keeps every field row of a
+    range 16-byte aligned and K8's 128-primitive warp groups whole)."""
+    buckets = max(1, int(buckets))
+    cuts = [0]
+    for i in range(1, buckets):
+        c = (n * i // buckets) // align * align
+        if c > cuts[-1]:
+            cuts.append(c)
+    if n > cuts[-1] or not n:
+        cuts.append(n)
+    return [(cuts[i], cuts[i + 1]) for i in range(len(cuts) - 1)]
+
+
+def bucketed_allreduce(grads: DeviceGrads, bounds: list, group=None, produce=None, consume=None,
+                       comm_stream=None) -> None:
+    """Per primitive range [a, b) of `bounds`, in order: produce(a, b)
+    writes the range's gradients (compute stream), one grouped SUM
+    all-reduce of the range's rows of every SUM field (DeviceGrads.
+    SUM_FIELDS) plus a MAX all-reduce of its g_z rows runs on
+    `comm_stream`, then consume(a, b) uses the reduced rows (compute stream).
+    On CUDA every produce is queued first, so range i's all-reduce overlaps
+    the production of the later ranges, and consume(i) overlaps the
+    all-reduce of range i + 1 (the streams are ordered by events; NCCL's
+    own stream waits for the issuing stream).  Without a comm stream (CPU /
+    gloo, or one process) the same calls run in program order.  The result
+    equals allreduce_gradients + one consume over everything: the reduced
+    values of a row do not depend on how rows are grouped."""
+    world = _world(group)
+    cuda = comm_stream is not None and grads.g_z.is_cuda
+
+    def reduce_range(a, b):
+        if world == 1:
+            return
+        g = grads.rows(a, b)
+        with dist._coalescing_manager(group, grads.g_z.device if cuda else None, async_ops=True) as cm:
+            for f in DeviceGrads.SUM_FIELDS:
+                dist.all_reduce(getattr(g, f), op=dist.ReduceOp.SUM, group=group)
+        cm.wait()
+        dist.all_reduce(g.g_z, op=dist.ReduceOp.MAX, group=group)
+
+    if not cuda:
+        for a, b in bounds:
+            if produce:
+                produce(a, b)
+        for a, b in bounds:
+            reduce_range(a, b)
+            if consume:
+                consume(a, b)
+        return
+    main = torch.cuda.current_stream(grads.g_z.device)
+    produced = []
+    for a, b in bounds:
+        if produce:
+            produce(a, b)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        produced.append(ev)
+    reduced = []
+    with torch.cuda.stream(comm_stream):
+        for (a, b), ev in zip(bounds, produced):
+            comm_stream.wait_event(ev)
+            reduce_range(a, b)
+            done = torch.cuda.Event()
+            done.record(comm_stream)
+            reduced.append(done)
+    for (a, b), ev in zip(bounds, reduced):
+        main.wait_event(ev)
+        if consume:
+            consume(a, b)
+
+
 class ImageLoss:
     """Device image loss + pixel gradient (losses.py:103-113) for one image
     size; the value is read lazily (value() synchronises)."""
@@ -154,18 +227,22 @@ class IntervalStats:
         self.mu_sum = torch.zeros((n, 3), dtype=torch.float64, device=device)
         self.steps = 0
 
-    def add(self, grads: DeviceGrads, views: int = 1, skip: torch.Tensor | None = None):
+    def add(self, grads: DeviceGrads, views: int = 1, skip: torch.Tensor | None = None, rows: tuple | None = None):
         """`skip`: optional device int32 flag; nonzero = this step adds nothing
-        (the caller then takes the `views` back, see Trainer)."""
+        (the caller then takes the `views` back, see Trainer).  `rows`
+        = (a, b): only primitives [a, b) (the step's view count is then
+        added by the caller, once)."""
         n = self.uv_sum.numel()
         if grads.g_uv.numel() != n:  # trainer.py:146 starts a new interval after densify
             raise ValueError(f"IntervalStats covers {n} primitives, gradients {grads.g_uv.numel()}")
-        N.check(N.lib().ssg_interval_stats_add_ex(n, grads.g_uv.data_ptr(), grads.g_z.data_ptr(),
-                                                  grads.d_mu.data_ptr(), self.uv_sum.data_ptr(),
-                                                  self.z_max.data_ptr(), self.mu_sum.data_ptr(),
+        a, b = rows if rows is not None else (0, n)
+        N.check(N.lib().ssg_interval_stats_add_ex(b - a, grads.g_uv[a:b].data_ptr(), grads.g_z[a:b].data_ptr(),
+                                                  grads.d_mu[a:b].data_ptr(), self.uv_sum[a:b].data_ptr(),
+                                                  self.z_max[a:b].data_ptr(), self.mu_sum[a:b].data_ptr(),
                                                   skip.data_ptr() if skip is not None else None,
                                                   _stream(self.uv_sum.device)), "ssg_interval_stats_add_ex")
-        self.steps += views
+        if rows is None:
+            self.steps += views
 
     def bundle(self):
         tr = getattr(self, "_trainer", None)
@@ -199,29 +276,37 @@ class DeviceAdam:
         self.n_skipped_dev = torch.zeros(1, dtype=torch.int32, device=dev)  # accumulated, adam.py:79
 
     def step(self, grads, iteration: int = 0, d_beta: torch.Tensor | None = None,
-             skip: torch.Tensor | None = None) -> None:
+             skip: torch.Tensor | None = None, rows: tuple | None = None, advance: bool = True) -> None:
         """adam.py:71-97; `d_beta` (d_eta + regularizer) drives beta, d_eta
         drives dir.  `skip`: optional device int32 flag, nonzero = the step is
-        skipped on the device (the caller then takes `t` back, see Trainer)."""
+        skipped on the device (the caller then takes `t` back, see Trainer).
+        `rows` = (a, b): update primitives [a, b) only (d_beta then covers
+        the same rows); advance=False keeps the step count (the later ranges
+        of one step: the caller advances once)."""
         ds, cfg = self.ds, self.cfg
         if ds.n == 0:
             return
-        self.t += 1
+        if advance:
+            self.t += 1
+        a, b = rows if rows is not None else (0, ds.n)
+        if b <= a:
+            return
+        sub = ds.rows(a, b)
         p = N.SsgParams()
-        p.n, p.sh_degree, p.sh_coeffs = ds.n, ds.sh_degree, ds.K
-        p.mu, p.log_scale, p.rot = ds.mu.data_ptr(), ds.log_scale.data_ptr(), ds.rot.data_ptr()
-        p.sh, p.opacity_logits = ds.sh.data_ptr(), ds.opacity_logits.data_ptr()
-        p.beta, p.dir = ds.beta.data_ptr(), ds.dir.data_ptr()
-        g = N.SsgGradBuffers()
-        g.d_mu, g.d_log_scale, g.d_rot = grads.d_mu.data_ptr(), grads.d_log_scale.data_ptr(), grads.d_rot.data_ptr()
-        g.d_sh, g.d_opacity_logits = grads.d_sh.data_ptr(), grads.d_opacity_logits.data_ptr()
-        g.d_eta = grads.d_eta.data_ptr()
+        p.n, p.sh_degree, p.sh_coeffs = b - a, ds.sh_degree, ds.K
+        p.mu, p.log_scale, p.rot = sub.mu.data_ptr(), sub.log_scale.data_ptr(), sub.rot.data_ptr()
+        p.sh, p.opacity_logits = sub.sh.data_ptr(), sub.opacity_logits.data_ptr()
+        p.beta, p.dir = sub.beta.data_ptr(), sub.dir.data_ptr()
+        g = N.SsgGradBuffers()  # any object with the gradient fields (row slices [a, b))
+        g.d_mu, g.d_log_scale = grads.d_mu[a:b].data_ptr(), grads.d_log_scale[a:b].data_ptr()
+        g.d_rot, g.d_sh = grads.d_rot[a:b].data_ptr(), grads.d_sh[a:b].data_ptr()
+        g.d_opacity_logits, g.d_eta = grads.d_opacity_logits[a:b].data_ptr(), grads.d_eta[a:b].data_ptr()
         g.d_beta = d_beta.data_ptr() if d_beta is not None else None
         s = N.SsgAdamState()
         for f in self.FIELDS:
-            setattr(s, "m_" + f, self.m[f].data_ptr())
-            setattr(s, "v_" + f, self.v[f].data_ptr())
-        s.row_ok, s.n_skipped = self.row_ok.data_ptr(), self.n_skipped_dev.data_ptr()
+            setattr(s, "m_" + f, self.m[f][a:b].data_ptr())
+            setattr(s, "v_" + f, self.v[f][a:b].data_ptr())
+        s.row_ok, s.n_skipped = self.row_ok[a:b].data_ptr(), self.n_skipped_dev.data_ptr()
         hp = N.SsgAdamHparams()
         hp.t = self.t
         hp.lr_mu, hp.lr_scale, hp.lr_rot = cfg.position_lr_at(iteration), cfg.lr_scale, cfg.lr_rot
@@ -253,8 +338,16 @@ class Trainer:
     last step) between steps."""
 
     def __init__(self, eng: Engine, ds: DeviceScene, adam: DeviceAdam, cfg: TrainConfig | None = None,
-                 pipelined: bool = False):
+                 pipelined: bool = False, buckets: int = 1):
         self.eng, self.ds, self.adam = eng, ds, adam
+        # buckets > 1: the projection backward, gradient all-reduce and the
+        # update run per primitive range, the all-reduce of range i on a
+        # communication stream under the projection backward of the later
+        # ranges and the update of the earlier ones (bucketed_allreduce);
+        # parameters are the same as with one bucket
+        self.buckets = max(1, int(buckets))
+        self._comm = None
+        self.tail_events = None  # list: (start, end) CUDA events of each step's post-blend tail
         self.cfg = cfg or adam.cfg
         self._loss = {}
         self.d_beta = None
@@ -322,16 +415,9 @@ class Trainer:
         self._skip_host.copy_(self._skip_dev, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
-        grads = eng.backward(ds, view, s, f.final_T, f.last_idx, dL, rebin=False)
-        allreduce_gradients(grads, group)
         if stats is not None:
             stats._trainer = self  # bundle() flushes first
-            stats.add(grads, views=_world(group), skip=self._skip_dev)
-        N.check(N.lib().ssg_regularize(n, ds.beta.data_ptr(), ds.opacity_logits.data_ptr(), grads.d_eta.data_ptr(),
-                                       cfg.lambda_beta_reg, cfg.lambda_opacity_reg, self.d_beta.data_ptr(),
-                                       grads.d_opacity_logits.data_ptr(), lossfn.sums.data_ptr(),
-                                       _stream(eng.device)), "ssg_regularize")
-        self.adam.step(grads, iteration, d_beta=self.d_beta[:n], skip=self._skip_dev)
+        self._update(view, s, f, dL, iteration, stats, group, self._skip_dev, lossfn)
         loss = lossfn.value_tensor()
         self._pending = (ev, (view, target, iteration, stats, s, group), loss)
         return loss, f
@@ -371,16 +457,68 @@ class Trainer:
             bad = any_rank(not math.isfinite(loss), group, eng.device)
             if bad:  # fit2d.py:70-71: no backward, no update
                 return v, f
-        grads = eng.backward(ds, view, s, f.final_T, f.last_idx, dL, rebin=False)
-        allreduce_gradients(grads, group)
-        if stats is not None:
-            stats.add(grads, views=_world(group))
-        N.check(N.lib().ssg_regularize(n, ds.beta.data_ptr(), ds.opacity_logits.data_ptr(), grads.d_eta.data_ptr(),
-                                       cfg.lambda_beta_reg, cfg.lambda_opacity_reg, self.d_beta.data_ptr(),
-                                       grads.d_opacity_logits.data_ptr(), lossfn.sums.data_ptr(),
-                                       _stream(eng.device)), "ssg_regularize")
-        self.adam.step(grads, iteration, d_beta=self.d_beta[:n])
+        self._update(view, s, f, dL, iteration, stats, group, None, lossfn)
         return lossfn.value_tensor(), f
+
+    def _comm_stream(self) -> torch.cuda.Stream:
+        if self._comm is None:
+            self._comm = torch.cuda.Stream(self.eng.device)
+        return self._comm
+
+    def _regularize(self, grads: DeviceGrads, rows: tuple, sums: torch.Tensor) -> None:
+        """losses.py:116-136 gradients for primitives [a, b): d_beta = d_eta
+        + the beta penalty's, d_logits += the opacity penalty's (after the
+        all-reduce: the penalty is added once, not per rank)."""
+        a, b = rows
+        ds, cfg = self.ds, self.cfg
+        N.check(N.lib().ssg_regularize(b - a, ds.beta[a:b].data_ptr(), ds.opacity_logits[a:b].data_ptr(),
+                                       grads.d_eta[a:b].data_ptr(), cfg.lambda_beta_reg, cfg.lambda_opacity_reg,
+                                       self.d_beta[a:b].data_ptr(), grads.d_opacity_logits[a:b].data_ptr(),
+                                       sums.data_ptr(), _stream(self.eng.device)), "ssg_regularize")
+
+    def _update(self, view, s, f, dL, iteration, stats, group, skip, lossfn) -> None:
+        """Backward, gradient all-reduce, interval statistics, regularizer
+        and Adam (fit2d.py:72-78, trainer.py:127-129 for the view-parallel
+        sum), in one piece or per primitive bucket."""
+        eng, ds = self.eng, self.ds
+        n = ds.n
+        world = _world(group)
+        grads = eng.backward(ds, view, s, f.final_T, f.last_idx, dL, rebin=False, projection=False)
+        cam = camera_struct(view, s)
+        tail = None
+        if self.tail_events is not None:  # the post-blend tail: projection backward .. Adam
+            tail = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            tail[0].record()
+            self.tail_events.append(tail)
+        if self.buckets <= 1:
+            eng.projection_backward(ds, cam, grads)
+            allreduce_gradients(grads, group)
+            if stats is not None:
+                stats.add(grads, views=world, skip=skip)
+            self._regularize(grads, (0, n), lossfn.sums)
+            self.adam.step(grads, iteration, d_beta=self.d_beta[:n], skip=skip)
+            if tail is not None:
+                tail[1].record()
+            return
+        if stats is not None:
+            stats.steps += world
+        self.adam.t += 1
+        if getattr(self, "_reg_sums", None) is None:  # the penalty value stays in lossfn.sums
+            self._reg_sums = torch.zeros(3, dtype=torch.float64, device=eng.device)
+
+        def produce(a, b):
+            eng.projection_backward(ds, cam, grads, rows=(a, b))
+
+        def consume(a, b):
+            if stats is not None:
+                stats.add(grads, skip=skip, rows=(a, b))
+            self._regularize(grads, (a, b), self._reg_sums)
+            self.adam.step(grads, iteration, d_beta=self.d_beta[a:b], skip=skip, rows=(a, b), advance=False)
+
+        bucketed_allreduce(grads, bucket_bounds(n, self.buckets), group, produce, consume,
+                           comm_stream=self._comm_stream() if world > 1 else None)
+        if tail is not None:
+            tail[1].record()
 
 
 def training_step(eng: Engine, ds: DeviceScene, adam: DeviceAdam, view, target: torch.Tensor,

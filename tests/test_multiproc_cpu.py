@@ -107,3 +107,77 @@ def test_any_rank_decision_world2():
         p.join(timeout=60)
     assert sorted(r[0] for r in res) == [0, 1]
     assert all(r[1] is True and r[2] is False for r in res)
+
+
+def _worker_bucketed(rank, world, port, q, n, buckets):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2605_18334_b200.train import bucket_bounds, bucketed_allreduce
+    src = _grads(rank, n=n)
+    g = _grads(rank, n=n)
+    g.flat.zero_()
+    g.g_z.zero_()
+    order = []
+
+    def produce(a, b):  # a range's gradients appear only at its produce step
+        order.append(("p", a, b))
+        for f in DeviceGrads.SUM_FIELDS + ("g_z",):
+            getattr(g, f)[a:b] = getattr(src, f)[a:b]
+
+    seen = {}
+
+    def consume(a, b):  # a consumer sees its rows fully reduced
+        order.append(("c", a, b))
+        seen[(a, b)] = (g.d_sh[a:b].clone(), g.g_z[a:b].clone())
+
+    bounds = bucket_bounds(n, buckets, align=8)
+    bucketed_allreduce(g, bounds, produce=produce, consume=consume)
+    q.put((rank, bounds, order, g.flat.clone(), g.g_z.clone(), seen))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,buckets", [(37, 3), (64, 1), (200, 4)])
+def test_bucketed_allreduce_world2(n, buckets):
+    """bucketed_allreduce (config 5's overlapped all-reduce, train.py):
+    every range is produced before its reduction, consumed after it, in
+    range order, and the result equals one all-reduce of everything."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_bucketed, args=(r, 2, port, q, n, buckets)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, bounds, order, flat, gz, seen = q.get(timeout=120)
+        res[r] = (bounds, order, flat, gz, seen)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a, b = _grads(0, n=n), _grads(1, n=n)
+    for r in range(2):
+        bounds, order, flat, gz, seen = res[r]
+        assert bounds[0][0] == 0 and bounds[-1][1] == n and all(x[1] == y[0] for x, y in zip(bounds, bounds[1:]))
+        assert len(bounds) == min(buckets, len(bounds)) and all(x[0] % 8 == 0 for x in bounds)
+        prod = [o for o in order if o[0] == "p"]
+        cons = [o for o in order if o[0] == "c"]
+        assert [o[1:] for o in prod] == bounds and [o[1:] for o in cons] == bounds
+        torch.testing.assert_close(flat, a.flat + b.flat)
+        torch.testing.assert_close(gz, torch.maximum(a.g_z, b.g_z))
+        for (lo, hi), (dsh, z) in seen.items():
+            torch.testing.assert_close(dsh, a.d_sh[lo:hi] + b.d_sh[lo:hi])
+            torch.testing.assert_close(z, torch.maximum(a.g_z[lo:hi], b.g_z[lo:hi]))
+    assert torch.equal(res[0][2], res[1][2])
+
+
+@pytest.mark.parametrize("n,buckets", [(0, 4), (100, 1), (1000, 4), (1000, 16), (130, 8)])
+def test_bucket_bounds(n, buckets):
+    from paper_2605_18334_b200.train import bucket_bounds
+    bounds = bucket_bounds(n, buckets)
+    if n == 0:
+        assert bounds == [(0, 0)]
+        return
+    assert bounds[0][0] == 0 and bounds[-1][1] == n
+    assert all(lo < hi for lo, hi in bounds) and len(bounds) <= buckets
+    assert all(lo % 128 == 0 for lo, _ in bounds)
