@@ -16,8 +16,8 @@ copies inside the timed region, wall clock, max over ranks.
 --impl reference runs the reference's own CPU implementation (the
 unmodified reference package built into oracle/_ref, Cython+OpenMP blend on
 all host cores; falls back to the C oracle port when oracle/_ref is absent)
-on a bounded homothetic 1/k sample of the same frame (see
-synthetic.homothetic_sample) and reports full-frame views/s = 1/(k * t_sample).
+on one full config-2 frame, with a bounded homothetic 1/k sample
+(synthetic.homothetic_sample) timed beside it as a cross-check.
 """
 
 from __future__ import annotations
@@ -38,15 +38,18 @@ import numpy as np  # noqa: E402
 
 METRIC = "fwd+bwd raster ms/frame, 1M skew Gaussians @1080p; views/s at 1/2/4/8 GPU"
 # libssg_b200 kernel launches per fwd+bwd frame (all hand-written, no library
-# kernels): preprocess_fwd 1; depth sort + count scan 1 (cooperative);
-# two-level counting scatter 8 (rows: count, rowscan, rowstart, scatter;
-# tiles: count, tilescan, tilestart, scatter); blend_fwd 2 (fp32 kernel +
-# exact path over its flagged pixels); blend_bwd 2 (same); preprocess_bwd 1.
-LAUNCHES_PER_FRAME = 15
-LAUNCHES_NOTE = ("per frame: k_preprocess_forward 1, k_depth_sort 1, k_cs1_{count,rowscan,rowstart,scatter} 4, "
-                 "k_cs2_{count,tilescan,tilestart,scatter} 4, k_blend_forward 1 + k_blend_forward_redo 1, "
-                 "k_blend_backward 1 + k_blend_backward_redo_list 1, k_preprocess_backward 1; no library "
-                 "kernels (cudaMemsetAsync excluded)")
+# kernels; cudaMemsetAsync excluded): preprocess_fwd 1; depth sort + count
+# scan 8 (minmax, bucket count / scan / scatter / rank / big-bucket sort,
+# count scan, the gated exact fallback); two-level counting scatter 8 (rows:
+# count, rowscan, rowstart, scatter; tiles: count, tilescan, tilestart,
+# scatter); blend_fwd 2 (fp32 kernel + exact path over its flagged pixels);
+# blend_bwd 2 (same); preprocess_bwd 1.
+LAUNCHES_PER_FRAME = 22
+LAUNCHES_NOTE = ("per frame: k_preprocess_forward 1, osort::k_minmax 1, bsort::k_{count,scan,scatter,rank,big,"
+                 "count_scan} 6, dsort::k_depth_sort 1 (exact fallback, returns at once unless flagged), "
+                 "k_cs1_{count,rowscan,rowstart,scatter} 4, k_cs2_{count,tilescan,tilestart,scatter} 4, "
+                 "k_blend_forward 1 + k_blend_forward_redo 1, k_blend_backward 1 + k_blend_backward_redo_list 1, "
+                 "k_preprocess_backward 1; no library kernels (cudaMemsetAsync excluded)")
 UNIT = "views/s"
 N_PRIM, WIDTH, HEIGHT = 1_000_000, 1920, 1080
 # per-pair algorithmic instruction counts (fixed, not tuned)

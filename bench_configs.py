@@ -148,7 +148,9 @@ def config4(args, rank, world, local):
                 "d2h_bytes_per_step": len(mine) * H4 * W4 * (24 + 8 + 4 + 8),
                 "path": "render_forward per view with the scene in pinned host memory (uploaded per call, "
                         "like the reference API), fp64 frame bundle back to host"},
-        "gpu_launches": (B.LAUNCHES_PER_FRAME - 3) * len(mine) * args.steps,
+        # per view the frame's forward launches minus the projection (one
+        # batched projection per 8 views)
+        "gpu_launches": ((B.LAUNCHES_PER_FRAME - 4) * len(mine) + -(-len(mine) // 8)) * args.steps,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         sub_view = views[0]
