@@ -30,10 +30,10 @@ def render_views(ds: DeviceScene, views, s: float = 0.3, engine=None,
     """Forward-render every view of `views` (same width/height) into
     out[v] (float32 (V,H,W,3) on the engine's device).
 
-    `engine` may be one Engine or several: with k engines, view i renders on
-    engine i % k, each on its own CUDA stream, so one view's latency-bound
-    projection and binning overlap another view's issue-bound blend (the
-    views are independent; every engine owns its buffers)."""
+    `engine` may be one Engine or several: with k engines, the groups of 8
+    views go to the engines round-robin, each on its own CUDA stream, so one
+    view's latency-bound binning overlaps another view's issue-bound blend
+    (the views are independent; every engine owns its buffers)."""
     engines = list(engine) if isinstance(engine, (list, tuple)) else [engine or default_engine()]
     eng = engines[0]
     if not views:
@@ -56,16 +56,20 @@ def render_views(ds: DeviceScene, views, s: float = 0.3, engine=None,
         lanes = [e.lane_stream() for e in engines]
         for st in lanes:
             st.wait_event(start)
-        for i, v in enumerate(views):
-            k = i % len(engines)
+        # groups of up to 8 views (one batched projection each), dealt to
+        # the engines round-robin
+        B = N.MAX_BATCH_VIEWS
+        for g, b0 in enumerate(range(0, len(views), B)):
+            k = g % len(engines)
             with torch.cuda.stream(lanes[k]):
-                engines[k].forward(ds, v, s, color_out=out[i], sync=(i < len(engines)))
+                engines[k].forward_views(ds, views[b0:b0 + B], s, out=out[b0:b0 + B], sync_first=g < len(engines))
         for st in lanes:
             done = torch.cuda.Event()
             done.record(st)
             main.wait_event(done)
+    used = engines if len(engines) == 1 else engines[:-(-len(views) // N.MAX_BATCH_VIEWS)]
     try:
-        for e in engines:
+        for e in used:
             e.instances()
     except N.NativeError:  # capacity overflow somewhere in the batch: redo with read-backs
         for i, v in enumerate(views):

@@ -126,7 +126,7 @@ def test_full_size_properties(plain):
 
 def test_config4_view_batch_equals_single_views():
     scene = ball_scene(200_000, seed=3)
-    views = orbit_views(6, width=1297, height=840, fov_x=0.9)
+    views = orbit_views(20, width=1297, height=840, fov_x=0.9)  # 3 groups of <= 8 views
     eng = Engine()
     ds = DeviceScene.from_host(scene)
     singles = []
