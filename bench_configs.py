@@ -103,10 +103,11 @@ def config4(args, rank, world, local):
     clocks.mark(t_start, time.perf_counter())
     clk = clocks.stop()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-    # per-stage times from one separate, untimed batch (stage events would
-    # perturb the timed loop): totals over the batch / views
+    # per-stage times from one separate, untimed batch on one lane (stage
+    # events would perturb the timed loop; lanes overlap stages): totals over
+    # the batch / views
     eng.stage_events = {}
-    render_views(ds, mine, engine=lanes, out=out)
+    render_views(ds, mine, engine=eng, out=out)
     torch.cuda.synchronize()
     stage_ms = {k: sum(a.elapsed_time(b) for a, b in v) / max(len(mine), 1) for k, v in eng.stage_events.items()}
     eng.stage_events = None
