@@ -23,7 +23,7 @@ python tools/launch_table.py gpurun_out/${tag}_launches.csv > gpurun_out/${tag}_
 if [ -z "${NO_NCU:-}" ]; then
 for k in blend preprocess sort cs; do
   case $k in blend) rx="k_blend"; sk=6; c=2;; preprocess) rx="k_preprocess"; sk=6; c=2;;
-             sort) rx="bsort|osort|dsort"; sk=0; c=12;; cs) rx="k_cs"; sk=24; c=8;; esac
+             sort) rx="k_count|k_scan|k_scatter|k_rank|k_minmax|k_depth_sort"; sk=0; c=8;; cs) rx="k_cs"; sk=24; c=8;; esac
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$rx" -s $sk -c $c \
     -o gpurun_out/${tag}_$k -f python bench.py --steps 2 --warmup 3 --e2e-steps 1 --no-cpu > gpurun_out/${tag}_ncu_$k.log 2>&1
   python tools/ncu_summary.py gpurun_out/${tag}_$k.ncu-rep > gpurun_out/${tag}_ncu_$k.txt 2>&1
