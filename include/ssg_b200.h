@@ -327,6 +327,14 @@ int ssg_image_loss(const float *rendered, const float *target, int32_t width, in
 int ssg_regularize(int64_t n, const float *beta, const float *opacity_logits, const float *d_eta,
                    float lambda_beta, float lambda_opacity, float *d_beta, float *d_logits, double *sums,
                    void *stream);
+/* A step's loss value and fate, on the device (no host read-back): loss[0] =
+ * (1-l) sums[0]/(3HW) + l (1 - sums[1]/(3 (H-10)(W-10))) + sums[2] (l == 0: the
+ * L1 term only), in the reference's fp64 operation order (losses.py:103-113,
+ * fit2d.py:69); flag[0] = 2 when n_instances[1] > capacity (the frame's lists
+ * were truncated), else 1 when the loss is not finite (fit2d.py:70-71), else 0.
+ * n_instances / flag may be NULL (value only). */
+int ssg_step_value(const double *sums, int32_t width, int32_t height, double lambda_ssim,
+                   const int64_t *n_instances, int64_t capacity, double *loss, int32_t *flag, void *stream);
 /* trainer.py:49-53 _IntervalStats.add: uv_sum += g_uv, z_max = max(z_max, g_z),
  * mu_sum += d_mu */
 int ssg_interval_stats_add(int64_t n, const float *g_uv, const float *g_z, const float *d_mu,

@@ -34,7 +34,7 @@ EXPORTS = ("ssg_abi_version", "ssg_last_error", "ssg_grid_dims", "ssg_bin_temp_b
            "ssg_densify_temp_bytes", "ssg_densify_plan", "ssg_densify_apply", "ssg_ply_unpack",
            "ssg_quantize_u8", "ssg_blend_det_temp_bytes", "ssg_blend_backward_det", "ssg_erf_probe",
            "ssg_pack_splats", "ssg_blend_forward_ex", "ssg_blend_backward_ex",
-           "ssg_zero_screen_grads", "ssg_preprocess_forward_views")
+           "ssg_zero_screen_grads", "ssg_preprocess_forward_views", "ssg_step_value")
 
 _vp = ctypes.c_void_p
 
@@ -105,7 +105,7 @@ class SsgAdamHparams(ctypes.Structure):
 
 SPLAT_BYTES = 64
 SPLAT64_BYTES = 64
-ABI_VERSION = 6
+ABI_VERSION = 7
 MAX_BATCH_VIEWS = 8  # SSG_MAX_BATCH_VIEWS
 
 _lib = None
@@ -180,6 +180,8 @@ def lib():
     L.ssg_loss_scratch_floats.restype = ctypes.c_int64
     L.ssg_loss_scratch_floats.argtypes = [ctypes.c_int32, ctypes.c_int32]
     L.ssg_image_loss.argtypes = [_vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_float, _vp, _vp, _vp, _vp]
+    L.ssg_step_value.argtypes = [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, _vp, ctypes.c_int64, _vp, _vp,
+                                 _vp]
     L.ssg_regularize.argtypes = [ctypes.c_int64, _vp, _vp, _vp, ctypes.c_float, ctypes.c_float, _vp, _vp, _vp, _vp]
     L.ssg_interval_stats_add.argtypes = [ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
     L.ssg_interval_stats_add_ex.argtypes = [ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]

@@ -24,7 +24,7 @@ int check_launch(const char *what) {
 
 }  // namespace ssg
 
-extern "C" int ssg_abi_version(void) { return 6; }
+extern "C" int ssg_abi_version(void) { return 7; }
 
 extern "C" const char *ssg_last_error(void) { return ssg::g_err; }
 

@@ -351,3 +351,29 @@ extern "C" int ssg_interval_stats_add(int64_t n, const float *g_uv, const float 
                                       double *uv_sum, float *z_max, double *mu_sum, void *stream) {
     return ssg_interval_stats_add_ex(n, g_uv, g_z, d_mu, uv_sum, z_max, mu_sum, nullptr, stream);
 }
+
+namespace ssg {
+__global__ void k_step_value(const double *sums, int32_t W, int32_t H, double lam, const int64_t *n_inst,
+                             int64_t capacity, double *loss, int32_t *flag) {
+    // explicit roundings: the operations of ImageLoss.value_tensor (torch fp64)
+    const double l1 = __ddiv_rn(sums[0], __dmul_rn(__dmul_rn(3.0, (double)W), (double)H));
+    double img = l1;
+    if (lam != 0.0) {
+        const double n = __dmul_rn(__dmul_rn(3.0, (double)(W - 10)), (double)(H - 10));
+        img = __dadd_rn(__dmul_rn(__dsub_rn(1.0, lam), l1), __dmul_rn(lam, __dsub_rn(1.0, __ddiv_rn(sums[1], n))));
+    }
+    const double v = __dadd_rn(img, sums[2]);
+    *loss = v;
+    if (flag) *flag = (n_inst && n_inst[1] > capacity) ? 2 : (isfinite(v) ? 0 : 1);
+}
+}  // namespace ssg
+
+extern "C" int ssg_step_value(const double *sums, int32_t width, int32_t height, double lambda_ssim,
+                              const int64_t *n_instances, int64_t capacity, double *loss, int32_t *flag,
+                              void *stream) {
+    using namespace ssg;
+    if (!sums || !loss || width < 1 || height < 1 || lambda_ssim < 0.0) return SSG_ERR_INVALID_ARGUMENT;
+    k_step_value<<<1, 1, 0, (cudaStream_t)stream>>>(sums, width, height, lambda_ssim, n_instances, capacity, loss,
+                                                    flag);
+    return check_launch("k_step_value");
+}

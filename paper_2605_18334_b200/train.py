@@ -403,11 +403,12 @@ class Trainer:
         if self.d_beta is None or self.d_beta.shape[0] < n:
             self.d_beta = torch.empty((max(n, 1), 3), dtype=torch.float32, device=eng.device)
         self._penalty(lossfn)
-        v = lossfn.value_tensor()
-        # the step's fate on the device: 2 overflow > 1 non-finite > 0 run
-        over = eng.n_inst_dev[1] > eng.capacity
-        code = torch.where(over, 2, torch.where(torch.isfinite(v), 0, 1).to(torch.int64))
-        self._skip_dev.copy_(code.reshape(1))
+        # the step's loss and fate on the device, one kernel: 2 overflow > 1
+        # non-finite > 0 run
+        v = torch.empty(1, dtype=torch.float64, device=eng.device)
+        N.check(N.lib().ssg_step_value(lossfn.sums.data_ptr(), lossfn.W, lossfn.H, lossfn.lam,
+                                       eng.n_inst_dev.data_ptr(), eng.capacity, v.data_ptr(),
+                                       self._skip_dev.data_ptr(), _stream(eng.device)), "ssg_step_value")
         if _world(group) > 1:
             dist.all_reduce(self._skip_dev, op=dist.ReduceOp.MAX, group=group)
         # read the flag back now: waiting for it at the next step then waits
@@ -418,7 +419,7 @@ class Trainer:
         if stats is not None:
             stats._trainer = self  # bundle() flushes first
         self._update(view, s, f, dL, iteration, stats, group, self._skip_dev, lossfn)
-        loss = lossfn.value_tensor()
+        loss = v[0]  # this rank's loss (taken before the update, as fit2d.py:69 does)
         self._pending = (ev, (view, target, iteration, stats, s, group), loss)
         return loss, f
 
