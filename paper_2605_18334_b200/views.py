@@ -12,6 +12,7 @@ scene (Engine.forward_views / ssg_preprocess_forward_views).
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from . import _native as N
@@ -75,3 +76,74 @@ def render_views(ds: DeviceScene, views, s: float = 0.3, engine=None,
         for i, v in enumerate(views):
             eng.forward(ds, v, s, color_out=out[i], sync=True)
     return out
+
+
+_lane_engines: dict = {}
+
+
+def lane_engines(k: int, device=None) -> list:
+    """k engines for render_views on one device (the default engine first),
+    cached so their buffers persist across batches."""
+    eng = default_engine(device)
+    key = str(eng.device)
+    lst = _lane_engines.setdefault(key, [eng])
+    while len(lst) < k:
+        lst.append(Engine(eng.device))
+    return lst[:max(k, 1)]
+
+
+def render_views_host(scene, views, s: float = 0.3, lanes: int = 3, u8: bool = False):
+    """Host API of a view batch (a trajectory, a serving batch): the host
+    scene is uploaded once, the views are rendered on the device in groups
+    of up to 8 (one batched projection each) dealt round-robin to `lanes`
+    engines on their own streams, and every group's images are copied back
+    on a copy stream as soon as the group is done (the device-to-host copy
+    overlaps the later groups' rendering).  Returns one (V,H,W,3) numpy
+    array: float32 colour, or the dataset.py:33-38 u8 quantisation done on
+    the device (u8=True, 4x fewer bytes back)."""
+    from .serving import quantize_u8_device
+    views = list(views)
+    engines = lane_engines(lanes)
+    eng = engines[0]
+    ds = scene if isinstance(scene, DeviceScene) else DeviceScene.from_host(scene, eng.device)
+    if not views:
+        return np.empty((0, 0, 0, 3), dtype=np.uint8 if u8 else np.float32)
+    W, H = int(views[0].width), int(views[0].height)
+    if any(int(v.width) != W or int(v.height) != H for v in views):
+        raise ValueError("render_views needs views of one image size")
+    V = len(views)
+    img = torch.empty((V, H, W, 3), dtype=torch.float32, device=eng.device)
+    q = torch.empty((V, H, W, 3), dtype=torch.uint8, device=eng.device) if u8 else img
+    host = torch.empty((V, H, W, 3), dtype=q.dtype, pin_memory=True)
+    main = torch.cuda.current_stream(eng.device)
+    start = torch.cuda.Event()
+    start.record(main)
+    streams = [e.lane_stream() for e in engines]
+    copy = getattr(eng, "_copy_stream", None)
+    if copy is None:
+        copy = eng._copy_stream = torch.cuda.Stream(eng.device)
+    for st in streams + [copy]:
+        st.wait_event(start)
+    B = N.MAX_BATCH_VIEWS
+    for g, b0 in enumerate(range(0, V, B)):
+        k = g % len(engines)
+        b1 = min(V, b0 + B)
+        with torch.cuda.stream(streams[k]):
+            engines[k].forward_views(ds, views[b0:b1], s, out=img[b0:b1], sync_first=g < len(engines))
+            if u8:
+                q[b0:b1] = quantize_u8_device(img[b0:b1])
+            done = torch.cuda.Event()
+            done.record(streams[k])
+        copy.wait_event(done)
+        with torch.cuda.stream(copy):
+            host[b0:b1].copy_(q[b0:b1], non_blocking=True)
+    copy.synchronize()
+    for st in streams:
+        st.synchronize()
+    try:
+        for e in engines[:-(-V // B)]:
+            e.instances()
+    except N.NativeError:  # capacity overflow somewhere in the batch: redo synchronised
+        out = render_views(ds, views, s, engine=eng)
+        return (quantize_u8_device(out) if u8 else out).cpu().numpy()
+    return host.numpy()

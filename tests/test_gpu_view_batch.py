@@ -147,3 +147,19 @@ def test_forward_views_config4_sample_lists_bit_exact():
         assert torch.equal(out[j], ref[0])
         assert torch.equal(b.inst_prim[:m], ref[1])
         assert torch.equal(b.ranges, ref[2])
+
+
+def test_render_views_host_equals_device_batch():
+    from paper_2605_18334_b200.serving import quantize_u8_device
+    from paper_2605_18334_b200.views import render_views, render_views_host
+    rng = np.random.default_rng(9)
+    scene = fp32_round(random_scene(rng, 3000, sh_degree=3))
+    views = [random_view(rng, 112, 80) for _ in range(19)]
+    ds = DeviceScene.from_host(scene)
+    ref = render_views(ds, views, engine=Engine())
+    for lanes in (1, 3):
+        got = render_views_host(scene, views, lanes=lanes)
+        assert got.dtype == np.float32 and got.shape == (19, 80, 112, 3)
+        assert np.array_equal(got, ref.cpu().numpy())
+    u8 = render_views_host(scene, views, lanes=2, u8=True)
+    assert u8.dtype == np.uint8 and np.array_equal(u8, quantize_u8_device(ref).cpu().numpy())
