@@ -50,10 +50,37 @@ def _validate(scene, view, frame, dL_dpixels):
     return dL
 
 
+_SCENE_FIELDS = ("mu", "log_scale", "rot", "sh", "opacity_logits", "beta", "dir")
+
+
+def _reusable(eng, ds, cam, frame):
+    """The engine's last binning and blend decisions are this frame's when
+    the last drop-in render_forward on it rendered a scene equal to `ds`
+    (bitwise, on the device) from the same camera and s, and nothing has
+    binned since: then the recomputation of backward.py:49-53 would
+    reproduce them exactly, and the replay can use them directly.  Returns
+    the forward's DeviceScene or None."""
+    st = getattr(eng, "_dropin_state", None)
+    if st is None:
+        return None
+    fds, cam_bytes, s, gen = st
+    if gen != eng._bin_gen or s != float(frame.s) or cam_bytes != bytes(cam) or eng.last_m != frame.n_instances:
+        return None
+    if fds.n != ds.n or fds.sh_degree != ds.sh_degree or (eng.final_T.shape != (frame.height, frame.width)):
+        return None
+    if not all(torch.equal(getattr(fds, f), getattr(ds, f)) for f in _SCENE_FIELDS):
+        return None
+    return fds
+
+
 def _device_backward(scene, view, frame, dL):
     """Upload, recompute projection + binning (backward.py:49-53), replay.
     The frame and dL_dpixels uploads run on a second stream while the
-    recomputed projection and binning (which need only the scene) run."""
+    recomputed projection and binning (which need only the scene) run.
+    When the engine still holds this frame's own forward (same scene bits,
+    camera, s, and the frame's final_T / last_idx unchanged), the
+    recomputation is skipped: it would reproduce the same lists and
+    decisions."""
     from ..engine import camera_struct
     eng = default_engine()
     dev = eng.device
@@ -67,7 +94,17 @@ def _device_backward(scene, view, frame, dL):
         last_idx = torch.from_numpy(np.ascontiguousarray(frame.last_idx, dtype=np.int64)).to(
             dev, non_blocking=True).int()
         dL_dev = torch.from_numpy(dL).to(dev, non_blocking=True).float()
-    m = eng.project_and_bin(ds, camera_struct(view, frame.s))
+    cam = camera_struct(view, frame.s)
+    fds = _reusable(eng, ds, cam, frame)
+    if fds is not None:
+        main.wait_stream(side)
+        for t in (final_T, last_idx, dL_dev):
+            t.record_stream(main)
+        if torch.equal(final_T, eng.final_T) and torch.equal(last_idx, eng.last_idx):
+            g = eng.backward(fds, view, frame.s, eng.final_T, eng.last_idx, dL_dev, rebin=False,
+                             deterministic=True)
+            return eng, g
+    m = eng.project_and_bin(ds, cam)
     if m != frame.n_instances:
         raise FrameMismatchError("instance count differs from the forward pass")
     main.wait_stream(side)

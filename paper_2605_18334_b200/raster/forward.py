@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from ..camera import CameraView, to_opencv
-from ..engine import DeviceScene, default_engine
+from ..engine import DeviceScene, camera_struct, default_engine
 from . import backend
 
 MAX_IMAGE_DIM = 65535  # forward.py:21
@@ -62,4 +62,7 @@ def render_forward(scene, view: CameraView, s: float = 0.3,
     eng = default_engine()
     ds = DeviceScene.from_host(scene, eng.device)
     f = eng.forward(ds, view, s)
+    # what a following render_backward of this very frame can reuse (its
+    # own check: raster/backward._reusable)
+    eng._dropin_state = (ds, bytes(camera_struct(view, s)), float(s), eng._bin_gen)
     return frame_to_host(f)

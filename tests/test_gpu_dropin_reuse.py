@@ -1,0 +1,66 @@
+"""render_backward right after render_forward of the same scene reuses the
+engine's binning and blend decisions (raster/backward._reusable) instead of
+recomputing them; the result must be bit-identical to the recomputing path,
+and any change to the scene, camera, s or frame must take the full path."""
+
+import numpy as np
+import pytest
+
+from helpers import random_scene, random_view
+from paper_2605_18334_b200.engine import default_engine
+from paper_2605_18334_b200.raster import render_backward, render_forward
+from paper_2605_18334_b200.raster import backward as RB
+from paper_2605_18334_b200.synthetic import fp32_round
+
+pytestmark = pytest.mark.gpu
+GRADS = ("d_mu", "d_log_scale", "d_rot", "d_sh", "d_opacity_logits", "d_beta", "d_dir", "g_uv", "g_z")
+
+
+def _full(scene, view, frame, dL):
+    default_engine()._dropin_state = None   # forces the recomputation
+    return render_backward(scene, view, frame, dL)
+
+
+def _same(a, b):
+    for k in GRADS:
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+    assert a.n_skew_fallback == b.n_skew_fallback
+
+
+def test_reuse_is_bitwise_the_recomputation(monkeypatch):
+    rng = np.random.default_rng(21)
+    scene = fp32_round(random_scene(rng, 2500, sh_degree=3))
+    view = random_view(rng, 144, 96)
+    dL = np.random.default_rng(2).normal(size=(96, 144, 3))
+    calls = []
+    orig = RB._reusable
+    monkeypatch.setattr(RB, "_reusable", lambda *a: calls.append(r := orig(*a)) or r)
+    fr = render_forward(scene, view)
+    fast = render_backward(scene, view, fr, dL)
+    assert calls and calls[-1] is not None          # the reuse path ran
+    ref = _full(scene, view, fr, dL)
+    _same(fast, ref)
+
+
+def test_changes_take_the_full_path(monkeypatch):
+    rng = np.random.default_rng(22)
+    scene = fp32_round(random_scene(rng, 1500, sh_degree=2))
+    view = random_view(rng, 96, 80)
+    dL = np.random.default_rng(3).normal(size=(80, 96, 3))
+    fr = render_forward(scene, view)
+    # a changed scene (same shapes): the full path, the new scene's gradients
+    moved = scene.copy()
+    moved.sh[:, 0] += 0.01
+    got = render_backward(moved, view, fr, dL)
+    _same(got, _full(moved, view, fr, dL))
+    # a changed frame (last_idx edited): the full path
+    fr = render_forward(scene, view)
+    fr2 = type(fr)(**{**fr.__dict__, "final_T": fr.final_T.copy()})
+    fr2.final_T[0, 0] *= 0.5
+    got = render_backward(scene, view, fr2, dL)
+    _same(got, _full(scene, view, fr2, dL))
+    # an engine that binned since: the full path
+    fr = render_forward(scene, view)
+    render_forward(scene, random_view(rng, 96, 80))
+    got = render_backward(scene, view, fr, dL)
+    _same(got, _full(scene, view, fr, dL))
