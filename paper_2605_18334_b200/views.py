@@ -27,14 +27,19 @@ def shard_views(n_views: int, rank: int, world: int) -> range:
 
 
 def render_views(ds: DeviceScene, views, s: float = 0.3, engine=None,
-                 out: torch.Tensor | None = None) -> torch.Tensor:
+                 out: torch.Tensor | None = None, check: bool = True) -> torch.Tensor:
     """Forward-render every view of `views` (same width/height) into
     out[v] (float32 (V,H,W,3) on the engine's device).
 
     `engine` may be one Engine or several: with k engines, the groups of 8
     views go to the engines round-robin, each on its own CUDA stream, so one
     view's latency-bound binning overlaps another view's issue-bound blend
-    (the views are independent; every engine owns its buffers)."""
+    (the views are independent; every engine owns its buffers).
+
+    check=False: no host round trip at all (no instance-count read-back,
+    no capacity check) -- for capturing the batch as a CUDA graph once the
+    engines' buffers are sized; the caller then calls instances() on every
+    engine after running it (an overflow raises there)."""
     engines = list(engine) if isinstance(engine, (list, tuple)) else [engine or default_engine()]
     eng = engines[0]
     if not views:
@@ -49,7 +54,7 @@ def render_views(ds: DeviceScene, views, s: float = 0.3, engine=None,
     # end (an overflowing frame makes the batch re-render synchronised)
     if len(engines) == 1:
         # one pass over the scene projects up to MAX_BATCH_VIEWS views
-        eng.forward_views(ds, views, s, out=out, sync_first=True)
+        eng.forward_views(ds, views, s, out=out, sync_first=check)
     else:
         main = torch.cuda.current_stream(eng.device)
         start = torch.cuda.Event()
@@ -63,11 +68,14 @@ def render_views(ds: DeviceScene, views, s: float = 0.3, engine=None,
         for g, b0 in enumerate(range(0, len(views), B)):
             k = g % len(engines)
             with torch.cuda.stream(lanes[k]):
-                engines[k].forward_views(ds, views[b0:b0 + B], s, out=out[b0:b0 + B], sync_first=g < len(engines))
+                engines[k].forward_views(ds, views[b0:b0 + B], s, out=out[b0:b0 + B],
+                                         sync_first=check and g < len(engines))
         for st in lanes:
             done = torch.cuda.Event()
             done.record(st)
             main.wait_event(done)
+    if not check:
+        return out
     used = engines if len(engines) == 1 else engines[:-(-len(views) // N.MAX_BATCH_VIEWS)]
     try:
         for e in used:
