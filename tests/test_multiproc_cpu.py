@@ -41,7 +41,9 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     g = _grads(rank)
     allreduce_gradients(g)
-    q.put((rank, g.flat.clone(), g.g_z.clone(), g.d_sh.clone()))
+    # numpy (pickled by value): torch tensors would be shared through a
+    # socket of this process, which may exit before the parent reads them
+    q.put((rank, g.flat.numpy().copy(), g.g_z.numpy().copy(), g.d_sh.numpy().copy()))
     dist.destroy_process_group()
 
 
@@ -55,7 +57,7 @@ def test_gradient_allreduce_world2():
     out = dict()
     for _ in range(2):
         r, flat, gz, dsh = q.get(timeout=120)
-        out[r] = (flat, gz, dsh)
+        out[r] = (torch.from_numpy(flat), torch.from_numpy(gz), torch.from_numpy(dsh))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -129,11 +131,11 @@ def _worker_bucketed(rank, world, port, q, n, buckets):
 
     def consume(a, b):  # a consumer sees its rows fully reduced
         order.append(("c", a, b))
-        seen[(a, b)] = (g.d_sh[a:b].clone(), g.g_z[a:b].clone())
+        seen[(a, b)] = (g.d_sh[a:b].numpy().copy(), g.g_z[a:b].numpy().copy())
 
     bounds = bucket_bounds(n, buckets, align=8)
     bucketed_allreduce(g, bounds, produce=produce, consume=consume)
-    q.put((rank, bounds, order, g.flat.clone(), g.g_z.clone(), seen))
+    q.put((rank, bounds, order, g.flat.numpy().copy(), g.g_z.numpy().copy(), seen))  # numpy: by value
     dist.destroy_process_group()
 
 
@@ -163,12 +165,12 @@ def test_bucketed_allreduce_world2(n, buckets):
         prod = [o for o in order if o[0] == "p"]
         cons = [o for o in order if o[0] == "c"]
         assert [o[1:] for o in prod] == bounds and [o[1:] for o in cons] == bounds
-        torch.testing.assert_close(flat, a.flat + b.flat)
-        torch.testing.assert_close(gz, torch.maximum(a.g_z, b.g_z))
+        torch.testing.assert_close(torch.from_numpy(flat), a.flat + b.flat)
+        torch.testing.assert_close(torch.from_numpy(gz), torch.maximum(a.g_z, b.g_z))
         for (lo, hi), (dsh, z) in seen.items():
-            torch.testing.assert_close(dsh, a.d_sh[lo:hi] + b.d_sh[lo:hi])
-            torch.testing.assert_close(z, torch.maximum(a.g_z[lo:hi], b.g_z[lo:hi]))
-    assert torch.equal(res[0][2], res[1][2])
+            torch.testing.assert_close(torch.from_numpy(dsh), a.d_sh[lo:hi] + b.d_sh[lo:hi])
+            torch.testing.assert_close(torch.from_numpy(z), torch.maximum(a.g_z[lo:hi], b.g_z[lo:hi]))
+    assert (res[0][2] == res[1][2]).all()
 
 
 @pytest.mark.parametrize("n,buckets", [(0, 4), (100, 1), (1000, 4), (1000, 16), (130, 8)])
