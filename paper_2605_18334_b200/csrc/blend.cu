@@ -34,7 +34,7 @@
 // eight warps are combined in a fixed order and one thread per instance
 // stores the row (no atomics): per instance (the reference's (M,12) slots) or
 // primitive-major (each primitive's rows in ascending instance order, summed
-// in that order by k_reduce_prim_rows); their redo runs one warp per tile in
+// in that order by k_reduce_rank_rows); their redo runs one warp per tile in
 // pixel order.
 #include "ssg_common.cuh"
 
@@ -1184,18 +1184,19 @@ __global__ void k_prim_rows(int64_t n, const uint32_t *__restrict__ rank, const 
 }
 
 // deterministic mode: each primitive's rows summed in ascending instance
-// order (raster/backward.py:70-73: np.add.at visits k in order)
-__global__ void k_reduce_prim_rows(int64_t n, const uint64_t *__restrict__ prim_row,
-                                   const uint32_t *__restrict__ count, const float *__restrict__ rows,
+// order (raster/backward.py:70-73: np.add.at visits k in order), walked in
+// depth-rank order: thread r reads the rows of primitive order[r], which sit
+// right after rank r - 1's (rank_offset), so a warp reads one contiguous range
+__global__ void k_reduce_rank_rows(int64_t n, const uint32_t *__restrict__ order,
+                                   const uint64_t *__restrict__ rank_offset, const float *__restrict__ rows,
                                    float *__restrict__ screen) {
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
     float4 acc[3] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f),
                      make_float4(0.f, 0.f, 0.f, 0.f)};
-    const uint64_t r0 = prim_row[p];
-    const uint32_t c = count[p];
-    for (uint32_t i = 0; i < c; i++) {
-        const float4 *src = reinterpret_cast<const float4 *>(rows + (size_t)(r0 + i) * 12);
+    const uint64_t r0 = rank_offset[r], r1 = rank_offset[r + 1];
+    for (uint64_t i = r0; i < r1; i++) {
+        const float4 *src = reinterpret_cast<const float4 *>(rows + (size_t)i * 12);
 #pragma unroll
         for (int q = 0; q < 3; q++) {
             const float4 v = src[q];
@@ -1205,7 +1206,7 @@ __global__ void k_reduce_prim_rows(int64_t n, const uint64_t *__restrict__ prim_
             acc[q].w += v.w;
         }
     }
-    float4 *dst = reinterpret_cast<float4 *>(screen + (size_t)p * 12);
+    float4 *dst = reinterpret_cast<float4 *>(screen + (size_t)order[r] * 12);
 #pragma unroll
     for (int q = 0; q < 3; q++) dst[q] = acc[q];
 }
@@ -1412,7 +1413,7 @@ extern "C" int ssg_blend_backward_det(int64_t n, int64_t m, int32_t width, int32
         ntx, ntx * nty, width, background[0], background[1], background[2], splat, splat64, bins->inst_prim,
         bins->ranges, frame->last_idx, dL_dpixels, frame->blend_mask, frame->redo_mask, rows, prim_row,
         prim->tile_rect);
-    k_reduce_prim_rows<<<gb, 256, 0, st>>>(n, prim_row, prim->tile_count, rows, grads->screen);
+    k_reduce_rank_rows<<<gb, 256, 0, st>>>(n, bins->depth_order, bins->rank_offset, rows, grads->screen);
     return check_launch("k_blend_backward(det)");
 }
 
