@@ -68,13 +68,25 @@ constexpr int kUnsureNaN = 0x7fc00002; // ... of a pixel on the exact path
 // The ellipse {power >= far_thr} (r2 = -2 far_thr, widened by max(1e-3,
 // 4 band) relative + 1e-4 absolute) is what the per-warp culling tests
 // against the warp's 8x4 block of pixel centres, exactly.
-struct SmemBatch {
-    float4 A[kBatch];
-    float4 B[kBatch];
-    float4 C[kBatch];
-    float4 D[kBatch];
-    float4 X[kBatch];
+template <int NB>
+struct SmemBatchT {
+    float4 A[NB];
+    float4 B[NB];
+    float4 C[NB];
+    float4 D[NB];
+    float4 X[NB];
 };
+using SmemBatch = SmemBatchT<kBatch>;
+// the deterministic backward stages half batches: its per-warp partial sums
+// ([warp][instance][12] floats) then take 24 KB instead of 48 KB, and twice
+// as many CTAs fit an SM
+#ifndef SSG_DET_BATCH
+#define SSG_DET_BATCH 128
+#endif
+constexpr int kDetBatch = SSG_DET_BATCH;
+#ifndef SSG_DET_MINB
+#define SSG_DET_MINB 8
+#endif
 struct Staged {
     float4 A, B, C, D, X;
 };
@@ -109,8 +121,9 @@ __device__ __forceinline__ Staged stage_values(const ssg_splat *splat, uint32_t 
     return v;
 }
 
+template <int NB>
 __device__ __forceinline__ void stage_splat(const ssg_splat *splat, uint32_t p, double ox, double oy,
-                                            SmemBatch &s, int slot) {
+                                            SmemBatchT<NB> &s, int slot) {
     const Staged v = stage_values(splat, p, ox, oy);
     s.A[slot] = v.A;
     s.B[slot] = v.B;
@@ -762,15 +775,16 @@ __device__ __forceinline__ float *dest_row(float *out, int k, uint32_t p, int tx
 }
 
 template <int kMode>
-__global__ void __launch_bounds__(kThreads, kMode == 0 ? SSG_BWD_MINB : 2)
+__global__ void __launch_bounds__(kThreads, kMode == 0 ? SSG_BWD_MINB : SSG_DET_MINB)
 k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float bg2,
                  const ssg_splat *__restrict__ splat, const uint32_t *__restrict__ inst_prim,
                  const int32_t *__restrict__ ranges, const float *__restrict__ final_T,
                  const int32_t *__restrict__ last_idx, const uint32_t *__restrict__ blend_mask,
                  const uint32_t *__restrict__ redo_mask, const float *__restrict__ dL, float *__restrict__ out,
                  const uint64_t *__restrict__ prim_row, const uint64_t *__restrict__ tile_rect) {
-    __shared__ SmemBatch s;
-    __shared__ float *sRow[kBatch];  // destination gradient row of each staged instance
+    constexpr int kB = kMode == 0 ? kBatch : kDetBatch;  // instances staged per batch
+    __shared__ SmemBatchT<kB> s;
+    __shared__ float *sRow[kB];  // destination gradient row of each staged instance
     __shared__ int sMax[kWarps];
     extern __shared__ __align__(16) float s_part[];  // deterministic modes: [warp][instance][12]
     const int tile = blockIdx.x;
@@ -828,16 +842,16 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
     // this lane's destination pointer slot: sRow[j] + my_comp, read as one
     // 64-bit shared load per visit (the pointer array's shared-window address)
     const uint32_t aRow = smem_addr(sRow);
-    float *part = kMode != 0 ? s_part + (size_t)warp * kBatch * 12 : nullptr;
+    float *part = kMode != 0 ? s_part + (size_t)warp * kB * 12 : nullptr;
 
     // batches aligned to the forward's chunk grid (start + 256 b), top down
-    for (int b = (hi - start - 1) / kBatch; b >= 0; b--) {
-        const int lo = start + b * kBatch;
-        const int cnt = min(kBatch, hi - lo);
+    for (int b = (hi - start - 1) / kB; b >= 0; b--) {
+        const int lo = start + b * kB;
+        const int cnt = min(kB, hi - lo);
         // this warp's mask words of the batch (lane q < 8 holds chunk q)
         uint32_t words = 0;
         if (blend_mask && lane < 8 && 32 * lane < cnt)
-            words = blend_mask[mask_word(start, tile, b * (kBatch / 32) + lane, warp)];
+            words = blend_mask[mask_word(start, tile, b * (kB / 32) + lane, warp)];
         __syncthreads();  // previous batch fully consumed
         for (int t = threadIdx.x; t < cnt; t += kThreads) {
             const uint32_t p = inst_prim[lo + t];
@@ -953,7 +967,7 @@ k_blend_backward(int32_t ntx, int32_t W, int32_t H, float bg0, float bg1, float 
                 for (int c = 0; c < 3; c++) acc[c] = reinterpret_cast<const float4 *>(s_part + j * 12)[c];
 #pragma unroll
                 for (int w = 1; w < kWarps; w++) {
-                    const float4 *src = reinterpret_cast<const float4 *>(s_part + ((size_t)w * kBatch + j) * 12);
+                    const float4 *src = reinterpret_cast<const float4 *>(s_part + ((size_t)w * kB + j) * 12);
 #pragma unroll
                     for (int c = 0; c < 3; c++) {
                         const float4 v = src[c];
@@ -1218,7 +1232,7 @@ __global__ void k_erf_probe(const double *x, int64_t n, float *e32, double *e64)
     if (e64) e64[i] = ref_erf(x[i]);
 }
 
-constexpr size_t kDetSmem = sizeof(float) * kWarps * kBatch * 12;
+constexpr size_t kDetSmem = sizeof(float) * kWarps * kDetBatch * 12;
 
 // per-device one-time launch setup (function attributes are per device)
 struct DevSetup {
