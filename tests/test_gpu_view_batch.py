@@ -163,3 +163,25 @@ def test_render_views_host_equals_device_batch():
         assert np.array_equal(got, ref.cpu().numpy())
     u8 = render_views_host(scene, views, lanes=2, u8=True)
     assert u8.dtype == np.uint8 and np.array_equal(u8, quantize_u8_device(ref).cpu().numpy())
+
+
+def test_forward_views_empty_and_behind_camera_scenes():
+    """No primitives, or every primitive behind the cameras: the batch
+    renders the background, like the one-view path."""
+    from paper_2605_18334_b200.scene import Scene
+    rng = np.random.default_rng(4)
+    views = [random_view(rng, 64, 48) for _ in range(10)]
+    empty = Scene(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0, 4, 3)), np.zeros((0, 2)),
+                  np.zeros((0, 3)), np.zeros((0, 3)), background=np.array([0.25, 0.5, 0.75]), sh_degree=1)
+    eng = Engine()
+    out = eng.forward_views(DeviceScene.from_host(empty), views, 0.3)
+    eng.instances()
+    assert torch.all(out == torch.tensor([0.25, 0.5, 0.75], device="cuda"))
+    scene = fp32_round(random_scene(rng, 500, sh_degree=1))
+    ds = DeviceScene.from_host(scene)
+    behind = [random_view(rng, 64, 48, dist=0.01) for _ in range(3)]   # inside the cloud
+    single = Engine()
+    ref = [single.forward(ds, v, 0.3).color.clone() for v in behind]
+    got = Engine().forward_views(ds, behind, 0.3)
+    for a, b in zip(ref, got):
+        assert torch.equal(a, b)
