@@ -438,6 +438,17 @@ class Engine:
         self._ensure_prim(ds.n)
         sc = ds.struct()
         B = N.MAX_BATCH_VIEWS
+        # projection and binning on a high-priority stream, the blends on a
+        # low-priority one: when several engines render batches side by side
+        # (views.render_views lanes), an engine's latency-bound binning gets
+        # the SM slots the other engines' issue-bound blends free up first
+        caller = torch.cuda.current_stream(self.device)
+        hi, lo = self._prio_streams()
+        fork = torch.cuda.Event()
+        fork.record(caller)
+        hi.wait_event(fork)
+        lo.wait_event(fork)
+        last_blend = None
         for b0 in range(0, len(views), B):
             chunk = views[b0:b0 + B]
             k = len(chunk)
@@ -445,14 +456,35 @@ class Engine:
             sets = self._view_sets(k)
             cam_arr = (N.SsgCamera * k)(*cams)
             out_arr = (N.SsgPrimBuffers * k)(*[self._set_struct(d) for d in sets[:k]])
-            with self._mark("preprocess_fwd_views"):
-                N.check(self.lib.ssg_preprocess_forward_views(ctypes.byref(sc), cam_arr, out_arr, k, self._stream()),
-                        "ssg_preprocess_forward_views")
+            with torch.cuda.stream(hi):
+                if last_blend is not None:  # the view sets are the previous group's blend inputs
+                    hi.wait_event(last_blend)
+                with self._mark("preprocess_fwd_views"):
+                    N.check(self.lib.ssg_preprocess_forward_views(ctypes.byref(sc), cam_arr, out_arr, k,
+                                                                  hi.cuda_stream), "ssg_preprocess_forward_views")
             for j, v in enumerate(chunk):
                 for f in self._SET_FIELDS:
                     setattr(self, f, sets[j][f])
-                self.forward(ds, v, s, color_out=out[b0 + j], sync=sync_first and b0 + j == 0, _cam=cams[j])
+                W, H = int(cams[j].width), int(cams[j].height)
+                with torch.cuda.stream(hi):
+                    if last_blend is not None:  # the binning buffers are the previous blend's inputs
+                        hi.wait_event(last_blend)
+                    m = self._bin(ds.n, W, H, sync_first and b0 + j == 0)
+                    binned = torch.cuda.Event()
+                    binned.record(hi)
+                with torch.cuda.stream(lo):
+                    lo.wait_event(binned)
+                    self._blend_frame(ds, W, H, m, s, out[b0 + j], False)
+                    last_blend = torch.cuda.Event()
+                    last_blend.record(lo)
+        caller.wait_event(last_blend)
         return out
+
+    def _prio_streams(self):
+        if getattr(self, "_prio", None) is None:
+            low, high = torch.cuda.Stream.priority_range()
+            self._prio = (torch.cuda.Stream(self.device, priority=high), torch.cuda.Stream(self.device, priority=low))
+        return self._prio
 
     def project(self, ds: DeviceScene, view: CameraView, s: float = 0.3) -> torch.Tensor:
         """Projection only (projection.py:151-235): the screen radii (n,)
@@ -511,6 +543,11 @@ class Engine:
             cam = _cam
             W, H = int(cam.width), int(cam.height)
             m = self._bin(ds.n, W, H, sync)
+        return self._blend_frame(ds, W, H, m, s, color_out, defer_exact)
+
+    def _blend_frame(self, ds: DeviceScene, W: int, H: int, m: int, s: float,
+                     color_out: torch.Tensor | None, defer_exact: bool) -> DeviceFrame:
+        """The blend half of forward() over the current binning (current stream)."""
         self._ensure_frame(W, H)
         if color_out is not None and (tuple(color_out.shape) != (H, W, 3) or color_out.dtype != torch.float32
                                       or not color_out.is_contiguous() or color_out.device != self.device):

@@ -100,7 +100,7 @@ def lane_engines(k: int, device=None) -> list:
     return lst[:max(k, 1)]
 
 
-def render_views_host(scene, views, s: float = 0.3, lanes: int = 3, u8: bool = False):
+def render_views_host(scene, views, s: float = 0.3, lanes: int = 4, u8: bool = False):
     """Host API of a view batch (a trajectory, a serving batch): the host
     scene is uploaded once, the views are rendered on the device in groups
     of up to 8 (one batched projection each) dealt round-robin to `lanes`
