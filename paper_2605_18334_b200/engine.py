@@ -390,19 +390,21 @@ class Engine:
 
     def _view_sets(self, k: int) -> list:
         """k per-view screen-record sets for ssg_preprocess_forward_views
-        (valid / depth / radius are not written by a batch).  Sized like the
-        primary buffers (_prim_n rows), so whichever set is bound satisfies
+        (valid / depth / radius are not written by a batch), grown on demand
+        (a short last group reuses the first sets).  Sized like the primary
+        buffers (_prim_n rows), so whichever set is bound satisfies
         _ensure_prim's invariant."""
-        key = (self._prim_n, k)
-        if getattr(self, "_vsets_key", None) != key:
-            nn = self._prim_n
-            self._vsets = [dict(splat=self._empty((nn, N.SPLAT_BYTES // 8), torch.float64),
-                                splat64=self._empty((nn, N.SPLAT64_BYTES // 8), torch.float64),
-                                depth_key=self._empty((nn,), torch.int64),
-                                tile_count=self._empty((nn,), torch.int32),
-                                tile_rect=self._empty((nn,), torch.int64),
-                                n_fallback=self._empty((1,), torch.int32)) for _ in range(k)]
-            self._vsets_key = key
+        if getattr(self, "_vsets_n", None) != self._prim_n:
+            self._vsets = []
+            self._vsets_n = self._prim_n
+        nn = self._prim_n
+        while len(self._vsets) < k:
+            self._vsets.append(dict(splat=self._empty((nn, N.SPLAT_BYTES // 8), torch.float64),
+                                    splat64=self._empty((nn, N.SPLAT64_BYTES // 8), torch.float64),
+                                    depth_key=self._empty((nn,), torch.int64),
+                                    tile_count=self._empty((nn,), torch.int32),
+                                    tile_rect=self._empty((nn,), torch.int64),
+                                    n_fallback=self._empty((1,), torch.int32)))
         return self._vsets
 
     @staticmethod
