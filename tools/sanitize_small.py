@@ -4,7 +4,10 @@
 Covers the fp32 kernels, the exact path (all_exact), the deterministic
 backward, the plugin slot's per-instance slots, both depth sorts (the
 cooperative one below 2M keys via the binning, the onesweep one through the
-sort hook) and the counting scatter."""
+sort hook) and the counting scatter; the view-batched projection with its
+lanes (priority streams), the pipelined + bucketed training step (step-value
+kernel, range-wise projection backward / Adam) and the deterministic
+backward's half batches."""
 
 from __future__ import annotations
 
@@ -57,6 +60,23 @@ def main():
     tmp = torch.empty(int(L.ssg_test_sort_temp_bytes(n, 8)), dtype=torch.uint8, device="cuda")
     N.check(L.ssg_test_sort(keys.data_ptr(), vals.data_ptr(), 8, 1, n, 8, tmp.data_ptr(),
                             torch.cuda.current_stream().cuda_stream), "sort")
+    torch.cuda.synchronize()
+    # view batches (ssg_preprocess_forward_views, 2 lanes, 11 views: 8 + 3)
+    from paper_2605_18334_b200.views import render_views
+    views = [random_view(rng, 72, 40) for _ in range(11)]
+    render_views(ds, views, engine=[Engine(), Engine()])
+    # a pipelined, bucketed training step (ssg_step_value, range-wise
+    # projection backward, regularizer and Adam)
+    from paper_2605_18334_b200.train import DeviceAdam, IntervalStats, Trainer
+    tds = DeviceScene.from_host(scene)
+    teng = Engine()
+    teng.deterministic = True
+    tr = Trainer(teng, tds, DeviceAdam(tds), pipelined=True, buckets=3)
+    stats = IntervalStats(tds.n, teng.device)
+    target = torch.rand((40, 72, 3), device="cuda")
+    for it in range(3):
+        tr.step(views[it], target, it, stats=stats)
+    tr.flush()
     torch.cuda.synchronize()
     print("sanitize_small: ok")
 
