@@ -323,8 +323,8 @@ def main():
                     help="BASELINE.json config: 2 (default, the headline), 3 (50%% skew-free), "
                          "4 (3M, 64-view forward batch sharded over ranks), 5 (2M view-parallel training)")
     args = ap.parse_args()
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
-        return spawn(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        return spawn(args)  # (the reference arm is one CPU process whatever --gpus says)
     if args.config in (4, 5):
         import bench_configs
         return bench_configs.main(args)
