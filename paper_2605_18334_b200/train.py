@@ -141,15 +141,20 @@ def bucketed_allreduce(grads: DeviceGrads, bounds: list, group=None, produce=Non
     values of a row do not depend on how rows are grouped."""
     world = _world(group)
     cuda = comm_stream is not None and grads.g_z.is_cuda
+    nccl = world > 1 and dist.get_backend(group) == "nccl"
 
     def reduce_range(a, b):
         if world == 1:
             return
         g = grads.rows(a, b)
-        with dist._coalescing_manager(group, grads.g_z.device if cuda else None, async_ops=True) as cm:
+        if cuda and not nccl:  # gloo over CUDA tensors: no coalescing support
             for f in DeviceGrads.SUM_FIELDS:
                 dist.all_reduce(getattr(g, f), op=dist.ReduceOp.SUM, group=group)
-        cm.wait()
+        else:
+            with dist._coalescing_manager(group, grads.g_z.device if cuda else None, async_ops=True) as cm:
+                for f in DeviceGrads.SUM_FIELDS:
+                    dist.all_reduce(getattr(g, f), op=dist.ReduceOp.SUM, group=group)
+            cm.wait()
         dist.all_reduce(g.g_z, op=dist.ReduceOp.MAX, group=group)
 
     if not cuda:

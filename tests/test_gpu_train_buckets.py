@@ -137,3 +137,62 @@ def test_nccl_two_ranks_match_summed_gradients():
         adam.step(g, it)
     for f in FIELDS:
         torch.testing.assert_close(res[0][f], getattr(ds, f).cpu(), rtol=1e-5, atol=1e-6)
+
+
+def _gloo_cuda_worker(rank, world, port, start, views, targets, q):
+    """Two ranks on one GPU with gloo over CUDA tensors: exercises the
+    comm-stream path of bucketed_allreduce (events, the grouped all-reduce,
+    the per-range consumers) where NCCL needs one GPU per rank."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    eng = Engine(torch.device("cuda", 0))
+    eng.deterministic = True
+    ds = DeviceScene.from_host(start, eng.device)
+    adam = DeviceAdam(ds, _no_reg())
+    tr = Trainer(eng, ds, adam, buckets=4)
+    for it in range(3):
+        tr.step(views[(it + rank) % 3], targets[(it + rank) % 3].to(eng.device), it)
+    torch.cuda.synchronize()
+    q.put((rank, {f: getattr(ds, f).cpu().numpy() for f in FIELDS}))
+    dist.destroy_process_group()
+
+
+def test_bucketed_allreduce_two_ranks_one_gpu_gloo():
+    import torch.multiprocessing as mp
+    start, views, targets = _setup(n=800)
+    targets = [t.cpu() for t in targets]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_cuda_worker, args=(r, 2, port, start, views, targets, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for f in FIELDS:
+        assert np.array_equal(res[0][f], res[1][f]), f
+    # one process: the two views' gradients summed, then the same updates
+    eng = Engine()
+    eng.deterministic = True
+    ds = DeviceScene.from_host(start)
+    adam = DeviceAdam(ds, _no_reg())
+    from paper_2605_18334_b200.train import ImageLoss
+    for it in range(3):
+        acc = None
+        for r in range(2):
+            v = views[(it + r) % 3]
+            f = eng.forward(ds, v, 0.3)
+            lossfn = ImageLoss(f.width, f.height, adam.cfg.lambda_ssim, eng.device)
+            dL = lossfn(f.color, targets[(it + r) % 3].cuda())
+            g = eng.backward(ds, v, 0.3, f.final_T, f.last_idx, dL, rebin=False)
+            acc = (g.flat.clone(), g.g_z.clone()) if acc is None else (acc[0] + g.flat, torch.maximum(acc[1], g.g_z))
+        g.flat.copy_(acc[0])
+        g.g_z.copy_(acc[1])
+        adam.step(g, it)
+    for f in FIELDS:
+        np.testing.assert_allclose(res[0][f], getattr(ds, f).cpu().numpy(), rtol=1e-5, atol=1e-6)
