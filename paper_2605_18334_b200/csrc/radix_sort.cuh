@@ -1,12 +1,13 @@
-// radix_sort.cuh -- small helpers shared by the binning kernels (the depth
-// sort itself lives in depth_sort.cuh).
+// radix_sort.cuh -- helpers shared by the radix sorts (depth_sort.cuh: the
+// cooperative LSD sort; onesweep.cuh: the decoupled look-back sort;
+// bucket_sort.cuh: the bucket depth sort) and the counting scatter: the
+// 256-byte workspace carve-up and the lane mask used by warp-level ranking.
 #pragma once
 
 #include "ssg_common.cuh"
 
 namespace ssg {
 namespace radix {
-
 
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
