@@ -640,18 +640,20 @@ extern "C" int ssg_bin_finish(int64_t n, int64_t m, int32_t width, int32_t heigh
     const size_t smc1 = sizeof(uint32_t) * kCsWarps * (nty + 1), smc2 = sizeof(uint32_t) * kCsWarps * (ntx + 1);
     // the largest grids (4096 tiles per side) need > 48 KB; function
     // attributes are per device, so the one-time setup is per device ordinal
-    static bool attr_dev[64] = {false};
+    static DeviceOnce attr_once;
     int sms = 148, dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SSG_ERR_CUDA;
-    if (!attr_dev[dev]) {
-        const int mx = (int)(kCsWarps * cs_warp_smem<uint64_t>(4096));
-        const void *fs[] = {CS_KERNELS(k_cs1_scatter), CS_KERNELS(k_cs2_scatter), (const void *)k_cs1_count,
-                            (const void *)k_cs2_count};
-        cudaError_t e = cudaSuccess;
-        for (const void *f : fs)
-            if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    {
+        cudaError_t e = attr_once.run([](int) {
+            const int mx = (int)(kCsWarps * cs_warp_smem<uint64_t>(4096));
+            const void *fs[] = {CS_KERNELS(k_cs1_scatter), CS_KERNELS(k_cs2_scatter), (const void *)k_cs1_count,
+                                (const void *)k_cs2_count};
+            cudaError_t r = cudaSuccess;
+            for (const void *f : fs)
+                if (r == cudaSuccess) r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            return r;
+        });
+        if (e == cudaSuccess) e = cudaGetDevice(&dev);
         if (e != cudaSuccess) { set_error("cudaFuncSetAttribute(binning)", e); return SSG_ERR_CUDA; }
-        attr_dev[dev] = true;
     }
     const unsigned g1 = (unsigned)((L.nch1 + kCsWarps - 1) / kCsWarps);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

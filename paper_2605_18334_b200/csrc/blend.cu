@@ -1240,20 +1240,20 @@ struct DevSetup {
 };
 static int dev_setup(DevSetup &out) {
     static DevSetup cache[64];
-    static bool ready[64] = {false};
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess || dev < 0 || dev >= 64) { set_error("cudaGetDevice", e); return SSG_ERR_CUDA; }
-    if (!ready[dev]) {
-        e = cudaFuncSetAttribute(k_blend_backward<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDetSmem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_blend_backward<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDetSmem);
+    static DeviceOnce once;
+    cudaError_t e = once.run([](int dev) {
+        cudaError_t r = cudaFuncSetAttribute(k_blend_backward<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kDetSmem);
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(k_blend_backward<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDetSmem);
         int sms = 148;
-        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (e != cudaSuccess) { set_error("blend setup", e); return SSG_ERR_CUDA; }
-        cache[dev].redo_grid = sms * 12;  // 48 redo warps per SM
-        ready[dev] = true;
-    }
+        if (r == cudaSuccess) r = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (r == cudaSuccess) cache[dev].redo_grid = sms * 12;  // 48 redo warps per SM
+        return r;
+    });
+    int dev = 0;
+    if (e == cudaSuccess) e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) { set_error("blend setup", e); return SSG_ERR_CUDA; }
     out = cache[dev];
     return SSG_OK;
 }

@@ -419,12 +419,11 @@ static inline cudaError_t sort_and_scan(const uint64_t *keys, uint32_t *order, c
     if (e != cudaSuccess) return e;
     if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    static bool attr_dev[64] = {false};       // function attributes are per device
-    if (!attr_dev[dev]) {
-        e = cudaFuncSetAttribute(k_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBigSmem);
-        if (e != cudaSuccess) return e;
-        attr_dev[dev] = true;
-    }
+    static DeviceOnce attr_once;       // function attributes are per device
+    e = attr_once.run([](int) {
+        return cudaFuncSetAttribute(k_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBigSmem);
+    });
+    if (e != cudaSuccess) return e;
     const int64_t nc = num_chunks(n);
     const unsigned gm = (unsigned)(nc < (int64_t)sms * 4 ? nc : (int64_t)sms * 4);
     // k_minmax reads only kmin / kmax, the first two fields of both Ctl types

@@ -536,21 +536,23 @@ static inline cudaError_t sort_and_scan(const uint64_t *keys, uint32_t *order, c
     // the smem attribute and the co-resident grid size belong to the device:
     // cached per device ordinal (function attributes are per device)
     static int grid_max_dev[64] = {0};
+    static DeviceOnce setup_once;
     const int smem = (int)sizeof(Smem);
+    e = setup_once.run([smem](int dev) {
+        cudaError_t r = cudaFuncSetAttribute(k_depth_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (r != cudaSuccess) return r;
+        int sms = 0, per = 0;
+        r = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (r == cudaSuccess) r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_depth_sort, kThreads, smem);
+        if (r != cudaSuccess) return r;
+        if (per < 1) return cudaErrorInvalidConfiguration;
+        grid_max_dev[dev] = sms * per;
+        return cudaSuccess;
+    });
+    if (e != cudaSuccess) return e;
     int dev = 0;
     e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-    if (grid_max_dev[dev] == 0) {
-        e = cudaFuncSetAttribute(k_depth_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        int sms = 0, per = 0;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_depth_sort, kThreads, smem);
-        if (e != cudaSuccess) return e;
-        if (per < 1) return cudaErrorInvalidConfiguration;
-        grid_max_dev[dev] = sms * per;
-    }
     const int grid_max = grid_max_dev[dev];
     const int grid = (int)(nt < grid_max ? nt : grid_max);
     void *params[] = {&a};

@@ -410,12 +410,11 @@ static inline cudaError_t sort_and_scan(const uint64_t *keys, uint32_t *order, c
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    static bool attr_dev[64] = {false};   // function attributes are per device
-    if (!attr_dev[dev]) {
-        e = cudaFuncSetAttribute(k_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
-        if (e != cudaSuccess) return e;
-        attr_dev[dev] = true;
-    }
+    static DeviceOnce attr_once;   // function attributes are per device
+    e = attr_once.run([](int) {
+        return cudaFuncSetAttribute(k_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem);
+    });
+    if (e != cudaSuccess) return e;
     const unsigned g = (unsigned)(nt < (int64_t)sms * 4 ? nt : (int64_t)sms * 4);
     k_minmax<<<g, kT, 0, st>>>(keys, n, ctl);
     k_hist<<<g, kT, 0, st>>>(keys, n, ctl, hist);

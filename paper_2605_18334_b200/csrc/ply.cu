@@ -87,14 +87,10 @@ extern "C" int ssg_ply_unpack(const uint8_t *payload, int64_t n, int32_t stride,
         if (types[c] >= 0 && (offsets[c] < 0 || offsets[c] >= stride)) return SSG_ERR_INVALID_ARGUMENT;
     }
     const size_t smem = (size_t)stride * kPlyVerts;
-    static bool attr_dev[64] = {false};  // function attributes are per device
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SSG_ERR_CUDA;
-    if (!attr_dev[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(k_ply_unpack, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        if (e != cudaSuccess) { set_error("cudaFuncSetAttribute(ply)", e); return SSG_ERR_CUDA; }
-        attr_dev[dev] = true;
-    }
+    static DeviceOnce attr_once;  // function attributes are per device
+    const cudaError_t e = attr_once.run(
+        [](int) { return cudaFuncSetAttribute(k_ply_unpack, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
+    if (e != cudaSuccess) { set_error("cudaFuncSetAttribute(ply)", e); return SSG_ERR_CUDA; }
     const unsigned blocks = (unsigned)((n + kPlyVerts - 1) / kPlyVerts);
     k_ply_unpack<<<blocks, kPlyThreads, smem, (cudaStream_t)stream>>>(payload, n, stride, ncomp, map, sh_coeffs,
                                                                         *out);

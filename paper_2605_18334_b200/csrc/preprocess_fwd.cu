@@ -309,14 +309,12 @@ template <int DEG>
 static int launch_views(const ssg_scene &sc, const MvArgs &a, cudaStream_t st) {
     constexpr int K3 = 3 * (DEG + 1) * (DEG + 1);
     const size_t smem = sizeof(float) * (size_t)kMvThreads * mv_sh_stride(K3);
-    static bool attr_dev[64] = {false};  // function attributes are per device
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev >= 0 && dev < 64 && !attr_dev[dev]) {
-        cudaFuncSetAttribute(k_preprocess_forward_views<DEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        attr_dev[dev] = true;
-    }
+    static DeviceOnce attr_once;  // function attributes are per device
+    const cudaError_t e = attr_once.run([smem](int) {
+        return cudaFuncSetAttribute(k_preprocess_forward_views<DEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem);
+    });
+    if (e != cudaSuccess) { set_error("cudaFuncSetAttribute(preprocess views)", e); return SSG_ERR_CUDA; }
     const unsigned blocks = (unsigned)((sc.n + kMvThreads - 1) / kMvThreads);
     k_preprocess_forward_views<DEG><<<blocks, kMvThreads, smem, st>>>(sc, a);
     return check_launch("k_preprocess_forward_views");

@@ -11,7 +11,32 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "../../include/ssg_b200.h"
+
+namespace ssg {
+// One-time setup that belongs to a device (function attributes, __constant__
+// uploads, occupancy-derived grid sizes): run once per device ordinal, under
+// a mutex so concurrent first calls from several host threads are safe.
+struct DeviceOnce {
+    std::mutex mu;
+    bool done[64] = {};
+    // fn() -> cudaError_t runs on the calling thread's current device
+    template <class F>
+    cudaError_t run(F &&fn) {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return e;
+        if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+        std::lock_guard<std::mutex> lock(mu);
+        if (done[dev]) return cudaSuccess;
+        e = fn(dev);
+        if (e == cudaSuccess) done[dev] = true;
+        return e;
+    }
+};
+}  // namespace ssg
 
 #define SSG_ALPHA_MAX 0.99f          // kernel_math.py:17
 #define SSG_ALPHA_SKIP (1.0f / 255.0f) // kernel_math.py:18

@@ -289,21 +289,20 @@ extern "C" int ssg_image_loss(const float *rendered, const float *target, int32_
     if (with_ssim && (width < kWin || height < kWin)) return SSG_ERR_INVALID_ARGUMENT;  // losses.py:58-59
     if (with_ssim && !scratch) return SSG_ERR_INVALID_ARGUMENT;
     // __constant__ memory belongs to each device: upload once per device ordinal
-    static bool gauss_set_dev[64] = {false};
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SSG_ERR_CUDA;
-    if (!gauss_set_dev[dev]) {  // losses.py:28-32, normalised in fp64
-        double g[kWin], sum = 0.0;
-        for (int u = 0; u < kWin; u++) {
-            const double x = u - (kWin - 1) / 2.0;
-            g[u] = exp(-x * x / (2.0 * 1.5 * 1.5));
-            sum += g[u];
-        }
-        float gf[kWin];
-        for (int u = 0; u < kWin; u++) gf[u] = (float)(g[u] / sum);
-        cudaError_t e = cudaMemcpyToSymbol(c_gauss, gf, sizeof(gf));
+    static DeviceOnce gauss_once;
+    {
+        const cudaError_t e = gauss_once.run([](int) {  // losses.py:28-32, normalised in fp64
+            double g[kWin], sum = 0.0;
+            for (int u = 0; u < kWin; u++) {
+                const double x = u - (kWin - 1) / 2.0;
+                g[u] = exp(-x * x / (2.0 * 1.5 * 1.5));
+                sum += g[u];
+            }
+            float gf[kWin];
+            for (int u = 0; u < kWin; u++) gf[u] = (float)(g[u] / sum);
+            return cudaMemcpyToSymbol(c_gauss, gf, sizeof(gf));
+        });
         if (e != cudaSuccess) { set_error("gauss constant", e); return SSG_ERR_CUDA; }
-        gauss_set_dev[dev] = true;
     }
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(sums, 0, 2 * sizeof(double), st);
