@@ -482,16 +482,25 @@ def main():
             best = max(best, nb / (a.elapsed_time(b) * 1e-3) / 1e9)
         return best
     h2d_gbs, d2h_gbs = link_gbs(True), link_gbs(False)
-    link_floor_s = h2d / (h2d_gbs * 1e9) + d2h / (d2h_gbs * 1e9)
+    serial_floor_s = h2d / (h2d_gbs * 1e9) + d2h / (d2h_gbs * 1e9)
+    # render_forward: scene up, then frame down (serial); render_backward:
+    # dL + scene + frame up while the gradients go down (both directions)
+    fwd_h2d, fwd_d2h = scene_bytes, HEIGHT * WIDTH * (24 + 8 + 4 + 8)
+    link_floor_s = (fwd_h2d / (h2d_gbs * 1e9) + fwd_d2h / (d2h_gbs * 1e9) +
+                    max((h2d - fwd_h2d) / (h2d_gbs * 1e9), (d2h - fwd_d2h) / (d2h_gbs * 1e9)))
     e2e = {"value": world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
            "link": {"h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs, "floor_ms": link_floor_s * 1e3,
-                    "frac": link_floor_s / e2e_s,
-                    "note": "pinned 256 MiB copies, best of 4; floor = the step's H2D + D2H bytes at "
-                            "those rates, serialised (the API's calls are synchronous)"},
+                    "serial_floor_ms": serial_floor_s * 1e3, "frac": link_floor_s / e2e_s,
+                    "note": "pinned 256 MiB copies, best of 4, one direction at a time; floor = "
+                            "render_forward's bytes serialised + render_backward's two directions "
+                            "overlapped (max of its H2D and D2H times)"},
            "path": "paper_2605_18334_b200.raster.render_forward + render_backward, numpy fp64 "
-                   "scene/dL in pinned host memory, fp64 outputs back to host; backward "
-                   "recomputes projection+binning like the reference"}
+                   "scene/dL in pinned host memory, fp64 outputs back to host; the backward "
+                   "replays on the forward's lists while the scene is uploaded in chunks and the "
+                   "gradients downloaded chunk by chunk, then checks the uploaded scene and frame "
+                   "bitwise against the forward's (a difference reruns projection + binning, like "
+                   "the reference's recompute)"}
 
     # ---- roofline of the dominant kernel (blend backward): FP32 issue bound
     import torch.cuda as tc

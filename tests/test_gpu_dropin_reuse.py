@@ -1,7 +1,10 @@
 """render_backward right after render_forward of the same scene reuses the
-engine's binning and blend decisions (raster/backward._reusable) instead of
-recomputing them; the result must be bit-identical to the recomputing path,
-and any change to the scene, camera, s or frame must take the full path."""
+engine's binning and blend decisions instead of recomputing them
+(raster/backward._pipelined_backward: speculative replay while the scene is
+uploaded chunk-wise, gradients downloaded chunk-wise, a bitwise check at the
+end; raster/backward._reusable for screen_gradients).  The result must be
+bit-identical to the recomputing path, and any change to the scene,
+background, camera, s or frame must end on the full path."""
 
 import numpy as np
 import pytest
@@ -33,13 +36,53 @@ def test_reuse_is_bitwise_the_recomputation(monkeypatch):
     view = random_view(rng, 144, 96)
     dL = np.random.default_rng(2).normal(size=(96, 144, 3))
     calls = []
-    orig = RB._reusable
-    monkeypatch.setattr(RB, "_reusable", lambda *a: calls.append(r := orig(*a)) or r)
+    orig = RB._pipelined_backward
+    monkeypatch.setattr(RB, "_pipelined_backward", lambda *a, **k: calls.append(r := orig(*a, **k)) or r)
     fr = render_forward(scene, view)
     fast = render_backward(scene, view, fr, dL)
-    assert calls and calls[-1] is not None          # the reuse path ran
+    assert calls and calls[-1] is not None          # the pipelined reuse path ran
     ref = _full(scene, view, fr, dL)
     _same(fast, ref)
+    # screen_gradients' reuse (_reusable) against its recomputation
+    fr = render_forward(scene, view)
+    a = RB.screen_gradients(scene, view, fr, dL)
+    default_engine()._dropin_state = None
+    b = RB.screen_gradients(scene, view, fr, dL)
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("field", ["mu", "log_scale", "rot", "sh", "opacity_logits", "beta", "dir", "background"])
+def test_late_chunk_change_is_caught(field, monkeypatch):
+    """One value of the LAST primitive (the last upload chunk) changed
+    between forward and backward: the speculative result is discarded and
+    the projection + binning recomputed."""
+    rng = np.random.default_rng(23)
+    scene = fp32_round(random_scene(rng, 2000, sh_degree=1))
+    view = random_view(rng, 96, 64)
+    dL = np.random.default_rng(4).normal(size=(64, 96, 3))
+    fr = render_forward(scene, view)
+    moved = scene.copy()
+    a = getattr(moved, field)
+    if field == "background":
+        a[1] = 1.0 - a[1]
+    elif field in ("mu", "log_scale", "rot"):   # fp64 on the device; tiny, keeps the tile lists
+        a[-1].flat[0] += 1e-9
+    else:                                       # fp32 appearance fields
+        a[-1].flat[0] += 0.25
+    eng = default_engine()
+    binned = []
+    orig = eng.project_and_bin
+    monkeypatch.setattr(eng, "project_and_bin", lambda *x, **k: binned.append(1) or orig(*x, **k))
+    got = render_backward(moved, view, fr, dL)
+    assert binned                                   # the change was caught
+    monkeypatch.undo()
+    _same(got, _full(moved, view, fr, dL))
+    # unchanged: no recomputation
+    fr = render_forward(scene, view)
+    monkeypatch.setattr(eng, "project_and_bin", lambda *x, **k: binned.append(2) or orig(*x, **k))
+    render_backward(scene, view, fr, dL)
+    assert 2 not in binned
 
 
 def test_changes_take_the_full_path(monkeypatch):
