@@ -15,7 +15,9 @@ from __future__ import annotations
 
 import ctypes
 import dataclasses
+import functools
 import math
+import threading
 
 import numpy as np
 import torch
@@ -169,6 +171,8 @@ class Engine:
         self.deterministic = False  # backward(): bitwise-repeatable gradients (slower)
         self._exact_pending = None  # event of a deferred forward exact path
         self.all_exact = False      # test mode: every pixel on the exact fp64 path
+        # held by the drop-in entry points (dropin_serialized) for a whole call
+        self.lock = threading.RLock()
 
     def _mark(self, name: str):
         """Context for per-stage CUDA-event timing on the launching stream."""
@@ -739,11 +743,29 @@ class Engine:
 
 
 _engines: dict = {}
+_engines_lock = threading.Lock()
 
 
 def default_engine(device=None) -> Engine:
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     key = str(dev)
-    if key not in _engines:
-        _engines[key] = Engine(dev)
-    return _engines[key]
+    with _engines_lock:
+        if key not in _engines:
+            _engines[key] = Engine(dev)
+        return _engines[key]
+
+
+def dropin_serialized(fn):
+    """The drop-in entry points share one engine per device (its buffers,
+    streams and the last forward's state).  The reference's functions are
+    pure and may be called from any thread (SURVEY.md section 8(b),
+    threading), so each call holds the current device's default-engine lock
+    for its whole duration: concurrent calls run one after another, each
+    with the single-thread result."""
+    @functools.wraps(fn)
+    def call(*args, **kwargs):
+        if not torch.cuda.is_available():  # fn's own argument checks, then its CUDA error
+            return fn(*args, **kwargs)
+        with default_engine().lock:
+            return fn(*args, **kwargs)
+    return call

@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from ..camera import CameraView, to_opencv
-from ..engine import DeviceScene, default_engine
+from ..engine import DeviceScene, default_engine, dropin_serialized
 from . import backend
 from .forward import FrameBundle  # noqa: F401
 
@@ -254,6 +254,7 @@ def _host(t: torch.Tensor) -> torch.Tensor:
     return dst
 
 
+@dropin_serialized
 def screen_gradients(scene, view: CameraView, frame, dL_dpixels) -> dict:
     """Per-primitive screen-space gradients (mirror of _screen_gradients,
     backward.py:42-74): d_mean2d, d_conic, d_skew2d, d_opair, d_color."""
@@ -267,6 +268,7 @@ def screen_gradients(scene, view: CameraView, frame, dL_dpixels) -> dict:
             "d_opair": sc[:, 7:9], "d_color": sc[:, 9:12]}
 
 
+@dropin_serialized
 def render_backward(scene, view: CameraView, frame, dL_dpixels: np.ndarray,
                     backend_name: str | None = None) -> GradientBundle:
     backend.active_backend(backend_name)

@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from ..camera import CameraView, to_opencv
-from ..engine import DeviceScene, camera_struct, default_engine
+from ..engine import DeviceScene, camera_struct, default_engine, dropin_serialized
 from . import backend
 
 MAX_IMAGE_DIM = 65535  # forward.py:21
@@ -53,6 +53,7 @@ def frame_to_host(f) -> FrameBundle:
                        s=f.s)
 
 
+@dropin_serialized
 def render_forward(scene, view: CameraView, s: float = 0.3,
                    backend_name: str | None = None) -> FrameBundle:
     backend.active_backend(backend_name)

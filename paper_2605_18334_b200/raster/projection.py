@@ -18,7 +18,7 @@ from types import SimpleNamespace
 import numpy as np
 
 from ..camera import CameraView, to_opencv
-from ..engine import DeviceScene, default_engine
+from ..engine import DeviceScene, default_engine, dropin_serialized
 
 
 @dataclasses.dataclass
@@ -47,6 +47,7 @@ class ScreenSplat:
     radius: float
 
 
+@dropin_serialized
 def project_scene(scene, view: CameraView, s: float = 0.3) -> SimpleNamespace:
     """projection.py:151-235 on the device; fp64 host arrays."""
     eng = default_engine()

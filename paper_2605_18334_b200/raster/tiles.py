@@ -15,7 +15,7 @@ import math
 import numpy as np
 import torch
 
-from ..engine import TILE, default_engine, grid_dims  # noqa: F401  (re-exported)
+from ..engine import TILE, default_engine, dropin_serialized, grid_dims  # noqa: F401  (re-exported)
 
 
 @dataclasses.dataclass
@@ -46,6 +46,7 @@ def grid_from_engine(eng, ntx: int, nty: int) -> TileGrid:
                     inst_tile.cpu().numpy().astype(np.int64))
 
 
+@dropin_serialized
 def bin_arrays(mean2d, radius, depth, valid, width: int, height: int) -> TileGrid:
     """Vectorized binning over primitive arrays (tiles.py:43-79)."""
     eng = default_engine()

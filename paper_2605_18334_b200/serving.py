@@ -29,7 +29,7 @@ import torch
 
 from . import _native as N
 from .camera import OPENCV, OPENGL, CameraView
-from .engine import DeviceScene, default_engine
+from .engine import DeviceScene, default_engine, dropin_serialized
 from .views import render_views
 
 HEADER = struct.Struct("<IHH")  # service.py:31: frame_id u32, width u16, height u16
@@ -68,6 +68,7 @@ def _device_scene(scene, dev) -> DeviceScene:
     return DeviceScene.from_host(scene, dev)
 
 
+@dropin_serialized
 def render_frame(scene, frame_id: int, view: CameraView, s: float = 0.3) -> bytes:
     """service.py:105-107: header + RGB8 pixels of `view`."""
     eng = default_engine()
@@ -77,6 +78,7 @@ def render_frame(scene, frame_id: int, view: CameraView, s: float = 0.3) -> byte
     return HEADER.pack(frame_id, f.width, f.height) + px.tobytes()
 
 
+@dropin_serialized
 def render_views_u8(scene, views, s: float = 0.3) -> torch.Tensor:
     """Every view of one image size rendered and quantised on the device:
     (V,H,W,3) u8."""
@@ -124,6 +126,7 @@ def save_trajectory(path, views) -> None:
         json.dump(doc, f, indent=1)
 
 
+@dropin_serialized
 def render_trajectory(scene, trajectory, out_dir, s: float = 0.3) -> list[str]:
     """trajectory.py:12-31: one PNG per entry, names zero-padded to
     max(4, digits of the last index); the scene is uploaded once and every

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .engine import DeviceScene, Engine, default_engine
+from .engine import DeviceScene, Engine, default_engine, dropin_serialized
 
 
 def shard_views(n_views: int, rank: int, world: int) -> range:
@@ -40,7 +40,11 @@ def render_views(ds: DeviceScene, views, s: float = 0.3, engine=None,
     no capacity check) -- for capturing the batch as a CUDA graph once the
     engines' buffers are sized; the caller then calls instances() on every
     engine after running it (an overflow raises there)."""
-    engines = list(engine) if isinstance(engine, (list, tuple)) else [engine or default_engine()]
+    if engine is None:  # the shared default engine: one call at a time
+        eng = default_engine()
+        with eng.lock:
+            return render_views(ds, views, s, engine=eng, out=out, check=check)
+    engines = list(engine) if isinstance(engine, (list, tuple)) else [engine]
     eng = engines[0]
     if not views:
         return torch.empty((0, 0, 0, 3), dtype=torch.float32, device=eng.device)
@@ -100,6 +104,7 @@ def lane_engines(k: int, device=None) -> list:
     return lst[:max(k, 1)]
 
 
+@dropin_serialized
 def render_views_host(scene, views, s: float = 0.3, lanes: int = 4, u8: bool = False):
     """Host API of a view batch (a trajectory, a serving batch): the host
     scene is uploaded once, the views are rendered on the device in groups
