@@ -496,7 +496,9 @@ def main():
                             "render_forward's bytes serialised + render_backward's two directions "
                             "overlapped (max of its H2D and D2H times)"},
            "path": "paper_2605_18334_b200.raster.render_forward + render_backward, numpy fp64 "
-                   "scene/dL in pinned host memory, fp64 outputs back to host; the backward "
+                   "scene/dL in pinned host memory, fp64 outputs back to host; the forward renders "
+                   "the previous device copy of the scene while the scene uploads (re-rendered if "
+                   "the upload differs in any bit); the backward "
                    "replays on the forward's lists while the scene is uploaded in chunks and the "
                    "gradients downloaded chunk by chunk, then checks the uploaded scene and frame "
                    "bitwise against the forward's (a difference reruns projection + binning, like "

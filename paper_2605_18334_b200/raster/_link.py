@@ -1,0 +1,48 @@
+"""Host-link helpers of the drop-in calls: the copy streams, the host scene
+as fp64 arrays in the device layout, and the on-device bitwise comparison
+of two device scenes (the check that makes a speculative result exact)."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+SCENE_FIELDS = ("mu", "log_scale", "rot", "sh", "opacity_logits", "beta", "dir")
+_INT_VIEW = {torch.float64: torch.int64, torch.float32: torch.int32}
+_STREAMS: dict = {}
+
+
+def copy_streams(dev) -> tuple:
+    """(host->device, device->host) streams of a device, created once."""
+    key = str(dev)
+    if key not in _STREAMS:
+        _STREAMS[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    return _STREAMS[key]
+
+
+def host_fields(scene, n: int, K: int) -> dict:
+    """The scene's fields as C-contiguous fp64 arrays shaped like the device
+    copy (no copy when they already are, e.g. pinned caller arrays)."""
+    shapes = {"mu": (n, 3), "log_scale": (n, 3), "rot": (n, 4), "sh": (n, K, 3), "opacity_logits": (n, 2),
+              "beta": (n, 3), "dir": (n, 3)}
+    out = {}
+    for f, shp in shapes.items():
+        a = np.asarray(getattr(scene, f))
+        if f == "sh":
+            a = a.reshape(n, -1, 3)[:, :K, :]
+        out[f] = np.ascontiguousarray(a, dtype=np.float64).reshape(shp)
+    return out
+
+
+def upload_rows(ds, srcs: dict, a: int, b: int, dev) -> None:
+    """Rows [a, b) of every field into `ds` on the current stream (fp64 in
+    flight, converted on the device where `ds` keeps fp32)."""
+    for f in SCENE_FIELDS:
+        getattr(ds, f)[a:b].copy_(torch.from_numpy(srcs[f][a:b]).to(dev, non_blocking=True))
+
+
+def scenes_differ(a, b) -> torch.Tensor:
+    """Device bool: any bit of any field differs (NaN-safe: compared as
+    integers).  No host synchronisation."""
+    return torch.stack([(getattr(a, f).view(_INT_VIEW[getattr(a, f).dtype]) !=
+                         getattr(b, f).view(_INT_VIEW[getattr(b, f).dtype])).any() for f in SCENE_FIELDS]).any()

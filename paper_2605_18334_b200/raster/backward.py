@@ -16,7 +16,7 @@ import torch
 
 from ..camera import CameraView, to_opencv
 from ..engine import DeviceScene, default_engine, dropin_serialized
-from . import backend
+from . import _link, backend
 from .forward import FrameBundle  # noqa: F401
 
 
@@ -118,15 +118,7 @@ def _device_backward(scene, view, frame, dL):
     return eng, g
 
 
-_PIPE_STREAMS: dict = {}
 _OUT_FIELDS = ("d_mu", "d_log_scale", "d_rot", "d_sh", "d_opacity_logits", "d_beta", "d_dir", "g_uv", "g_z")
-
-
-def _pipe_streams(dev):
-    key = str(dev)
-    if key not in _PIPE_STREAMS:
-        _PIPE_STREAMS[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
-    return _PIPE_STREAMS[key]
 
 
 # 8 chunks measured best at config 2 (16.2 ms backward; 6: 16.8, 12: 17.1;
@@ -168,15 +160,8 @@ def _pipelined_backward(scene, view, frame, dL, chunks: int | None = None):
     K = fds.K
     dev = eng.device
     main = torch.cuda.current_stream(dev)
-    up, down = _pipe_streams(dev)
-    shapes = {"mu": (n, 3), "log_scale": (n, 3), "rot": (n, 4), "sh": (n, K, 3), "opacity_logits": (n, 2),
-              "beta": (n, 3), "dir": (n, 3)}
-    srcs = {}
-    for f, shp in shapes.items():
-        a = np.asarray(getattr(scene, f))
-        if f == "sh":
-            a = a.reshape(n, -1, 3)[:, :K, :]
-        srcs[f] = np.ascontiguousarray(a, dtype=np.float64).reshape(shp)
+    up, down = _link.copy_streams(dev)
+    srcs = _link.host_fields(scene, n, K)
     ds = DeviceScene(*(torch.empty_like(getattr(fds, f)) for f in _SCENE_FIELDS), fds.background, deg)
     bounds = bucket_bounds(n, chunks or _PIPE_CHUNKS, align=128)
     # host -> device in the order the device needs it: dL, the scene chunk by
@@ -190,8 +175,7 @@ def _pipelined_backward(scene, view, frame, dL, chunks: int | None = None):
         ev_dl = torch.cuda.Event()
         ev_dl.record(up)
         for a, b in bounds:
-            for f in _SCENE_FIELDS:
-                getattr(ds, f)[a:b].copy_(torch.from_numpy(srcs[f][a:b]).to(dev, non_blocking=True))
+            _link.upload_rows(ds, srcs, a, b, dev)
             ev = torch.cuda.Event()
             ev.record(up)
             ev_up.append(ev)
@@ -225,9 +209,7 @@ def _pipelined_backward(scene, view, frame, dL, chunks: int | None = None):
     for t in (final_T, last_idx):
         t.record_stream(main)
     frame_diff = (final_T.view(torch.int32) != eng.final_T.view(torch.int32)).any() | (last_idx != eng.last_idx).any()
-    scene_diff = torch.stack([(getattr(ds, f).view(_INT_VIEW[getattr(ds, f).dtype]) !=
-                               getattr(fds, f).view(_INT_VIEW[getattr(fds, f).dtype])).any()
-                              for f in _SCENE_FIELDS]).any()
+    scene_diff = _link.scenes_differ(ds, fds)
     differs = bool((scene_diff | frame_diff).item())  # synchronises the main stream
     down.synchronize()
     if differs:
@@ -242,9 +224,6 @@ def _pipelined_backward(scene, view, frame, dL, chunks: int | None = None):
     n_fb = eng.n_skew_fallback()
     o = {f: t.numpy() for f, t in outs.items()}
     return GradientBundle(**o, n_skew_fallback=n_fb)
-
-
-_INT_VIEW = {torch.float64: torch.int64, torch.float32: torch.int32}
 
 
 def _host(t: torch.Tensor) -> torch.Tensor:

@@ -107,3 +107,47 @@ def test_changes_take_the_full_path(monkeypatch):
     render_forward(scene, random_view(rng, 96, 80))
     got = render_backward(scene, view, fr, dL)
     _same(got, _full(scene, view, fr, dL))
+
+
+def _frame_same(a, b):
+    for k in ("color", "final_T", "n_contrib", "last_idx"):
+        x, y = getattr(a, k), getattr(b, k)
+        assert x.dtype == y.dtype and np.array_equal(x, y), k
+    assert (a.n_instances, a.n_primitives, a.width, a.height, a.s) == \
+        (b.n_instances, b.n_primitives, b.width, b.height, b.s)
+
+
+def test_speculative_forward_is_exact():
+    """render_forward renders the engine's previous device scene while the
+    caller's scene uploads, then compares the two bitwise: the same scene
+    gives the non-speculative frame bit for bit; a changed one (any field,
+    last primitive only) is re-rendered from the upload."""
+    from paper_2605_18334_b200.raster import forward as RF
+    rng = np.random.default_rng(31)
+    scene = fp32_round(random_scene(rng, 2200, sh_degree=3))
+    views = [random_view(rng, 112, 80) for _ in range(3)]
+    eng = default_engine()
+
+    def fresh(sc, v):
+        eng._dropin_state = None
+        return render_forward(sc, v)
+
+    render_forward(scene, views[0])
+    eng._spec_skip = 0
+    for v in views:                                  # same scene, new cameras: speculation holds
+        got = render_forward(scene, v)
+        assert eng._spec_skip == 0
+        _frame_same(got, fresh(scene, v))
+        eng._spec_skip = 0
+    for field in ("mu", "log_scale", "rot", "sh", "opacity_logits", "beta", "dir"):
+        render_forward(scene, views[0])
+        eng._spec_skip = 0
+        moved = scene.copy()
+        getattr(moved, field)[-1].flat[0] += 1e-9 if field in ("mu", "log_scale", "rot") else 0.25
+        got = render_forward(moved, views[1])
+        assert eng._spec_skip == RF._SPEC_BACKOFF, field   # the change was caught
+        _frame_same(got, fresh(moved, views[1]))
+        # a backward of that frame is the recompute path's
+        dL = np.random.default_rng(5).normal(size=(80, 112, 3))
+        fr = render_forward(moved, views[1])
+        _same(render_backward(moved, views[1], fr, dL), _full(moved, views[1], fr, dL))
