@@ -34,6 +34,16 @@ def host_fields(scene, n: int, K: int) -> dict:
     return out
 
 
+def host_empty(shape, dtype) -> torch.Tensor:
+    """Output buffer of a drop-in call: page-locked (fast, asynchronous
+    device->host copies) when the pinned pool can grow, else ordinary host
+    memory (the copies then run synchronously, same bytes)."""
+    try:
+        return torch.empty(shape, dtype=dtype, pin_memory=True)
+    except RuntimeError:
+        return torch.empty(shape, dtype=dtype)
+
+
 def upload_rows(ds, srcs: dict, a: int, b: int, dev) -> None:
     """Rows [a, b) of every field into `ds` on the current stream (fp64 in
     flight, converted on the device where `ds` keeps fp32)."""

@@ -189,8 +189,8 @@ def _pipelined_backward(scene, view, frame, dL, chunks: int | None = None):
     dL_dev.record_stream(main)
     g = eng.backward(fds, view, frame.s, eng.final_T, eng.last_idx, dL_dev, rebin=False, deterministic=True,
                      projection=False)
-    outs = {f: torch.empty(getattr(g, "d_eta" if f in ("d_beta", "d_dir") else f).shape, dtype=torch.float64,
-                           pin_memory=True) for f in _OUT_FIELDS}
+    outs = {f: _link.host_empty(getattr(g, "d_eta" if f in ("d_beta", "d_dir") else f).shape, torch.float64)
+            for f in _OUT_FIELDS}
     for (a, b), ev in zip(bounds, ev_up):
         main.wait_event(ev)
         eng.projection_backward(ds, cam, g, rows=(a, b))
@@ -228,7 +228,7 @@ def _pipelined_backward(scene, view, frame, dL, chunks: int | None = None):
 
 def _host(t: torch.Tensor) -> torch.Tensor:
     src = t.to(torch.float64)
-    dst = torch.empty(src.shape, dtype=torch.float64, pin_memory=True)
+    dst = _link.host_empty(src.shape, torch.float64)
     dst.copy_(src, non_blocking=True)
     return dst
 

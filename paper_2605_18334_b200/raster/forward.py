@@ -38,7 +38,7 @@ def _to_host(t: torch.Tensor, dtype: torch.dtype) -> np.ndarray:
     """Device -> pinned host copy with the boundary dtype conversion done on
     the device first (the host never loops over the data)."""
     src = t.to(dtype)
-    dst = torch.empty(src.shape, dtype=dtype, pin_memory=True)
+    dst = _link.host_empty(src.shape, dtype)
     dst.copy_(src, non_blocking=True)
     return dst
 
@@ -89,7 +89,7 @@ def _speculative_forward(eng, scene, view, s):
     f = eng.forward(fds, view, s)
     srcs_dev = [f.color.to(torch.float64), f.final_T.to(torch.float64), f.n_contrib,
                 f.last_idx.to(torch.int64)]
-    outs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in srcs_dev]
+    outs = [_link.host_empty(t.shape, t.dtype) for t in srcs_dev]
     ev_f = torch.cuda.Event()
     ev_f.record(main)
     down.wait_event(ev_f)
