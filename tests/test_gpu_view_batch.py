@@ -185,3 +185,30 @@ def test_forward_views_empty_and_behind_camera_scenes():
     got = Engine().forward_views(ds, behind, 0.3)
     for a, b in zip(ref, got):
         assert torch.equal(a, b)
+
+
+def test_render_views_host_speculation_is_exact():
+    """A host batch of the scene the engine rendered last renders on the
+    kept device copy while the upload runs, then checks the upload bitwise;
+    a changed scene (one value of the last primitive) re-renders."""
+    from paper_2605_18334_b200.views import lane_engines, render_views, render_views_host
+    rng = np.random.default_rng(12)
+    scene = fp32_round(random_scene(rng, 2500, sh_degree=2))
+    views = [random_view(rng, 96, 72) for _ in range(11)]
+    ref = render_views(DeviceScene.from_host(scene), views, engine=Engine()).cpu().numpy()
+    render_views_host(scene, views, lanes=2)
+    kept = lane_engines(2)[0]._host_batch_scene
+    got = render_views_host(scene, views, lanes=2)
+    assert lane_engines(2)[0]._host_batch_scene is kept          # speculation held
+    assert np.array_equal(got, ref)
+    moved = scene.copy()
+    moved.sh[-1, 0, 0] += 0.25
+    ref2 = render_views(DeviceScene.from_host(moved), views, engine=Engine()).cpu().numpy()
+    got2 = render_views_host(moved, views, lanes=2)
+    assert lane_engines(2)[0]._host_batch_scene is not kept      # caught, re-rendered
+    assert np.array_equal(got2, ref2)
+    moved.mu[-1, 0] += 1e-9                                       # fp64 geometry, one ulp-scale change
+    ref3 = render_views(DeviceScene.from_host(moved), views, engine=Engine()).cpu().numpy()
+    k2 = lane_engines(2)[0]._host_batch_scene
+    assert np.array_equal(render_views_host(moved, views, lanes=2, u8=False), ref3)
+    assert lane_engines(2)[0]._host_batch_scene is not k2
