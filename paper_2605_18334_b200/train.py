@@ -394,15 +394,42 @@ class Trainer:
         redo, _ = self._step_sync(view, target, iteration, stats, s, group, True)
         loss.copy_(redo)  # the step's returned loss becomes the re-run's
 
+    def _stage_target(self, target: torch.Tensor):
+        """A host target image (pinned: asynchronous) goes up on a copy
+        stream while the forward renders; _target_ready makes the loss wait
+        for it.  Device targets pass through."""
+        if target.is_cuda:
+            return target, None
+        st = getattr(self, "_h2d", None)
+        if st is None:
+            st = self._h2d = torch.cuda.Stream(self.eng.device)
+        with torch.cuda.stream(st):
+            t = target.to(self.eng.device, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(st)
+        return t, ev
+
+    def _target_ready(self, staged) -> torch.Tensor:
+        t, ev = staged
+        if ev is not None:
+            main = torch.cuda.current_stream(self.eng.device)
+            main.wait_event(ev)
+            t.record_stream(main)
+        return t
+
     def step(self, view, target: torch.Tensor, iteration: int, stats: IntervalStats | None = None,
              s: float = 0.3, group=None, check_finite: bool = True):
-        """fit2d.py:62-78.  Returns (loss tensor of this rank, frame)."""
+        """fit2d.py:62-78.  Returns (loss tensor of this rank, frame).
+        `target` may be a device tensor or a host one (pinned host memory
+        uploads under the forward)."""
         if not self.pipelined:
             return self._step_sync(view, target, iteration, stats, s, group, check_finite)
         self.flush()
         eng, ds, cfg = self.eng, self.ds, self.cfg
+        staged = self._stage_target(target)
         f = eng.forward(ds, view, s, sync=False)
         lossfn = self.loss_for(f.width, f.height)
+        target = self._target_ready(staged)
         dL = lossfn(f.color, target)
         n = ds.n
         if self.d_beta is None or self.d_beta.shape[0] < n:
@@ -439,8 +466,10 @@ class Trainer:
     def _step_sync(self, view, target: torch.Tensor, iteration: int, stats: IntervalStats | None,
                    s: float, group, check_finite: bool):
         eng, ds, cfg = self.eng, self.ds, self.cfg
+        staged = self._stage_target(target)
         f = eng.forward(ds, view, s, sync=False)  # M is checked with the loss below
         lossfn = self.loss_for(f.width, f.height)
+        target = self._target_ready(staged)
         dL = lossfn(f.color, target)
         n = ds.n
         if self.d_beta is None or self.d_beta.shape[0] < n:

@@ -196,3 +196,16 @@ def test_bucketed_allreduce_two_ranks_one_gpu_gloo():
         adam.step(g, it)
     for f in FIELDS:
         np.testing.assert_allclose(res[0][f], getattr(ds, f).cpu().numpy(), rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("pipelined", [False, True])
+def test_host_targets_equal_device_targets(pipelined):
+    """A pinned host target image uploads on the trainer's copy stream under
+    the forward; the steps equal those with the image already on the device."""
+    start, views, targets = _setup(seed=5, n=900)
+    host = [t.cpu().pin_memory() for t in targets]
+    a = _run(start, views, targets, 1, pipelined)
+    b = _run(start, views, host, 1, pipelined)
+    for f in FIELDS:
+        assert torch.equal(getattr(a[0], f), getattr(b[0], f)), f
+    np.testing.assert_allclose(a[3], b[3], rtol=1e-12)  # fp64 atomic loss sums: order-dependent ulps
