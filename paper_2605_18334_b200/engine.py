@@ -79,9 +79,11 @@ class DeviceScene:
         K = (deg + 1) ** 2
         n = int(np.asarray(scene.mu).shape[0])
 
+        from .hostlink import to_device
+
         def up(a, shape, f32):
             a = np.ascontiguousarray(a, dtype=np.float64).reshape(shape)
-            t = torch.from_numpy(a).to(dev, non_blocking=True)
+            t = to_device(a, dev)  # pageable sources go through pinned staging
             return t.float() if f32 else t
 
         sh = np.asarray(scene.sh)

@@ -7,6 +7,8 @@ from __future__ import annotations
 import numpy as np
 import torch
 
+from ..hostlink import is_pinned, to_device  # noqa: F401  (re-exported)
+
 SCENE_FIELDS = ("mu", "log_scale", "rot", "sh", "opacity_logits", "beta", "dir")
 _INT_VIEW = {torch.float64: torch.int64, torch.float32: torch.int32}
 _STREAMS: dict = {}
@@ -44,11 +46,11 @@ def host_empty(shape, dtype) -> torch.Tensor:
         return torch.empty(shape, dtype=dtype)
 
 
-def upload_rows(ds, srcs: dict, a: int, b: int, dev) -> None:
+def upload_rows(ds, srcs: dict, a: int, b: int, dev, pinned: dict | None = None) -> None:
     """Rows [a, b) of every field into `ds` on the current stream (fp64 in
     flight, converted on the device where `ds` keeps fp32)."""
     for f in SCENE_FIELDS:
-        getattr(ds, f)[a:b].copy_(torch.from_numpy(srcs[f][a:b]).to(dev, non_blocking=True))
+        getattr(ds, f)[a:b].copy_(to_device(srcs[f][a:b], dev, None if pinned is None else pinned[f]))
 
 
 def scenes_differ(a, b) -> torch.Tensor:

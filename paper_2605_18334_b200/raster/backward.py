@@ -91,11 +91,9 @@ def _device_backward(scene, view, frame, dL):
     side = eng.lane_stream()
     side.wait_stream(main)
     with torch.cuda.stream(side):
-        final_T = torch.from_numpy(np.ascontiguousarray(frame.final_T, dtype=np.float64)).to(
-            dev, non_blocking=True).float()
-        last_idx = torch.from_numpy(np.ascontiguousarray(frame.last_idx, dtype=np.int64)).to(
-            dev, non_blocking=True).int()
-        dL_dev = torch.from_numpy(dL).to(dev, non_blocking=True).float()
+        final_T = _link.to_device(np.ascontiguousarray(frame.final_T, dtype=np.float64), dev).float()
+        last_idx = _link.to_device(np.ascontiguousarray(frame.last_idx, dtype=np.int64), dev).int()
+        dL_dev = _link.to_device(dL, dev).float()
     cam = camera_struct(view, frame.s)
     fds = _reusable(eng, ds, cam, frame)
     if fds is not None:
@@ -162,37 +160,38 @@ def _pipelined_backward(scene, view, frame, dL, chunks: int | None = None):
     main = torch.cuda.current_stream(dev)
     up, down = _link.copy_streams(dev)
     srcs = _link.host_fields(scene, n, K)
+    pin = {f: _link.is_pinned(a) for f, a in srcs.items()}
     ds = DeviceScene(*(torch.empty_like(getattr(fds, f)) for f in _SCENE_FIELDS), fds.background, deg)
     bounds = bucket_bounds(n, chunks or _PIPE_CHUNKS, align=128)
     # host -> device in the order the device needs it: dL, the scene chunk by
     # chunk, the frame's final_T / last_idx (only for the final comparison)
     up.wait_stream(main)
-    ev_up = []
     with torch.cuda.stream(up):
-        # dL first: the replay needs only it (it runs on the forward's own
-        # final_T / last_idx, which the frame's are compared with at the end)
-        dL_dev = torch.from_numpy(dL).to(dev, non_blocking=True).float()
+        # the replay needs only dL (it runs on the forward's own final_T /
+        # last_idx, which the frame's are compared with at the end)
+        dL_dev = _link.to_device(dL, dev).float()
         ev_dl = torch.cuda.Event()
         ev_dl.record(up)
-        for a, b in bounds:
-            _link.upload_rows(ds, srcs, a, b, dev)
+
+    def upload(a, b):
+        with torch.cuda.stream(up):
+            _link.upload_rows(ds, srcs, a, b, dev, pin)
             ev = torch.cuda.Event()
             ev.record(up)
-            ev_up.append(ev)
-        final_T = torch.from_numpy(np.ascontiguousarray(frame.final_T, dtype=np.float64)).to(
-            dev, non_blocking=True).float()
-        last_idx = torch.from_numpy(np.ascontiguousarray(frame.last_idx, dtype=np.int64)).to(
-            dev, non_blocking=True).int()
-        ev_frame = torch.cuda.Event()
-        ev_frame.record(up)
+        return ev
+
+    # pinned sources: every chunk queued at once, before the replay (the link
+    # is the critical path and must not wait for the host); pageable: one
+    # chunk at a time, each after the device work queued so far
+    landed = [upload(a, b) for a, b in bounds] if all(pin.values()) else None
     main.wait_event(ev_dl)
     dL_dev.record_stream(main)
     g = eng.backward(fds, view, frame.s, eng.final_T, eng.last_idx, dL_dev, rebin=False, deterministic=True,
                      projection=False)
     outs = {f: _link.host_empty(getattr(g, "d_eta" if f in ("d_beta", "d_dir") else f).shape, torch.float64)
             for f in _OUT_FIELDS}
-    for (a, b), ev in zip(bounds, ev_up):
-        main.wait_event(ev)
+    for i, (a, b) in enumerate(bounds):
+        main.wait_event(landed[i] if landed is not None else upload(a, b))
         eng.projection_backward(ds, cam, g, rows=(a, b))
         eta = g.d_eta[a:b].to(torch.float64)
         pieces = {f: (eta if f in ("d_beta", "d_dir") else getattr(g, f)[a:b].to(torch.float64))
@@ -205,6 +204,11 @@ def _pipelined_backward(scene, view, frame, dL, chunks: int | None = None):
                 outs[f][a:b].copy_(t, non_blocking=True)
         for t in pieces.values():
             t.record_stream(down)
+    with torch.cuda.stream(up):
+        final_T = _link.to_device(np.ascontiguousarray(frame.final_T, dtype=np.float64), dev).float()
+        last_idx = _link.to_device(np.ascontiguousarray(frame.last_idx, dtype=np.int64), dev).int()
+        ev_frame = torch.cuda.Event()
+        ev_frame.record(up)
     main.wait_event(ev_frame)
     for t in (final_T, last_idx):
         t.record_stream(main)

@@ -15,6 +15,7 @@ import numpy as np
 import torch
 
 from ..camera import CameraView, to_opencv
+from .. import _native as N
 from ..engine import DeviceScene, camera_struct, default_engine, dropin_serialized
 from . import _link, backend
 
@@ -81,12 +82,24 @@ def _speculative_forward(eng, scene, view, s):
     srcs = _link.host_fields(scene, n, fds.K)
     ds = DeviceScene(*(torch.empty_like(getattr(fds, f)) for f in _link.SCENE_FIELDS), fds.background,
                      fds.sh_degree)
-    up.wait_stream(main)
-    with torch.cuda.stream(up):
-        _link.upload_rows(ds, srcs, 0, n, dev)
-        ev_up = torch.cuda.Event()
-        ev_up.record(up)
-    f = eng.forward(fds, view, s)
+    # pinned sources: the upload is queued first (it is the critical path);
+    # pageable ones block the host while they copy, so the speculative frame
+    # (no host round trip inside it) and its download are queued before them
+    pin = {f: _link.is_pinned(a) for f, a in srcs.items()}
+    pinned = all(pin.values())
+    ready = torch.cuda.Event()  # ds's memory is free on the main stream from here on
+    ready.record(main)
+
+    def upload():
+        up.wait_event(ready)
+        with torch.cuda.stream(up):
+            _link.upload_rows(ds, srcs, 0, n, dev, pin)
+            ev = torch.cuda.Event()
+            ev.record(up)
+        return ev
+
+    ev_up = upload() if pinned else None
+    f = eng.forward(fds, view, s, sync=False)
     srcs_dev = [f.color.to(torch.float64), f.final_T.to(torch.float64), f.n_contrib,
                 f.last_idx.to(torch.int64)]
     outs = [_link.host_empty(t.shape, t.dtype) for t in srcs_dev]
@@ -98,18 +111,27 @@ def _speculative_forward(eng, scene, view, s):
             o.copy_(t, non_blocking=True)
     for t in srcs_dev:
         t.record_stream(down)
+    if ev_up is None:
+        ev_up = upload()
     main.wait_event(ev_up)
-    differs = bool(_link.scenes_differ(ds, fds).item())  # synchronises the main stream
+    diff = _link.scenes_differ(ds, fds)
+    try:  # one read-back (synchronises the main stream): M and the comparison
+        m, (d,) = eng.instances(diff)
+        differs = d != 0.0
+    except N.NativeError:  # the speculative frame overflowed the instance buffers
+        differs, m = bool(diff.item()), None
     down.synchronize()
-    if differs:
-        eng._spec_skip = _SPEC_BACKOFF
-        f = eng.forward(ds, view, s)
-        eng._dropin_state = (ds, bytes(camera_struct(view, s)), float(s), eng._bin_gen)
+    if differs or m is None:
+        if differs:
+            eng._spec_skip = _SPEC_BACKOFF
+        keep = ds if differs else fds
+        f = eng.forward(keep, view, s)
+        eng._dropin_state = (keep, bytes(camera_struct(view, s)), float(s), eng._bin_gen)
         return frame_to_host(f)
     eng._dropin_state = (fds, bytes(camera_struct(view, s)), float(s), eng._bin_gen)
     c, t, nc, li = (o.numpy() for o in outs)
     return FrameBundle(color=c, final_T=t, n_contrib=nc, last_idx=li, width=f.width, height=f.height,
-                       n_primitives=f.n_primitives, n_instances=f.n_instances, s=f.s)
+                       n_primitives=f.n_primitives, n_instances=m, s=f.s)
 
 
 @dropin_serialized

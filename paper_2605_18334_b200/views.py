@@ -186,11 +186,12 @@ def render_views_host(scene, views, s: float = 0.3, lanes: int = 4, u8: bool = F
     main = torch.cuda.current_stream(dev)
     up, _ = _link.copy_streams(dev)
     srcs = _link.host_fields(scene, n, prev.K)
+    pin = {f: _link.is_pinned(a) for f, a in srcs.items()}
     ds = DeviceScene(*(torch.empty_like(getattr(prev, f)) for f in _link.SCENE_FIELDS), prev.background,
                      prev.sh_degree)
     up.wait_stream(main)
     with torch.cuda.stream(up):
-        _link.upload_rows(ds, srcs, 0, n, dev)
+        _link.upload_rows(ds, srcs, 0, n, dev, pin)
         landed = torch.cuda.Event()
         landed.record(up)
     host = _views_batch(engines, prev, views, s, u8)

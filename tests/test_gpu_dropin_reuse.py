@@ -151,3 +151,32 @@ def test_speculative_forward_is_exact():
         dL = np.random.default_rng(5).normal(size=(80, 112, 3))
         fr = render_forward(moved, views[1])
         _same(render_backward(moved, views[1], fr, dL), _full(moved, views[1], fr, dL))
+
+
+def test_pageable_and_pinned_sources_agree():
+    """Caller arrays in ordinary (pageable) host memory go through the pinned
+    staging ring (hostlink.to_device) in pieces; results equal those from
+    pinned arrays, including arrays larger than one staging buffer."""
+    import torch
+    from paper_2605_18334_b200 import hostlink
+    a = np.random.default_rng(3).normal(size=(3 * hostlink.STAGE_BYTES // 8 + 12345,))
+    d = hostlink.to_device(a, torch.device("cuda"))
+    assert np.array_equal(d.cpu().numpy(), a)
+    rng = np.random.default_rng(41)
+    scene = fp32_round(random_scene(rng, 1800, sh_degree=3))
+    view = random_view(rng, 100, 70)
+    dL = np.random.default_rng(6).normal(size=(70, 100, 3))
+
+    def pinned(x):
+        t = torch.empty(x.shape, dtype=torch.float64, pin_memory=True)
+        t.numpy()[...] = x
+        return t.numpy()
+    pscene = type(scene)(*(pinned(getattr(scene, f)) for f in scene.ARRAY_FIELDS), background=scene.background,
+                         sh_degree=scene.sh_degree)
+    default_engine()._dropin_state = None
+    fa = render_forward(scene, view)
+    ga = render_backward(scene, view, fa, dL)
+    fb = render_forward(pscene, view)               # speculative on the pageable upload's copy
+    gb = render_backward(pscene, view, fb, pinned(dL))
+    _frame_same(fa, fb)
+    _same(ga, gb)

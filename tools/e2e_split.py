@@ -32,9 +32,12 @@ def main():
         RB._PIPE_CHUNKS = int(sys.argv[1])
 
     scene, view, dL = bench.workload()
-    ps = Scene(*(pinned(getattr(scene, f)) for f in Scene.ARRAY_FIELDS), background=scene.background,
-               sh_degree=scene.sh_degree)
-    pdL = pinned(dL)
+    if os.environ.get("PAGEABLE"):  # the caller's own numpy arrays, as a reference user passes them
+        ps, pdL = scene, dL
+    else:
+        ps = Scene(*(pinned(getattr(scene, f)) for f in Scene.ARRAY_FIELDS), background=scene.background,
+                   sh_degree=scene.sh_degree)
+        pdL = pinned(dL)
     res = {"fwd": [], "bwd": [], "h2d_528MB": [], "d2h_528MB": [], "both_528MB": []}
     for it in range(8):
         torch.cuda.synchronize()
