@@ -46,11 +46,32 @@ def host_empty(shape, dtype) -> torch.Tensor:
         return torch.empty(shape, dtype=dtype)
 
 
-def upload_rows(ds, srcs: dict, a: int, b: int, dev, pinned: dict | None = None) -> None:
-    """Rows [a, b) of every field into `ds` on the current stream (fp64 in
-    flight, converted on the device where `ds` keeps fp32)."""
+def upload_rows(ds, srcs: dict, a: int, b: int, dev, pinned: dict | None = None) -> list:
+    """Host -> device copies of rows [a, b) of every field, queued on the
+    current stream: fp64 fields straight into `ds`, the fields `ds` keeps in
+    fp32 as fp64 device temporaries.  Returns the (destination, temporary)
+    conversions, which the caller runs on its compute stream once the
+    upload's event has passed -- a conversion kernel queued on the copy
+    stream would wait there for SM slots behind the compute stream's kernels
+    and hold up the copies behind it."""
+    conv = []
     for f in SCENE_FIELDS:
-        getattr(ds, f)[a:b].copy_(to_device(srcs[f][a:b], dev, None if pinned is None else pinned[f]))
+        dst, src = getattr(ds, f)[a:b], srcs[f][a:b]
+        pin = is_pinned(src) if pinned is None else pinned[f]
+        if dst.dtype == torch.float64 and pin:
+            dst.copy_(torch.from_numpy(src), non_blocking=True)
+        elif dst.dtype == torch.float64:
+            dst.copy_(to_device(src, dev, False))  # device-to-device: a copy-engine transfer
+        else:
+            conv.append((dst, to_device(src, dev, pin)))
+    return conv
+
+
+def finish_rows(conv: list, stream) -> None:
+    """Run upload_rows' conversions on `stream` (current stream context)."""
+    for dst, tmp in conv:
+        dst.copy_(tmp)
+        tmp.record_stream(stream)
 
 
 def scenes_differ(a, b) -> torch.Tensor:

@@ -175,10 +175,10 @@ def _pipelined_backward(scene, view, frame, dL, chunks: int | None = None):
 
     def upload(a, b):
         with torch.cuda.stream(up):
-            _link.upload_rows(ds, srcs, a, b, dev, pin)
+            conv = _link.upload_rows(ds, srcs, a, b, dev, pin)
             ev = torch.cuda.Event()
             ev.record(up)
-        return ev
+        return ev, conv
 
     # pinned sources: every chunk queued at once, before the replay (the link
     # is the critical path and must not wait for the host); pageable: one
@@ -191,7 +191,9 @@ def _pipelined_backward(scene, view, frame, dL, chunks: int | None = None):
     outs = {f: _link.host_empty(getattr(g, "d_eta" if f in ("d_beta", "d_dir") else f).shape, torch.float64)
             for f in _OUT_FIELDS}
     for i, (a, b) in enumerate(bounds):
-        main.wait_event(landed[i] if landed is not None else upload(a, b))
+        ev, conv = landed[i] if landed is not None else upload(a, b)
+        main.wait_event(ev)
+        _link.finish_rows(conv, main)
         eng.projection_backward(ds, cam, g, rows=(a, b))
         eta = g.d_eta[a:b].to(torch.float64)
         pieces = {f: (eta if f in ("d_beta", "d_dir") else getattr(g, f)[a:b].to(torch.float64))

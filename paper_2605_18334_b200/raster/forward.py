@@ -90,10 +90,12 @@ def _speculative_forward(eng, scene, view, s):
     ready = torch.cuda.Event()  # ds's memory is free on the main stream from here on
     ready.record(main)
 
+    conv = []
+
     def upload():
         up.wait_event(ready)
         with torch.cuda.stream(up):
-            _link.upload_rows(ds, srcs, 0, n, dev, pin)
+            conv.extend(_link.upload_rows(ds, srcs, 0, n, dev, pin))
             ev = torch.cuda.Event()
             ev.record(up)
         return ev
@@ -114,6 +116,7 @@ def _speculative_forward(eng, scene, view, s):
     if ev_up is None:
         ev_up = upload()
     main.wait_event(ev_up)
+    _link.finish_rows(conv, main)
     diff = _link.scenes_differ(ds, fds)
     try:  # one read-back (synchronises the main stream): M and the comparison
         m, (d,) = eng.instances(diff)

@@ -191,11 +191,12 @@ def render_views_host(scene, views, s: float = 0.3, lanes: int = 4, u8: bool = F
                      prev.sh_degree)
     up.wait_stream(main)
     with torch.cuda.stream(up):
-        _link.upload_rows(ds, srcs, 0, n, dev, pin)
+        conv = _link.upload_rows(ds, srcs, 0, n, dev, pin)
         landed = torch.cuda.Event()
         landed.record(up)
     host = _views_batch(engines, prev, views, s, u8)
     main.wait_event(landed)
+    _link.finish_rows(conv, main)
     if bool(_link.scenes_differ(ds, prev).item()):
         eng._host_batch_scene = ds
         host = _views_batch(engines, ds, views, s, u8)

@@ -1,6 +1,6 @@
-"""Timeline of one drop-in render_backward (config 2, pinned host arrays)
-from torch.profiler: copies and kernels per stream, ms from the first
-event: python tools/e2e_trace.py"""
+"""Timeline of one drop-in render_forward + render_backward (config 2,
+pinned host arrays) from torch.profiler: copies and kernels per stream, ms
+from the first event: python tools/e2e_trace.py [forward|backward]"""
 
 from __future__ import annotations
 
@@ -32,11 +32,16 @@ def main():
     for _ in range(3):
         fr = render_forward(ps, view)
         render_backward(ps, view, fr, pdL)
+    which = sys.argv[1] if len(sys.argv) > 1 else "backward"
     fr = render_forward(ps, view)
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
-        render_backward(ps, view, fr, pdL)
+        if which == "forward":
+            render_forward(ps, view)
+        else:
+            render_backward(ps, view, fr, pdL)
         torch.cuda.synchronize()
+    print(f"== render_{which}")
     evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
     cpu = [e for e in prof.events() if e.device_type.name == "CPU" and e.name in ("render_backward",)]
     t0 = min(e.time_range.start for e in evs)
