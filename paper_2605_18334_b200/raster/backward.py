@@ -218,6 +218,9 @@ def _pipelined_backward(scene, view, frame, dL, chunks: int | None = None):
     scene_diff = _link.scenes_differ(ds, fds)
     differs = bool((scene_diff | frame_diff).item())  # synchronises the main stream
     down.synchronize()
+    eng._spec_stats = st2 = getattr(eng, "_spec_stats", {"forward_hits": 0, "forward_misses": 0,
+                                                         "backward_hits": 0, "backward_misses": 0})
+    st2["backward_misses" if differs else "backward_hits"] += 1
     if differs:
         m = eng.project_and_bin(ds, cam)
         if m != frame.n_instances:

@@ -124,6 +124,9 @@ def _speculative_forward(eng, scene, view, s):
     except N.NativeError:  # the speculative frame overflowed the instance buffers
         differs, m = bool(diff.item()), None
     down.synchronize()
+    eng._spec_stats = st2 = getattr(eng, "_spec_stats", {"forward_hits": 0, "forward_misses": 0,
+                                                           "backward_hits": 0, "backward_misses": 0})
+    st2["forward_misses" if (differs or m is None) else "forward_hits"] += 1
     if differs or m is None:
         if differs:
             eng._spec_skip = _SPEC_BACKOFF
