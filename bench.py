@@ -88,6 +88,10 @@ def _load_reference():
         from skewsplat.raster.forward import render_forward
         if backend.active_backend() != "cython":
             return None
+        # every host core: torchrun exports OMP_NUM_THREADS=1 to its ranks,
+        # which the reference's OpenMP runtime would otherwise obey
+        from skewsplat.raster import _core
+        _core.set_num_threads(cpu_cores())
         return render_forward, render_backward
     except Exception:  # noqa: BLE001
         return None
@@ -237,6 +241,23 @@ def view_batch(eng, rank, world, local, barrier, max_over_ranks, reps=3):
             "parallelism": f"views sharded x{world} (contiguous blocks, no collective), {len(lanes)} view lanes"}
 
 
+# Test hook, never a bench number: every rank on GPU 0 over gloo, so the
+# multi-rank flow (spawn, barriers, max over ranks, rank-0 line, view
+# sharding) runs on a one-GPU box.  The line then carries "shared_gpu_test".
+SHARED_GPU = os.environ.get("SSG_BENCH_SHARED_GPU") == "1"
+
+
+def device_index() -> int:
+    return 0 if SHARED_GPU else int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def init_dist(torch, dist, local: int) -> None:
+    if SHARED_GPU:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+
 def spawn(args) -> int:
     """`--gpus N` without a torchrun environment: launch N ranks (one per
     GPU) through torch.distributed.run on 127.0.0.1 and pass the exit code
@@ -245,7 +266,7 @@ def spawn(args) -> int:
 
     import torch
     n_dev = torch.cuda.device_count()
-    if n_dev < args.gpus:
+    if n_dev < args.gpus and not SHARED_GPU:
         print(json.dumps({"error": f"--gpus {args.gpus} needs {args.gpus} GPUs; {n_dev} visible"}))
         return 2
     with socket.socket() as sk:
@@ -333,7 +354,7 @@ def main():
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = device_index()
     config = {"workload": ("config 3: G3 (G2 with a seeded 50% skew-free, tied-opacity half)"
                            if args.config == 3 else "config 2: G2") +
                           " synthetic 1M skew Gaussians (SH3, fp32-rounded), 1920x1080, "
@@ -351,7 +372,7 @@ def main():
     import torch.distributed as dist
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(torch, dist, local)
     from paper_2605_18334_b200.engine import DeviceScene, Engine
     from paper_2605_18334_b200.raster import render_backward, render_forward
 
@@ -607,6 +628,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(scene, view, dL_host, args.cpu_k, args.cpu_reps)
     if rank == 0:
+        if SHARED_GPU:
+            result["shared_gpu_test"] = True
         print(json.dumps(result))
     if world > 1:
         dist.destroy_process_group()

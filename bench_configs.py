@@ -34,7 +34,7 @@ def _setup(local, world):
     import torch.distributed as dist
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        B.init_dist(torch, dist, local)
     return torch, dist
 
 
@@ -209,6 +209,8 @@ def config4(args, rank, world, local):
         result["cpu_baseline"] = {"value": 1.0 / t, "unit": "views/s", "cores": B.cpu_cores(), "kind": kind,
                                   "sample": desc}
     if rank == 0:
+        if B.SHARED_GPU:
+            result["shared_gpu_test"] = True
         print(json.dumps(result))
     if world > 1:
         dist.destroy_process_group()
@@ -366,6 +368,8 @@ def config5(args, rank, world, local):
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = _cpu_train_sample(start, views[0], targets[0].cpu().numpy(), 64)
     if rank == 0:
+        if B.SHARED_GPU:
+            result["shared_gpu_test"] = True
         print(json.dumps(result))
     if world > 1:
         dist.destroy_process_group()
@@ -374,7 +378,7 @@ def config5(args, rank, world, local):
 def main(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = B.device_index()
     if args.impl == "reference":
         if rank == 0:
             print(json.dumps({"impl": "reference", "unavailable":
