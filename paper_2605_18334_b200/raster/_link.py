@@ -14,6 +14,23 @@ _INT_VIEW = {torch.float64: torch.int64, torch.float32: torch.int32}
 _STREAMS: dict = {}
 
 
+def drain_on_error(dev):
+    """Context for a speculative call: if it raises, wait for the copy
+    streams before the exception propagates (their transfers target buffers
+    the unwinding frees)."""
+    import contextlib
+
+    @contextlib.contextmanager
+    def ctx():
+        try:
+            yield
+        except BaseException:
+            for st in copy_streams(dev):
+                st.synchronize()
+            raise
+    return ctx()
+
+
 def copy_streams(dev) -> tuple:
     """(host->device, device->host) streams of a device, created once."""
     key = str(dev)

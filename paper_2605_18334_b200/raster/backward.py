@@ -262,7 +262,8 @@ def render_backward(scene, view: CameraView, frame, dL_dpixels: np.ndarray,
     backend.active_backend(backend_name)
     view = to_opencv(view)
     dL = _validate(scene, view, frame, dL_dpixels)
-    bundle = _pipelined_backward(scene, view, frame, dL)
+    with _link.drain_on_error(default_engine().device):
+        bundle = _pipelined_backward(scene, view, frame, dL)
     if bundle is not None:
         return bundle
     eng, g = _device_backward(scene, view, frame, dL)

@@ -148,7 +148,8 @@ def render_forward(scene, view: CameraView, s: float = 0.3,
     if view.width > MAX_IMAGE_DIM or view.height > MAX_IMAGE_DIM:
         raise ValueError("image dimension overflow")
     eng = default_engine()
-    fr = _speculative_forward(eng, scene, view, s)
+    with _link.drain_on_error(eng.device):
+        fr = _speculative_forward(eng, scene, view, s)
     if fr is not None:
         return fr
     ds = DeviceScene.from_host(scene, eng.device)
