@@ -4,6 +4,8 @@ of two device scenes (the check that makes a speculative result exact)."""
 
 from __future__ import annotations
 
+import contextlib
+
 import numpy as np
 import torch
 
@@ -14,21 +16,17 @@ _INT_VIEW = {torch.float64: torch.int64, torch.float32: torch.int32}
 _STREAMS: dict = {}
 
 
+@contextlib.contextmanager
 def drain_on_error(dev):
     """Context for a speculative call: if it raises, wait for the copy
     streams before the exception propagates (their transfers target buffers
     the unwinding frees)."""
-    import contextlib
-
-    @contextlib.contextmanager
-    def ctx():
-        try:
-            yield
-        except BaseException:
-            for st in copy_streams(dev):
-                st.synchronize()
-            raise
-    return ctx()
+    try:
+        yield
+    except BaseException:
+        for st in copy_streams(dev):
+            st.synchronize()
+        raise
 
 
 def copy_streams(dev) -> tuple:

@@ -7,7 +7,8 @@ cooperative one below 2M keys via the binning, the onesweep one through the
 sort hook) and the counting scatter; the view-batched projection with its
 lanes (priority streams), the pipelined + bucketed training step (step-value
 kernel, range-wise projection backward / Adam) and the deterministic
-backward's half batches."""
+backward's half batches; the drop-in render_forward / render_backward
+(speculative forward on the kept scene, chunked backward)."""
 
 from __future__ import annotations
 
@@ -77,6 +78,18 @@ def main():
     for it in range(3):
         tr.step(views[it], target, it, stats=stats)
     tr.flush()
+    torch.cuda.synchronize()
+    # the drop-in calls: speculative forward (kept scene), chunked backward
+    # (row-range projection backward, two copy streams), a changed scene
+    from paper_2605_18334_b200.raster import render_backward, render_forward
+    dLh = np.random.default_rng(7).normal(size=(40, 72, 3))
+    for sc in (scene, scene, scene.copy()):
+        fr = render_forward(sc, view)
+        render_backward(sc, view, fr, dLh)
+    moved = scene.copy()
+    moved.sh[-1, 0, 0] += 0.5
+    fr = render_forward(moved, view)
+    render_backward(moved, view, fr, dLh)
     torch.cuda.synchronize()
     print("sanitize_small: ok")
 
