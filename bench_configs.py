@@ -362,8 +362,10 @@ def config5(args, rank, world, local):
         "e2e": {"value": world / e2e_s, "unit": "views/s", "h2d_bytes_per_step": H4 * W4 * 12,
                 "d2h_bytes_per_step": 4, "path": "training_step with the target image copied from pinned "
                                                  "host memory and the loss read back each step"},
-        # per step: the frame's 13, image loss 2, regularizer 1, Adam 9 (rowcheck, 7 fields, renorm)
-        "gpu_launches": (B.LAUNCHES_PER_FRAME + 12) * args.steps,
+        # per step (tools/count_launches.py, torch.profiler): the frame's 22, image loss 2,
+        # regularizer value + gradients 2, step value 1, statistics 1, Adam 9 (row check, 7
+        # fields, quaternion renorm) = 36
+        "gpu_launches": (B.LAUNCHES_PER_FRAME + 14) * args.steps,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = _cpu_train_sample(start, views[0], targets[0].cpu().numpy(), 64)
