@@ -363,8 +363,8 @@ def config5(args, rank, world, local):
                 "d2h_bytes_per_step": 4, "path": "training_step with the target image copied from pinned "
                                                  "host memory and the loss read back each step"},
         # per step (tools/count_launches.py, torch.profiler): the frame's 22, image loss 2,
-        # regularizer value + gradients 2, step value 1, statistics 1, Adam 9 (row check, 7
-        # fields, quaternion renorm) = 36
+        # regularizer value + gradients 2, step value 1, Adam 9 (row check, 7 fields,
+        # quaternion renorm) = 36
         "gpu_launches": (B.LAUNCHES_PER_FRAME + 14) * args.steps,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
