@@ -360,6 +360,7 @@ class Trainer:
         self._pending = None
         self._skip_dev = torch.zeros(1, dtype=torch.int32, device=eng.device)
         self._skip_host = torch.zeros(1, dtype=torch.int32, pin_memory=True) if pipelined else None
+        self._loss_host = torch.zeros(1, dtype=torch.float64, pin_memory=True) if pipelined else None
         self.skipped_steps = 0  # pipelined steps skipped on the device (non-finite loss)
         if pipelined:
             adam._trainer = self  # densify_and_prune flushes through it
@@ -369,6 +370,21 @@ class Trainer:
         if key not in self._loss:
             self._loss[key] = ImageLoss(W, H, self.cfg.lambda_ssim, self.eng.device)
         return self._loss[key]
+
+    def loss_value(self) -> float:
+        """The last pipelined step's loss on the host.  Waits only for that
+        step's forward, loss and flag (read back right after the loss
+        kernel), not for its backward and update, which keep running; a
+        step flagged for a re-run (instance overflow) is resolved first and
+        its re-run's loss returned."""
+        if self._pending is None:
+            raise RuntimeError("no pipelined step in flight")
+        ev, _, loss = self._pending
+        ev.synchronize()
+        if int(self._skip_host[0]) == 2:
+            self.flush()
+            return float(loss)
+        return float(self._loss_host[0])
 
     def flush(self) -> None:
         """Resolve the last pipelined step (see the class docstring)."""
@@ -446,6 +462,7 @@ class Trainer:
         # read the flag back now: waiting for it at the next step then waits
         # for this step's forward and loss only, not for its backward + Adam
         self._skip_host.copy_(self._skip_dev, non_blocking=True)
+        self._loss_host.copy_(v, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
         if stats is not None:

@@ -209,3 +209,17 @@ def test_host_targets_equal_device_targets(pipelined):
     for f in FIELDS:
         assert torch.equal(getattr(a[0], f), getattr(b[0], f)), f
     np.testing.assert_allclose(a[3], b[3], rtol=1e-12)  # fp64 atomic loss sums: order-dependent ulps
+
+
+def test_loss_value_equals_the_step_loss():
+    """Trainer.loss_value (the pinned read-back right after the loss kernel)
+    equals the step's returned device loss."""
+    start, views, targets = _setup(seed=8, n=700)
+    eng = Engine()
+    ds = DeviceScene.from_host(start)
+    tr = Trainer(eng, ds, DeviceAdam(ds), pipelined=True)
+    for it in range(4):
+        loss, _ = tr.step(views[it % 3], targets[it % 3], it)
+        got = tr.loss_value()
+        assert got == float(loss.item())
+    tr.flush()
