@@ -180,3 +180,30 @@ def test_pageable_and_pinned_sources_agree():
     gb = render_backward(pscene, view, fb, pinned(dL))
     _frame_same(fa, fb)
     _same(ga, gb)
+
+
+def test_speculative_forward_instance_overflow_falls_back():
+    """A speculative frame runs without the instance-count read-back; a
+    view needing more instances than the buffers hold (a much larger image
+    after a small one) overflows, is detected by the final read-back and
+    rendered again synchronised: the frame equals a fresh render."""
+    rng = np.random.default_rng(51)
+    scene = fp32_round(random_scene(rng, 3000, sh_degree=1))
+    small = random_view(rng, 480, 320, dist=40.0)   # far away: few instances
+    big = random_view(rng, 480, 320, dist=2.5)      # same image size, close: many more
+    eng = default_engine()
+    eng._dropin_state = None
+    eng.capacity = 0  # fresh buffers sized by the small frame
+    eng._bins_key = None
+    render_forward(scene, small)
+    eng._spec_skip = 0
+    hits = dict(getattr(eng, "_spec_stats", {}))
+    got = render_forward(scene, big)
+    st = eng._spec_stats
+    assert st["forward_misses"] == hits.get("forward_misses", 0) + 1     # overflow: redone
+    assert eng._spec_skip == 0                                          # the scene itself was equal
+    eng._dropin_state = None
+    fresh = render_forward(scene, big)
+    _frame_same(got, fresh)
+    dL = np.random.default_rng(2).normal(size=(320, 480, 3))
+    _same(render_backward(scene, big, got, dL), _full(scene, big, got, dL))
