@@ -129,20 +129,41 @@ def save_trajectory(path, views) -> None:
 @dropin_serialized
 def render_trajectory(scene, trajectory, out_dir, s: float = 0.3) -> list[str]:
     """trajectory.py:12-31: one PNG per entry, names zero-padded to
-    max(4, digits of the last index); the scene is uploaded once and every
-    frame is quantised on the device."""
+    max(4, digits of the last index).  The scene is uploaded once; runs of
+    up to 64 consecutive views of one image size render as one device batch
+    (views.render_views: one projection pass per 8 views), are quantised on
+    the device and come back as one copy, and the PNG encoding -- the
+    host-bound part -- runs on a thread pool (zlib releases the GIL) while
+    the next batch renders.  Same files, names and bytes as one view at a
+    time."""
+    from concurrent.futures import ThreadPoolExecutor
+
     from PIL import Image
+
+    from .views import render_views
     if not isinstance(trajectory, list):
         trajectory = load_trajectory(trajectory)
     os.makedirs(out_dir, exist_ok=True)
     eng = default_engine()
     ds = _device_scene(scene, eng.device)
     width = max(4, len(str(max(len(trajectory) - 1, 0))))
-    paths = []
-    for i, view in enumerate(trajectory):
-        f = eng.forward(ds, view, s)
-        px = quantize_u8_device(f.color).cpu().numpy()
-        path = os.path.join(out_dir, f"{i:0{width}d}.png")
+    paths = [os.path.join(out_dir, f"{i:0{width}d}.png") for i in range(len(trajectory))]
+
+    def save(px, path):
         Image.fromarray(px, mode="RGB").save(path, format="PNG")
-        paths.append(path)
+
+    with ThreadPoolExecutor(max_workers=max(1, min(8, os.cpu_count() or 1))) as pool:
+        pending = []
+        i = 0
+        while i < len(trajectory):
+            size = (int(trajectory[i].width), int(trajectory[i].height))
+            j = i + 1
+            while (j < len(trajectory) and j - i < 64
+                   and (int(trajectory[j].width), int(trajectory[j].height)) == size):
+                j += 1
+            px = quantize_u8_device(render_views(ds, trajectory[i:j], s, engine=eng)).cpu().numpy()
+            pending += [pool.submit(save, px[k], paths[i + k]) for k in range(j - i)]
+            i = j
+        for fut in pending:
+            fut.result()
     return paths

@@ -77,3 +77,23 @@ def test_trajectory_pngs_match_reference(tmp_path):
     batch = render_views_u8(scene, views)
     assert tuple(batch.shape) == (3, 48, 64, 3)
     _close_bytes(batch[0].cpu().numpy().tobytes(), D.quantize_u8(D.load_image(theirs[0])).tobytes())
+
+
+def test_trajectory_batches_mixed_sizes_equal_per_view(tmp_path):
+    """render_trajectory renders runs of one image size as device batches
+    and encodes on a thread pool: files, names and pixels equal a per-view
+    render, across a change of image size."""
+    from PIL import Image
+
+    from paper_2605_18334_b200.engine import DeviceScene, Engine
+    from paper_2605_18334_b200.serving import quantize_u8_device
+    rng = np.random.default_rng(9)
+    scene = fp32_round(random_scene(rng, 500, sh_degree=1))
+    views = [random_view(rng, 64, 48) for _ in range(5)] + [random_view(rng, 80, 40) for _ in range(4)] + \
+        [random_view(rng, 64, 48)]
+    paths = render_trajectory(scene, views, tmp_path / "t")
+    assert [os.path.basename(p) for p in paths] == [f"{i:04d}.png" for i in range(len(views))]
+    eng, ds = Engine(), DeviceScene.from_host(scene)
+    for p, v in zip(paths, views):
+        ref = quantize_u8_device(eng.forward(ds, v, 0.3).color).cpu().numpy()
+        assert np.array_equal(np.asarray(Image.open(p).convert("RGB")), ref)
